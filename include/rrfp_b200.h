@@ -1,0 +1,221 @@
+/*
+ * rrfp_b200.h -- C ABI of the B200-native RRFP pipeline runtime
+ * (arXiv 2605.18750).  Plain pointers and sizes only; no torch types.
+ *
+ * Every entry point replaces a function of the reference's Python
+ * scheduling path (/root/reference/pkg/src/rrfp); the citation is given
+ * per function.  All functions return 0 on success and a negative
+ * RRFP_E_* code on failure; rrfp_last_error() returns a thread-local
+ * message.  No C++ exception crosses this boundary.
+ *
+ * Task encoding (rrfp_task_t, uint32):
+ *   bits 0-1  direction (0 = B, 1 = F, 2 = W; the reference's
+ *             DISPATCH_RANK order, workload.py:37-40)
+ *   bits 2-5  model chunk   (C <= 16)
+ *   bits 6-15 microbatch    (M <= 1024)
+ *   bits 16-21 stage        (N <= 32)
+ * Keys index per-stage bitmasks: key = chunk * (32*MW) + mb, MW = ceil(M/32).
+ */
+#ifndef RRFP_B200_H
+#define RRFP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RRFP_OK 0
+#define RRFP_E_INVALID -1      /* bad argument / config (ValueError in the reference) */
+#define RRFP_E_DEADLOCK -2     /* EngineDeadlockError, engine.py:62-67            */
+#define RRFP_E_WATCHDOG -3     /* LiveWatchdogError, live.py:58-63                 */
+#define RRFP_E_CUDA -4         /* CUDA runtime failure                             */
+#define RRFP_E_CAPACITY -5     /* a device ring/heap would overflow                */
+#define RRFP_E_NOGPU -6        /* no CUDA device / kernel image                    */
+
+#define RRFP_DIR_B 0
+#define RRFP_DIR_F 1
+#define RRFP_DIR_W 2
+#define RRFP_WAIT 3
+
+#define RRFP_MAX_STAGES 32
+#define RRFP_MAX_RANKS 8
+#define RRFP_MAX_CHUNKS 16
+#define RRFP_MAX_MB 1024
+#define RRFP_MAX_WORDS 128     /* bitmask words per ready set: C*MW <= 128 */
+#define RRFP_MAX_RANKED 8
+
+/* hint kinds, arbitration.py:37 HINT_KINDS */
+#define RRFP_HINT_BF 0
+#define RRFP_HINT_FB 1
+#define RRFP_HINT_BPRIO 2
+#define RRFP_HINT_FPRIO 3
+#define RRFP_HINT_BFW 4
+#define RRFP_HINT_EXTERNAL 5
+
+/* backpressure modes, arbitration.py:32-34 */
+#define RRFP_BP_NORMAL 0
+#define RRFP_BP_DRAIN 1
+#define RRFP_BP_FOCUS 2
+
+typedef uint32_t rrfp_task_t;
+
+/* HintOrder, arbitration.py:40-66. ranked_dir uses RRFP_DIR_*, ranked_desc 1 = "desc". */
+typedef struct {
+  int32_t kind;
+  int32_t n_ranked;
+  int32_t ranked_dir[RRFP_MAX_RANKED];
+  int32_t ranked_desc[RRFP_MAX_RANKED];
+} rrfp_hint;
+
+/* One (stage, rank) arbitration snapshot: StageBuffers + BackpressureState +
+ * ArbiterState + StageProgress (arbitration.py:93-229) as bitmasks. */
+typedef struct {
+  int32_t M, C, MW, decompose;     /* shape; MW = ceil(M/32), C*MW <= RRFP_MAX_WORDS */
+  int32_t admission;               /* next chunk-0 mb at stage 0, or -1 */
+  int32_t mode, focus;             /* RRFP_BP_*, focus microbatch (-1) */
+  int32_t phase;                   /* next direction to probe: RRFP_DIR_F/B, or -1 = round start */
+  uint32_t fready[RRFP_MAX_WORDS];
+  uint32_t bready[RRFP_MAX_WORDS];
+  uint32_t wpend[RRFP_MAX_WORDS];
+  uint32_t doneF[RRFP_MAX_WORDS];
+  uint32_t doneB[RRFP_MAX_WORDS];
+} rrfp_stage_state;
+
+typedef struct {
+  int32_t kind;                    /* RRFP_DIR_B/F/W or RRFP_WAIT */
+  int32_t mb, chunk;
+} rrfp_decision;
+
+/* ---- arbitration twin -------------------------------------------------- */
+
+/* arbitrate + _weight_fallback, arbitration.py:232-303.  Pure.  The same
+ * __host__ __device__ code runs inside the device dispatcher. */
+int rrfp_arbitrate(const rrfp_stage_state* st, const rrfp_hint* hint, rrfp_decision* out);
+
+/* update_backpressure, arbitration.py:188-215.  In/out on mode/focus. */
+int rrfp_update_backpressure(rrfp_stage_state* st, int32_t limit, int32_t n_f, int32_t n_b);
+
+/* ---- replay engine (virtual clock) --------------------------------------- */
+
+/* Static description of one iteration plus the host-built tables
+ * (Workload.latency + build_injection_table, CommDelay.sample, TP skew).
+ * All int64 tables are microseconds.  Index helpers:
+ *   dur  [((s*3 + dir) * KEYS) + key]          latency + injected delay
+ *   comm [((s*2 + dir) * KEYS) + key]          delay of the message SENT by task (s,dir,key), dir in {B,F}
+ *   skew [(((s*2 + dir) * KEYS) + key) * R + r] arrival skew of message TO task (s,dir,key) at rank r
+ *   fixed[s * per_stage + i]                   FIXED-mode order (rrfp_task_t)
+ * KEYS = C * MW * 32.
+ */
+typedef struct {
+  int32_t N, M, C, R, MW, decompose;
+  int32_t buffer_limit;
+  int32_t fixed_mode;              /* 0 = RRFP arbitration, 1 = fixed per-stage order */
+  int32_t per_stage;               /* tasks per stage = M*C*(2 or 3) */
+  int32_t pad0;
+  int64_t coord_cost;              /* TpGroup.coordination_round_cost */
+  rrfp_hint hint;
+} rrfp_iter_desc;
+
+/* One trace record.  kind: 0 exec, 1 send, 2 recv, 3 coord(agreed), 4 coord(deferred). */
+typedef struct {
+  int64_t t0, t1;
+  int32_t kind, stage, rank;
+  rrfp_task_t task;
+} rrfp_event;
+
+typedef struct {
+  int64_t makespan;
+  int64_t agreed, deferred;
+  int32_t status;                  /* RRFP_OK / RRFP_E_DEADLOCK / RRFP_E_CAPACITY */
+  int32_t n_events;
+  int64_t compute[RRFP_MAX_STAGES];
+  int64_t coord[RRFP_MAX_STAGES];
+  int32_t n_f[RRFP_MAX_STAGES], n_b[RRFP_MAX_STAGES], n_w[RRFP_MAX_STAGES];
+  int32_t remaining[RRFP_MAX_STAGES];
+} rrfp_replay_result;
+
+/* Device workspace bytes for one replay of this shape. */
+size_t rrfp_replay_workspace_bytes(const rrfp_iter_desc* d);
+/* Max trace records a replay of this shape can emit. */
+int32_t rrfp_replay_event_capacity(const rrfp_iter_desc* d);
+
+/* engine.run_rrfp / baselines.run_fixed semantics (engine.py:344-367,
+ * baselines.py:94-172) on the CPU, using the same __host__ __device__
+ * state machine as the device kernel.  Host pointers. */
+int rrfp_replay_host(const rrfp_iter_desc* d, const int64_t* dur, const int64_t* comm,
+                     const int64_t* skew, const rrfp_task_t* fixed,
+                     rrfp_event* events, int32_t event_cap, rrfp_replay_result* res);
+
+/* The same replay as ONE device kernel (one CTA, one thread per stage,
+ * lockstep ticks).  All table/event/workspace pointers are DEVICE
+ * pointers; res is a device pointer.  Enqueued on `stream` (cudaStream_t). */
+int rrfp_replay_device(const rrfp_iter_desc* d, const int64_t* dur, const int64_t* comm,
+                       const int64_t* skew, const rrfp_task_t* fixed, void* workspace,
+                       rrfp_event* events, int32_t event_cap, rrfp_replay_result* res,
+                       void* stream);
+
+/* ---- free-running device runtime (live.run_live replacement) ------------ */
+
+typedef struct rrfp_runtime rrfp_runtime;
+
+/* Per-stage executor description (one per (stage, rank) lane).  */
+typedef struct {
+  int32_t N, M, C, R, MW, decompose;
+  int32_t buffer_limit;
+  int32_t fixed_mode;              /* 0 = arbitrate (FREE), 1 = follow order list (FIXED / replay) */
+  int32_t per_stage;
+  int32_t stage, rank;
+  int32_t device;                  /* CUDA ordinal */
+  int32_t compute_kind;            /* 0 = spin tasks (latency table), 1 = caller body graphs */
+  int32_t trace_cap;
+  double time_scale;               /* live.run_live time_scale */
+  int64_t coord_cost_ns;
+  rrfp_hint hint;
+} rrfp_lane_desc;
+
+int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** out);
+void rrfp_runtime_destroy(rrfp_runtime* rt);
+/* Device address of this lane's inbox block (flags + visible-at stamps), to be
+ * exported to peers (same process: plain pointer; other process: CUDA IPC). */
+int rrfp_runtime_inbox(rrfp_runtime* rt, void** dev_ptr, size_t* bytes);
+/* CUDA IPC handle (64 bytes) of the inbox allocation. */
+int rrfp_runtime_inbox_ipc(rrfp_runtime* rt, void* handle64);
+/* Open a peer's IPC handle; returns a device pointer usable in this process. */
+int rrfp_ipc_open(const void* handle64, void** dev_ptr);
+/* Wire neighbours: inbox of the lanes that receive this lane's F output
+ * (next stage, all R ranks) and B output (previous stage, all R ranks), and
+ * the TP group's agreement board slots.  Pointers may be peer pointers. */
+int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst_inboxes, void* const* bwd_dst_inboxes,
+                         void* const* tp_peer_inboxes);
+/* Load host tables (per-lane): dur_ns[3*KEYS] (spin length incl. injected
+ * delay), comm_ns[2*KEYS] (flag visibility delay of sent messages),
+ * skew_ns[2*KEYS*R] (arrival skew per destination rank), fixed order. */
+int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
+                             const int64_t* skew_ns, const rrfp_task_t* fixed);
+/* Register caller-captured compute bodies (cudaGraph_t for F, B, W; W may be
+ * NULL when not decomposed).  The bodies read the current task from
+ * rrfp_runtime_task_ptr().  Must be called before the first iteration. */
+int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* graph_f, void* graph_b, void* graph_w);
+int rrfp_runtime_task_ptr(rrfp_runtime* rt, void** dev_ptr);
+/* Build (first call) and launch one iteration's executor graph on the lane's
+ * stream; epoch must increase by one per iteration. Asynchronous. */
+int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream);
+/* Wait for the lane to finish (host poll with watchdog); copies the trace. */
+int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_event* events, int32_t cap,
+                      int32_t* n_events, int64_t* t0_ns);
+int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap);
+
+/* ---- stage-compute kernel entry points (unit-test surface) ------------- */
+
+/* Synthetic spin task: busy-wait `ns` on the device (%globaltimer). */
+int rrfp_spin(int64_t ns, void* stream);
+
+const char* rrfp_last_error(void);
+int rrfp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
