@@ -973,3 +973,66 @@ def run_live(w, hint="bf", limit=32, time_scale=1.0, seed=0, jitter="J0", tp=Non
         raise DeadlockError(failure[0])
     mk = max((e[1] for e in events if e[7] == "exec"), default=0)
     return events, mk
+
+
+# ----------------------------------------------------------- validate -----
+def validate(events, w, injected=None, slack=(0, 1.0, 0), clock="virtual", scale=1.0):
+    """validate_trace, validate.py:44-132 -> list of (kind, detail) violations.
+
+    ``events`` are 8-tuples (t0, t1, stage, rank, mb, chunk, dir, kind).
+    """
+    injected = injected or {}
+    out = []
+    sc = scale if clock == "wall" else 1.0
+    lower, up_rel, up_abs = slack
+    known = set()
+    for s in range(w["N"]):
+        for mb in range(w["M"]):
+            for c in range(w["C"]):
+                for d in ((F, B, W) if w["dec"] else (F, B)):
+                    known.add((d, s, mb, c))
+    by = {}
+    cnt = {}
+    ranks = set()
+    for t0, t1, s, r, mb, c, d, kind in events:
+        if kind != "exec":
+            continue
+        if t1 < t0:
+            out.append(("malformed", f"exec ends before start at stage {s}"))
+            continue
+        t = (d, s, mb, c)
+        if d is None or t not in known:
+            out.append(("malformed", f"unknown task {t}"))
+            continue
+        rk = 0 if r is None else r
+        ranks.add(rk)
+        cnt[(t, rk)] = cnt.get((t, rk), 0) + 1
+        by[(t, rk)] = (t0, t1, s)
+    ranks = ranks or {0}
+    for t in known:
+        for rk in sorted(ranks):
+            if cnt.get((t, rk), 0) != 1:
+                out.append(("completeness", f"{task_key(t)} x{cnt.get((t, rk), 0)} rank {rk}"))
+    for (t, rk), (t0, t1, s) in sorted(by.items()):
+        exp = (w["lat"][t] + injected.get(t, 0)) * sc
+        act = t1 - t0
+        if act < exp - lower or act > exp * up_rel + up_abs:
+            out.append(("duration", f"{task_key(t)} rank {rk}: {act} vs {exp}"))
+    lanes = {}
+    for (t, rk), (t0, t1, s) in by.items():
+        lanes.setdefault((s, rk), []).append((t0, t1, t))
+    for key, evs in sorted(lanes.items()):
+        evs.sort()
+        for a, b in zip(evs, evs[1:]):
+            if b[0] < a[1]:
+                out.append(("serialization", f"{key}: {task_key(a[2])} overlaps {task_key(b[2])}"))
+    eps = 2 if clock == "wall" else 1e-9
+    for src, dst, kind in task_graph(w):
+        delay = comm_delay_sample(w["comm"], src, dst, kind) * sc
+        for rk in sorted(ranks):
+            a, b = by.get((src, rk)), by.get((dst, rk))
+            if a is None or b is None:
+                continue
+            if b[0] < a[1] + delay - eps:
+                out.append(("precedence", f"{kind} {task_key(src)}->{task_key(dst)} rank {rk}"))
+    return out

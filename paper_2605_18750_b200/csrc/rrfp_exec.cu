@@ -1,0 +1,753 @@
+// rrfp_exec.cu -- the free-running device runtime that replaces live.run_live
+// (/root/reference/pkg/src/rrfp/live.py:111-523).
+//
+// One *lane* = one (stage, TP rank) executor on one GPU.  Per iteration the
+// lane runs ONE CUDA graph, launched once by the host:
+//
+//   init ─► WHILE(h_while) { dispatch ─► SWITCH(h_switch){B-body, F-body, W-body} ─► complete } ─► final
+//
+// * dispatch  (K2+K3, and K4 for TP): one warp polls the lane's inbox flags
+//   (ld.acquire.sys), ballots them into ready bitmasks, runs the shared
+//   __host__ __device__ arbiter (rrfp_core.cuh) and selects the body with
+//   cudaGraphSetConditional -- no host round trip per task.
+//   live.py:_worker/_resolve_round/_commit_locked (331-421, 246-297).
+// * bodies    caller compute graphs (GPT stage F/B/W) or synthetic spins of
+//   the latency table (live.py:388-390 semantics, time_scale applied).
+// * complete  (K1 + K11 + K12): optional jitter pad, completion bookkeeping
+//   (live._complete_locked 299-329), then the send: the payload was already
+//   written into the receiver's mailbox by the body; here the lane
+//   publishes visible-at stamp + epoch flag with st.release.sys into every
+//   destination rank's inbox (live._sender/_receiver 203-244).  A comm-delay
+//   is a visible-at time in the future, never a blocking sleep.
+//
+// Inbox flags carry the iteration epoch, so nothing is ever reset; an
+// iteration barrier in `init` keeps epochs of a lane group in step.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "rrfp_common.h"
+#include "rrfp_core.cuh"
+
+#define RRFP_MAX_KEYS (RRFP_MAX_WORDS * 32)
+#define RRFP_MAX_LANES 64
+#define LANE_NONE 3
+
+struct lane_inbox {
+  uint32_t fflag[RRFP_MAX_KEYS];
+  uint32_t bflag[RRFP_MAX_KEYS];
+  unsigned long long fvis[RRFP_MAX_KEYS];
+  unsigned long long bvis[RRFP_MAX_KEYS];
+  unsigned long long tp_prop[RRFP_MAX_RANKS];  // (round << 32) | decision code
+  uint32_t tp_cnt[RRFP_MAX_RANKS];             // proposer's view count at proposal
+  uint32_t view_count;                          // monotone count of visible arrivals
+  uint32_t done_epoch;                          // iteration barrier
+  uint32_t pad[2];
+};
+
+struct lane_state {
+  rrfp_lane_desc d;
+  int KEYS, nwords;
+  uint32_t epoch;
+  int32_t n_f, n_b, n_w, mode, focus, phase, next_adm, remaining, fixed_head, status;
+  int32_t cur_kind;
+  rrfp_task_t cur_task;
+  unsigned long long t_start, t_iter0, t_iter1;
+  unsigned long long tp_round;
+  uint32_t tp_snap;
+  int32_t n_lanes;
+  lane_inbox* inbox;                        // own inbox (local)
+  lane_inbox* fwd_dst[RRFP_MAX_RANKS];      // receivers of F output
+  lane_inbox* bwd_dst[RRFP_MAX_RANKS];      // receivers of B output
+  lane_inbox* tp_peer[RRFP_MAX_RANKS];      // TP group boards (incl. self)
+  lane_inbox* all[RRFP_MAX_LANES];          // every lane (iteration barrier)
+  const long long* dur_ns;                  // [3][KEYS] spin / jitter pad
+  const long long* comm_ns;                 // [2][KEYS]
+  const long long* dskew_ns;                // [2][KEYS][R] arrival skew of a sent msg at each dest rank
+  const rrfp_task_t* fixed;                 // [per_stage]
+  rrfp_event* ring;
+  int32_t ring_n, ring_cap;
+  volatile int32_t* abort_flag;             // host-mapped
+  cudaGraphConditionalHandle h_while, h_switch;
+  uint32_t doneF[RRFP_MAX_WORDS], doneB[RRFP_MAX_WORDS], wpend[RRFP_MAX_WORDS];
+  uint32_t fdisp[RRFP_MAX_WORDS], bdisp[RRFP_MAX_WORDS];
+  uint32_t recvF[RRFP_MAX_WORDS], recvB[RRFP_MAX_WORDS];
+};
+
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void ring_emit(lane_state* L, int kind, unsigned long long t0, unsigned long long t1,
+                          int rank, rrfp_task_t task) {
+  int i = atomicAdd(&L->ring_n, 1);
+  if (i < L->ring_cap) {
+    rrfp_event& e = L->ring[i];
+    e.t0 = (long long)t0; e.t1 = (long long)t1; e.kind = kind; e.stage = L->d.stage;
+    e.rank = rank; e.task = task;
+  }
+}
+
+__device__ __forceinline__ void spin_until(unsigned long long deadline) {
+  while (gtimer() < deadline) __nanosleep(64);
+}
+
+// ------------------------------------------------------------------ init
+__global__ void lane_init_kernel(lane_state* L) {
+  const int lane = threadIdx.x;
+  // iteration barrier: every lane of the job finished the previous epoch
+  if (lane == 0) {
+    L->epoch += 1;
+    uint32_t prev = L->epoch - 1;
+    unsigned long long t_guard = gtimer();
+    for (int i = 0; i < L->n_lanes; ++i) {
+      while (ld_acquire_sys(&L->all[i]->done_epoch) < prev) {
+        if (*L->abort_flag) break;
+        __nanosleep(128);
+      }
+    }
+    (void)t_guard;
+    L->n_f = L->n_b = L->n_w = 0;
+    L->mode = RRFP_BP_NORMAL; L->focus = -1; L->phase = -1;
+    L->next_adm = L->d.stage == 0 ? 0 : -1;
+    L->remaining = L->d.per_stage;
+    L->fixed_head = 0; L->status = 0; L->cur_kind = LANE_NONE;
+    L->ring_n = 0;
+    L->t_iter0 = gtimer();
+  }
+  for (int i = lane; i < RRFP_MAX_WORDS; i += 32) {
+    L->doneF[i] = L->doneB[i] = L->wpend[i] = 0;
+    L->fdisp[i] = L->bdisp[i] = 0;
+    L->recvF[i] = L->recvB[i] = 0;
+  }
+}
+
+__global__ void lane_final_kernel(lane_state* L) {
+  if (threadIdx.x == 0) {
+    L->t_iter1 = gtimer();
+    __threadfence_system();
+    st_release_sys(&L->inbox->done_epoch, L->epoch);
+  }
+}
+
+// ---------------------------------------------------------------- dispatch
+// Builds this lane's ready bitmasks from the inbox (warp-parallel), logs new
+// arrivals, returns the number of visible arrivals.
+__device__ void build_view(lane_state* L, uint32_t* sF, uint32_t* sB, unsigned long long now) {
+  const int lane = threadIdx.x;
+  const rrfp_lane_desc& d = L->d;
+  const int MW = d.MW;
+  const uint32_t ep = L->epoch;
+  const lane_inbox* in = L->inbox;
+  uint32_t count = 0;
+  for (int w = 0; w < L->nwords; ++w) {
+    int key = w * 32 + lane;
+    int mb = rrfp_key_mb(key, MW), c = rrfp_key_chunk(key, MW);
+    bool valid = mb < d.M;
+    bool af = valid && ld_acquire_sys(&in->fflag[key]) == ep && in->fvis[key] <= now;
+    bool ab = valid && ld_acquire_sys(&in->bflag[key]) == ep && in->bvis[key] <= now;
+    bool turn = valid && d.stage == d.N - 1 && c == d.C - 1;
+    uint32_t mF = __ballot_sync(0xffffffffu, af);
+    uint32_t mB = __ballot_sync(0xffffffffu, ab);
+    uint32_t mT = __ballot_sync(0xffffffffu, turn);
+    uint32_t newF = mF & ~L->recvF[w];
+    uint32_t newB = mB & ~L->recvB[w];
+    if ((newF >> lane) & 1u)
+      ring_emit(L, 2, in->fvis[key], in->fvis[key], d.rank, rrfp_make_task(RRFP_DIR_F, d.stage, mb, c));
+    if ((newB >> lane) & 1u)
+      ring_emit(L, 2, in->bvis[key], in->bvis[key], d.rank, rrfp_make_task(RRFP_DIR_B, d.stage, mb, c));
+    __syncwarp();
+    if (lane == 0) {
+      L->recvF[w] |= newF;
+      L->recvB[w] |= newB;
+      sF[w] = mF & ~L->fdisp[w];
+      sB[w] = (mB | mT) & L->doneF[w] & ~L->bdisp[w];
+    }
+    count += __popc(mF) + __popc(mB);
+  }
+  __syncwarp();
+  if (lane == 0 && count != L->inbox->view_count) {
+    st_release_sys(&L->inbox->view_count, count);
+  }
+  __syncwarp();
+}
+
+__device__ rrfp_decision lane_arbitrate(lane_state* L, const uint32_t* sF, const uint32_t* sB) {
+  const rrfp_lane_desc& d = L->d;
+  rrfp_bp_update(&L->mode, &L->focus, d.buffer_limit, L->n_f, L->n_b, L->doneF, L->doneB, d.M,
+                 d.C, d.MW);
+  rrfp_view_ref v;
+  v.fready = sF; v.bready = sB; v.wpend = L->wpend; v.doneF = L->doneF; v.doneB = L->doneB;
+  v.admission = L->next_adm;
+  return rrfp_arbitrate_core(v, d.hint, L->mode, L->focus, L->phase, d.M, d.C, d.MW, d.decompose);
+}
+
+__device__ rrfp_decision lane_fixed_head(lane_state* L, const uint32_t* sF, const uint32_t* sB) {
+  rrfp_decision dec; dec.kind = RRFP_WAIT; dec.mb = dec.chunk = -1;
+  if (L->fixed_head >= L->d.per_stage) return dec;
+  rrfp_task_t t = L->fixed[L->fixed_head];
+  int dir = rrfp_task_dir(t), mb = rrfp_task_mb(t), c = rrfp_task_chunk(t);
+  int k = rrfp_key(mb, c, L->d.MW);
+  bool ready;
+  if (dir == RRFP_DIR_F) ready = (L->d.stage == 0 && c == 0) || bit_get(sF, k);
+  else if (dir == RRFP_DIR_B) ready = bit_get(sB, k);
+  else ready = bit_get(L->wpend, k);
+  if (ready) { dec.kind = dir; dec.mb = mb; dec.chunk = c; }
+  return dec;
+}
+
+__device__ void lane_commit(lane_state* L, const rrfp_decision& dec) {
+  const rrfp_lane_desc& d = L->d;
+  int k = rrfp_key(dec.mb, dec.chunk, d.MW);
+  if (dec.kind == RRFP_DIR_F) {
+    if (d.stage == 0 && dec.chunk == 0) {
+      L->next_adm = (L->next_adm + 1 < d.M) ? L->next_adm + 1 : -1;
+      // FIXED mode may admit out of order: keep the cursor monotone past it
+    }
+    bit_set(L->fdisp, k);
+  } else if (dec.kind == RRFP_DIR_B) {
+    bit_set(L->bdisp, k);
+  } else {
+    bit_clr(L->wpend, k);
+  }
+  if (d.fixed_mode) L->fixed_head += 1;
+  else rrfp_advance_phase(&L->phase, d.hint, dec.kind);
+  L->cur_kind = dec.kind;
+  L->cur_task = rrfp_make_task(dec.kind, d.stage, dec.mb, dec.chunk);
+}
+
+__device__ __forceinline__ uint32_t dec_code(const rrfp_decision& d) {
+  return (uint32_t)d.kind | ((uint32_t)(d.mb & 1023) << 2) | ((uint32_t)(d.chunk & 15) << 12);
+}
+
+__global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
+  __shared__ uint32_t sF[RRFP_MAX_WORDS], sB[RRFP_MAX_WORDS];
+  __shared__ int s_kind, s_exit;
+  const int lane = threadIdx.x;
+  const rrfp_lane_desc& d = L->d;
+  const int R = d.R;
+  while (true) {
+    if (lane == 0) {
+      s_exit = 0;
+      if (*L->abort_flag) { L->status = RRFP_E_WATCHDOG; s_exit = 1; }
+      else if (L->remaining == 0) s_exit = 1;
+    }
+    __syncwarp();
+    if (s_exit) {
+      if (lane == 0) {
+        L->cur_kind = LANE_NONE;
+        cudaGraphSetConditional(L->h_switch, LANE_NONE);
+        cudaGraphSetConditional(L->h_while, 0);
+      }
+      return;
+    }
+    unsigned long long now = gtimer();
+    build_view(L, sF, sB, now);
+    if (lane == 0) {
+      rrfp_decision dec = d.fixed_mode ? lane_fixed_head(L, sF, sB) : lane_arbitrate(L, sF, sB);
+      s_kind = RRFP_WAIT;
+      if (R == 1) {
+        if (dec.kind == RRFP_WAIT) {
+          if (!d.fixed_mode) L->phase = -1;
+        } else {
+          lane_commit(L, dec);
+          s_kind = dec.kind;
+        }
+      } else {
+        // K4: TP agreement round over the group's boards (arbitration.py:323-334,
+        // live._resolve_round 246-277): publish, gather all R, same verdict everywhere.
+        unsigned long long round = ++L->tp_round;
+        unsigned long long word = (round << 32) | dec_code(dec);
+        uint32_t mycnt = L->inbox->view_count;
+        for (int r = 0; r < R; ++r) {
+          L->tp_peer[r]->tp_cnt[d.rank] = mycnt;
+          __threadfence_system();
+          st_release_sys64(&L->tp_peer[r]->tp_prop[d.rank], word);
+        }
+        rrfp_decision ds[RRFP_MAX_RANKS];
+        uint32_t snap = 0;
+        for (int r = 0; r < R; ++r) {
+          unsigned long long w;
+          while (((w = ld_acquire_sys64(&L->inbox->tp_prop[r])) >> 32) < round) {
+            if (*L->abort_flag) break;
+            __nanosleep(32);
+          }
+          uint32_t code = (uint32_t)w;
+          ds[r].kind = code & 3; ds[r].mb = (code >> 2) & 1023; ds[r].chunk = (code >> 12) & 15;
+          snap += L->inbox->tp_cnt[r];
+        }
+        bool all_wait = true, all_w = true;
+        for (int r = 0; r < R; ++r) {
+          all_wait = all_wait && ds[r].kind == RRFP_WAIT;
+          all_w = all_w && ds[r].kind == RRFP_DIR_W;
+        }
+        if (all_wait) {
+          L->phase = -1;
+        } else if (all_w) {
+          lane_commit(L, ds[0]);
+          s_kind = RRFP_DIR_W;
+        } else {
+          bool agreed = ds[0].kind == RRFP_DIR_F || ds[0].kind == RRFP_DIR_B;
+          for (int r = 1; r < R && agreed; ++r)
+            agreed = ds[r].kind == ds[0].kind && ds[r].mb == ds[0].mb && ds[r].chunk == ds[0].chunk;
+          unsigned long long t0 = gtimer();
+          spin_until(t0 + (unsigned long long)d.coord_cost_ns);
+          if (d.rank == 0)
+            ring_emit(L, agreed ? 3 : 4, t0, gtimer(), -1,
+                      agreed ? rrfp_make_task(ds[0].kind, d.stage, ds[0].mb, ds[0].chunk)
+                             : RRFP_NO_TASK);
+          if (agreed) {
+            lane_commit(L, ds[0]);
+            s_kind = ds[0].kind;
+          } else {
+            L->phase = -1;
+          }
+        }
+        L->tp_snap = snap;
+        // wait / deferral: retry only after a new arrival at ANY rank of the
+        // group (live.py:398-407); -1 tells the warp to enter that wait.
+        if (s_kind == RRFP_WAIT) s_kind = -1;
+      }
+      if (s_kind >= 0 && s_kind != RRFP_WAIT) {
+        L->t_start = gtimer();
+        cudaGraphSetConditional(L->h_switch, (unsigned)s_kind);
+      }
+    }
+    __syncwarp();
+    int k = s_kind;
+    if (k >= 0 && k != RRFP_WAIT) return;
+    if (R > 1 && k < 0) {
+      // TP wait: rebuild the view until any rank's arrival count changes
+      while (true) {
+        __syncwarp();
+        build_view(L, sF, sB, gtimer());
+        int go = 0;
+        if (lane == 0) {
+          uint32_t cur = 0;
+          for (int r = 0; r < R; ++r) cur += ld_acquire_sys(&L->tp_peer[r]->view_count);
+          go = (cur != L->tp_snap) || *L->abort_flag;
+        }
+        go = __shfl_sync(0xffffffffu, go, 0);
+        if (go) break;
+        __nanosleep(256);
+      }
+    } else {
+      __nanosleep(128);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- bodies
+// Synthetic compute: spin the task's table duration (latency+jitter, scaled).
+__global__ void lane_spin_body_kernel(lane_state* L) {
+  if (threadIdx.x == 0) {
+    rrfp_task_t t = L->cur_task;
+    int k = rrfp_key(rrfp_task_mb(t), rrfp_task_chunk(t), L->d.MW);
+    long long ns = L->dur_ns[(size_t)rrfp_task_dir(t) * L->KEYS + k];
+    spin_until(L->t_start + (unsigned long long)ns);
+  }
+}
+
+// ---------------------------------------------------------------- complete
+__device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end) {
+  const rrfp_lane_desc& d = L->d;
+  int dst_c, dst_s;
+  lane_inbox* const* dsts;
+  if (dir == RRFP_DIR_F) {
+    if (d.stage < d.N - 1) { dst_s = d.stage + 1; dst_c = c; }
+    else if (c < d.C - 1) { dst_s = 0; dst_c = c + 1; }
+    else return;  // turn-around: B readiness derives from doneF locally
+    dsts = L->fwd_dst;
+  } else {
+    if (d.stage > 0) { dst_s = d.stage - 1; dst_c = c; }
+    else if (c > 0) { dst_s = d.N - 1; dst_c = c - 1; }
+    else return;
+    dsts = L->bwd_dst;
+  }
+  (void)dst_s;
+  int key = rrfp_key(mb, c, d.MW);
+  int dkey = rrfp_key(mb, dst_c, d.MW);
+  long long delay = L->comm_ns[(size_t)dir * L->KEYS + key];
+  for (int r = 0; r < d.R; ++r) {
+    lane_inbox* in = dsts[r];
+    long long sk = L->dskew_ns[((size_t)dir * L->KEYS + dkey) * d.R + r];
+    unsigned long long vis = end + (unsigned long long)(delay + sk);
+    if (dir == RRFP_DIR_F) {
+      in->fvis[dkey] = vis;
+      __threadfence_system();
+      st_release_sys(&in->fflag[dkey], L->epoch);
+    } else {
+      in->bvis[dkey] = vis;
+      __threadfence_system();
+      st_release_sys(&in->bflag[dkey], L->epoch);
+    }
+  }
+  if (d.rank == 0)
+    ring_emit(L, 1, end, end + (unsigned long long)delay, -1, rrfp_make_task(dir, d.stage, mb, c));
+}
+
+__global__ void lane_complete_kernel(lane_state* L) {
+  if (threadIdx.x != 0) return;
+  int kind = L->cur_kind;
+  if (kind == LANE_NONE) return;
+  const rrfp_lane_desc& d = L->d;
+  rrfp_task_t t = L->cur_task;
+  int mb = rrfp_task_mb(t), c = rrfp_task_chunk(t);
+  int k = rrfp_key(mb, c, d.MW);
+  if (d.compute_kind == 1) {
+    // K11: injected jitter pads real compute (dur table holds the injection only)
+    long long pad = L->dur_ns[(size_t)kind * L->KEYS + k];
+    if (pad > 0) spin_until(gtimer() + (unsigned long long)pad);
+  }
+  unsigned long long end = gtimer();
+  ring_emit(L, 0, L->t_start, end, d.R > 1 ? d.rank : -1, t);
+  L->remaining -= 1;
+  if (kind == RRFP_DIR_F) {
+    bit_set(L->doneF, k);
+    L->n_f += 1;
+    lane_send(L, kind, mb, c, end);
+  } else if (kind == RRFP_DIR_B) {
+    bit_set(L->doneB, k);
+    L->n_b += 1;
+    if (d.decompose) bit_set(L->wpend, k);
+    lane_send(L, kind, mb, c, end);
+  } else {
+    L->n_w += 1;
+  }
+  L->cur_kind = LANE_NONE;
+}
+
+// ================================================================ host side
+struct rrfp_runtime {
+  rrfp_lane_desc d;
+  int dev;
+  lane_state* L;            // device
+  lane_inbox* inbox;        // device (separate allocation: IPC-exportable)
+  long long* tables;        // device
+  rrfp_task_t* fixed;       // device
+  rrfp_event* ring;         // device
+  int32_t* abort_host;      // mapped host memory
+  int32_t* abort_dev;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  cudaGraph_t body[3];
+  bool built;
+  cudaEvent_t done_ev;
+  int KEYS;
+  std::vector<void*> opened;
+};
+
+static int lane_check_desc(const rrfp_lane_desc* d) {
+  if (!d) return rrfp_fail(RRFP_E_INVALID, "null lane desc");
+  if (d->N < 1 || d->N > RRFP_MAX_STAGES || d->R < 1 || d->R > RRFP_MAX_RANKS || d->C < 1 ||
+      d->C > RRFP_MAX_CHUNKS || d->M < 1 || d->M > RRFP_MAX_MB || d->MW != (d->M + 31) / 32 ||
+      d->C * d->MW > RRFP_MAX_WORDS)
+    return rrfp_fail(RRFP_E_INVALID, "lane shape out of range");
+  if (d->N * d->R > RRFP_MAX_LANES) return rrfp_fail(RRFP_E_INVALID, "too many lanes");
+  if (d->stage < 0 || d->stage >= d->N || d->rank < 0 || d->rank >= d->R)
+    return rrfp_fail(RRFP_E_INVALID, "stage/rank out of range");
+  if (d->buffer_limit < 1) return rrfp_fail(RRFP_E_INVALID, "buffer_limit must be >= 1");
+  if (d->trace_cap < 16) return rrfp_fail(RRFP_E_INVALID, "trace_cap too small");
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** out) {
+  int rc = lane_check_desc(desc);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return rrfp_fail(RRFP_E_NOGPU, "no CUDA device");
+  RRFP_CUDA_TRY(cudaSetDevice(desc->device));
+  rrfp_runtime* rt = new rrfp_runtime();
+  rt->d = *desc;
+  rt->dev = desc->device;
+  rt->KEYS = desc->C * desc->MW * 32;
+  rt->built = false;
+  RRFP_CUDA_TRY(cudaMalloc(&rt->L, sizeof(lane_state)));
+  RRFP_CUDA_TRY(cudaMalloc(&rt->inbox, sizeof(lane_inbox)));
+  RRFP_CUDA_TRY(cudaMemset(rt->inbox, 0, sizeof(lane_inbox)));
+  size_t tbytes = sizeof(long long) * (size_t)rt->KEYS * (3 + 2 + 2 * desc->R);
+  RRFP_CUDA_TRY(cudaMalloc(&rt->tables, tbytes));
+  RRFP_CUDA_TRY(cudaMemset(rt->tables, 0, tbytes));
+  RRFP_CUDA_TRY(cudaMalloc(&rt->fixed, sizeof(rrfp_task_t) * (size_t)(desc->per_stage + 1)));
+  RRFP_CUDA_TRY(cudaMalloc(&rt->ring, sizeof(rrfp_event) * (size_t)desc->trace_cap));
+  RRFP_CUDA_TRY(cudaHostAlloc(&rt->abort_host, sizeof(int32_t), cudaHostAllocMapped));
+  *rt->abort_host = 0;
+  RRFP_CUDA_TRY(cudaHostGetDevicePointer(&rt->abort_dev, rt->abort_host, 0));
+  RRFP_CUDA_TRY(cudaEventCreateWithFlags(&rt->done_ev, cudaEventDisableTiming));
+  // host image of the lane state
+  lane_state h;
+  memset(&h, 0, sizeof(h));
+  h.d = *desc;
+  h.KEYS = rt->KEYS;
+  h.nwords = desc->C * desc->MW;
+  h.epoch = 0;
+  h.inbox = rt->inbox;
+  h.dur_ns = rt->tables;
+  h.comm_ns = rt->tables + 3 * rt->KEYS;
+  h.dskew_ns = rt->tables + 5 * (size_t)rt->KEYS;
+  h.fixed = rt->fixed;
+  h.ring = rt->ring;
+  h.ring_cap = desc->trace_cap;
+  h.abort_flag = rt->abort_dev;
+  h.n_lanes = 1;
+  h.all[0] = rt->inbox;
+  for (int r = 0; r < RRFP_MAX_RANKS; ++r) h.fwd_dst[r] = h.bwd_dst[r] = h.tp_peer[r] = rt->inbox;
+  RRFP_CUDA_TRY(cudaMemcpy(rt->L, &h, sizeof(h), cudaMemcpyHostToDevice));
+  *out = rt;
+  return RRFP_OK;
+}
+
+extern "C" void rrfp_runtime_destroy(rrfp_runtime* rt) {
+  if (!rt) return;
+  cudaSetDevice(rt->dev);
+  if (rt->exec) cudaGraphExecDestroy(rt->exec);
+  if (rt->graph) cudaGraphDestroy(rt->graph);
+  for (void* p : rt->opened) cudaIpcCloseMemHandle(p);
+  cudaFree(rt->L); cudaFree(rt->inbox); cudaFree(rt->tables); cudaFree(rt->fixed);
+  cudaFree(rt->ring); cudaFreeHost(rt->abort_host); cudaEventDestroy(rt->done_ev);
+  delete rt;
+}
+
+extern "C" int rrfp_runtime_inbox(rrfp_runtime* rt, void** dev_ptr, size_t* bytes) {
+  if (!rt || !dev_ptr) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  *dev_ptr = rt->inbox;
+  if (bytes) *bytes = sizeof(lane_inbox);
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_inbox_ipc(rrfp_runtime* rt, void* handle64) {
+  if (!rt || !handle64) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  cudaIpcMemHandle_t h;
+  RRFP_CUDA_TRY(cudaIpcGetMemHandle(&h, rt->inbox));
+  memcpy(handle64, &h, sizeof(h));
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  RRFP_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RRFP_OK;
+}
+
+// all_lanes: N*R inbox pointers (lane index = stage*R + rank), used for the
+// iteration barrier; fwd/bwd: R receivers each (NULL where no send exists).
+extern "C" int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst, void* const* bwd_dst,
+                                    void* const* tp_peer) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  lane_state h;
+  RRFP_CUDA_TRY(cudaMemcpy(&h, rt->L, sizeof(h), cudaMemcpyDeviceToHost));
+  int R = rt->d.R, NL = rt->d.N * R;
+  for (int r = 0; r < R; ++r) {
+    h.fwd_dst[r] = fwd_dst && fwd_dst[r] ? (lane_inbox*)fwd_dst[r] : rt->inbox;
+    h.bwd_dst[r] = bwd_dst && bwd_dst[r] ? (lane_inbox*)bwd_dst[r] : rt->inbox;
+    h.tp_peer[r] = tp_peer && tp_peer[r] ? (lane_inbox*)tp_peer[r] : rt->inbox;
+  }
+  // the iteration-barrier list follows the R tp peers in tp_peer[R..R+NL)
+  h.n_lanes = 1;
+  h.all[0] = rt->inbox;
+  if (tp_peer) {
+    h.n_lanes = NL;
+    for (int i = 0; i < NL; ++i) h.all[i] = tp_peer[R + i] ? (lane_inbox*)tp_peer[R + i] : rt->inbox;
+  }
+  RRFP_CUDA_TRY(cudaMemcpy(rt->L, &h, sizeof(h), cudaMemcpyHostToDevice));
+  return RRFP_OK;
+}
+
+// dur_ns[3*KEYS]; comm_ns[2*KEYS] (indexed by the sending task);
+// skew_ns[2*KEYS*R]: arrival skew at each destination rank, indexed by
+// [send direction][destination key][rank].
+extern "C" int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
+                                        const int64_t* skew_ns, const rrfp_task_t* fixed) {
+  if (!rt || !dur_ns || !comm_ns || !skew_ns) return rrfp_fail(RRFP_E_INVALID, "null table");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  size_t K = rt->KEYS, R = rt->d.R;
+  RRFP_CUDA_TRY(cudaMemcpy(rt->tables, dur_ns, sizeof(long long) * 3 * K, cudaMemcpyHostToDevice));
+  RRFP_CUDA_TRY(cudaMemcpy(rt->tables + 3 * K, comm_ns, sizeof(long long) * 2 * K, cudaMemcpyHostToDevice));
+  RRFP_CUDA_TRY(cudaMemcpy(rt->tables + 5 * K, skew_ns, sizeof(long long) * 2 * K * R,
+                           cudaMemcpyHostToDevice));
+  if (fixed && rt->d.per_stage > 0)
+    RRFP_CUDA_TRY(cudaMemcpy(rt->fixed, fixed, sizeof(rrfp_task_t) * rt->d.per_stage,
+                             cudaMemcpyHostToDevice));
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* graph_f, void* graph_b, void* graph_w) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  if (rt->built) return rrfp_fail(RRFP_E_INVALID, "bodies must be set before the first launch");
+  rt->body[RRFP_DIR_F] = (cudaGraph_t)graph_f;
+  rt->body[RRFP_DIR_B] = (cudaGraph_t)graph_b;
+  rt->body[RRFP_DIR_W] = (cudaGraph_t)graph_w;
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_task_ptr(rrfp_runtime* rt, void** dev_ptr) {
+  if (!rt || !dev_ptr) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  *dev_ptr = (char*)rt->L + offsetof(lane_state, cur_task);
+  return RRFP_OK;
+}
+
+static int add_kernel(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode_t* dep, int ndep,
+                      void* fn, lane_state* L) {
+  cudaKernelNodeParams kp;
+  memset(&kp, 0, sizeof(kp));
+  void* args[1] = {&L};
+  kp.func = fn;
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.kernelParams = args;
+  RRFP_CUDA_TRY(cudaGraphAddKernelNode(node, g, dep, ndep, &kp));
+  return RRFP_OK;
+}
+
+static int build_graph(rrfp_runtime* rt) {
+  cudaGraph_t g;
+  RRFP_CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphNode_t n_init, n_while, n_final, n_dec, n_sw, n_comp;
+  int rc = add_kernel(&n_init, g, nullptr, 0, (void*)lane_init_kernel, rt->L);
+  if (rc) return rc;
+  cudaGraphConditionalHandle hw, hs;
+  RRFP_CUDA_TRY(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hw;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  RRFP_CUDA_TRY(cudaGraphAddNode(&n_while, g, &n_init, 1, &cp));
+  cudaGraph_t loop = cp.conditional.phGraph_out[0];
+  if ((rc = add_kernel(&n_dec, loop, nullptr, 0, (void*)lane_dispatch_kernel, rt->L))) return rc;
+  RRFP_CUDA_TRY(cudaGraphConditionalHandleCreate(&hs, loop, LANE_NONE, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams sp = {};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = hs;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = 3;
+  RRFP_CUDA_TRY(cudaGraphAddNode(&n_sw, loop, &n_dec, 1, &sp));
+  for (int k = 0; k < 3; ++k) {
+    cudaGraph_t b = sp.conditional.phGraph_out[k];
+    cudaGraphNode_t n;
+    if (rt->d.compute_kind == 1 && rt->body[k]) {
+      RRFP_CUDA_TRY(cudaGraphAddChildGraphNode(&n, b, nullptr, 0, rt->body[k]));
+    } else if (rt->d.compute_kind == 0) {
+      if ((rc = add_kernel(&n, b, nullptr, 0, (void*)lane_spin_body_kernel, rt->L))) return rc;
+    } else {
+      RRFP_CUDA_TRY(cudaGraphAddEmptyNode(&n, b, nullptr, 0));
+    }
+  }
+  if ((rc = add_kernel(&n_comp, loop, &n_sw, 1, (void*)lane_complete_kernel, rt->L))) return rc;
+  if ((rc = add_kernel(&n_final, g, &n_while, 1, (void*)lane_final_kernel, rt->L))) return rc;
+  // store the handles in the device lane state
+  RRFP_CUDA_TRY(cudaMemcpy((char*)rt->L + offsetof(lane_state, h_while), &hw, sizeof(hw),
+                           cudaMemcpyHostToDevice));
+  RRFP_CUDA_TRY(cudaMemcpy((char*)rt->L + offsetof(lane_state, h_switch), &hs, sizeof(hs),
+                           cudaMemcpyHostToDevice));
+  RRFP_CUDA_TRY(cudaGraphInstantiate(&rt->exec, g, 0));
+  rt->graph = g;
+  rt->built = true;
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  (void)epoch;
+  if (!rt->built) {
+    int rc = build_graph(rt);
+    if (rc) return rc;
+  }
+  *rt->abort_host = 0;
+  RRFP_CUDA_TRY(cudaGraphLaunch(rt->exec, (cudaStream_t)stream));
+  RRFP_CUDA_TRY(cudaEventRecord(rt->done_ev, (cudaStream_t)stream));
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_event* events,
+                                 int32_t cap, int32_t* n_events, int64_t* t0_ns) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  struct timespec a, b;
+  clock_gettime(CLOCK_MONOTONIC, &a);
+  bool fired = false;
+  while (true) {
+    cudaError_t q = cudaEventQuery(rt->done_ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) return rrfp_fail(RRFP_E_CUDA, "lane: %s", cudaGetErrorString(q));
+    clock_gettime(CLOCK_MONOTONIC, &b);
+    double el = (b.tv_sec - a.tv_sec) + 1e-9 * (b.tv_nsec - a.tv_nsec);
+    if (!fired && watchdog_secs > 0 && el > watchdog_secs) {
+      *(volatile int32_t*)rt->abort_host = 1;  // dispatcher exits its loop
+      fired = true;
+    }
+    struct timespec ts = {0, 20000};
+    nanosleep(&ts, nullptr);
+  }
+  lane_state h;
+  RRFP_CUDA_TRY(cudaMemcpy(&h, rt->L, sizeof(h), cudaMemcpyDeviceToHost));
+  int n = h.ring_n < h.ring_cap ? h.ring_n : h.ring_cap;
+  if (n > cap) n = cap;
+  if (events && n > 0)
+    RRFP_CUDA_TRY(cudaMemcpy(events, rt->ring, sizeof(rrfp_event) * n, cudaMemcpyDeviceToHost));
+  if (n_events) *n_events = n;
+  if (t0_ns) *t0_ns = (int64_t)h.t_iter0;
+  if (fired || h.status == RRFP_E_WATCHDOG)
+    return rrfp_fail(RRFP_E_WATCHDOG, "watchdog: stage %d rank %d remaining=%d n_f=%d n_b=%d",
+                     rt->d.stage, rt->d.rank, h.remaining, h.n_f, h.n_b);
+  if (h.ring_n > h.ring_cap) return rrfp_fail(RRFP_E_CAPACITY, "trace ring overflow");
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  lane_state h;
+  RRFP_CUDA_TRY(cudaMemcpy(&h, rt->L, sizeof(h), cudaMemcpyDeviceToHost));
+  if (dump && cap)
+    snprintf(dump, cap,
+             "stage %d rank %d: epoch=%u remaining=%d mode=%d D=%d n_w=%d next_adm=%d "
+             "fixed_head=%d status=%d tp_round=%llu",
+             rt->d.stage, rt->d.rank, h.epoch, h.remaining, h.mode, h.n_f - h.n_b, h.n_w,
+             h.next_adm, h.fixed_head, h.status, (unsigned long long)h.tp_round);
+  return RRFP_OK;
+}
+
+__global__ void spin_kernel(long long ns) {
+  unsigned long long t0 = gtimer();
+  spin_until(t0 + (unsigned long long)ns);
+}
+
+extern "C" int rrfp_spin(int64_t ns, void* stream) {
+  spin_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(ns);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}

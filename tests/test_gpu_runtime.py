@@ -1,0 +1,134 @@
+"""Free-running device runtime (run_gpu) on the B200: live.run_live's test
+strategy (pkg/tests/test_live.py) plus replay-mode bit-exactness."""
+import pytest
+
+import paper_2605_18750_b200 as P
+from paper_2605_18750_b200.runtime import run_gpu
+import rrfp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SLACK = (5, 1.05, 400)   # wall traces: (lower_us, upper_rel, upper_abs_us)
+
+
+def _tuples(trace):
+    return [(e.t_start, e.t_end, e.stage, e.rank, e.microbatch, e.chunk, e.direction, e.event_kind)
+            for e in trace.events]
+
+
+def _oracle_w(w):
+    return O.from_workload_json(w.to_json())
+
+
+def _seqs(trace, n, rank=None):
+    per = [[] for _ in range(n)]
+    for e in sorted(trace.execs(), key=lambda e: e.t_start):
+        if rank is None or e.rank in (None, rank):
+            per[e.stage].append((e.direction, e.microbatch, e.chunk))
+    return per
+
+
+def _spec(n=4, m=8, **kw):
+    return P.GeneratorSpec(num_stages=n, num_microbatches=m, forward=P.uniform(100, 300),
+                           backward=P.uniform(150, 400), **kw)
+
+
+def test_live_iteration_is_complete_and_valid():
+    w = P.generate_workload(_spec(), 3)
+    tr, m = run_gpu(w, "bf", 32, time_scale=1.0, seed=3)
+    assert tr.clock == "wall"
+    viol = O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=1.0)
+    assert not viol, viol[:5]
+    assert m.total_tasks == w.task_count()
+    for s in m.per_stage:
+        assert s.compute + s.blocking + s.tp_coord == m.makespan
+
+
+def test_same_execution_multiset_as_virtual():
+    w = P.generate_workload(_spec(3, 6), 1)
+    tr, _ = run_gpu(w, "bf", 32, time_scale=1.0, seed=1)
+    ev, _ = O.run_rrfp(_oracle_w(w), "bf", 32, 1)
+    got = sorted((e.stage, e.direction, e.microbatch, e.chunk) for e in tr.execs())
+    want = sorted((s, d, mb, c) for (_, _, s, r, mb, c, d, k) in ev if k == "exec")
+    assert got == want
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_replay_mode_dispatch_bit_exact(seed):
+    """North-star parity: under a replayed seeded readiness/jitter trace the
+    device lanes execute exactly the oracle's per-stage dispatch order."""
+    spec = P.GeneratorSpec(num_stages=4, num_microbatches=16,
+                           forward=P.lognormal(10.0, 0.35, 8000, 60000),
+                           backward=P.lognormal(10.2, 0.35, 8000, 70000))
+    w = P.generate_workload(spec, seed)
+    jit = P.JITTER_PRESETS["J3"]
+    tr, _ = run_gpu(w, "bf", 32, time_scale=0.005, seed=seed, jitter=jit, mode="replay")
+    ev, _ = O.run_rrfp(_oracle_w(w), "bf", 32, seed, "J3")
+    want = [[(d, mb, c) for d, mb, c, _, _ in s] for s in O.exec_sequences(ev, 4)]
+    assert _seqs(tr, 4) == want
+
+
+def test_fixed_1f1b_follows_schedule():
+    w = P.generate_workload(_spec(4, 8), 5)
+    tr, m = run_gpu(w, "bf", 32, time_scale=1.0, seed=5, mode="fixed")
+    sched = P.build_1f1b_schedule(w)
+    want = [[(t.direction, t.microbatch, t.chunk) for t in st] for st in sched.per_stage_order]
+    assert _seqs(tr, 4) == want
+    viol = O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=1.0)
+    assert not viol, viol[:5]
+
+
+def test_tight_limits_never_stall():
+    for limit in (1, 2):
+        w = P.generate_workload(_spec(3, 6), 2)
+        tr, m = run_gpu(w, "bf", limit, time_scale=1.0, seed=2, watchdog_secs=10)
+        assert len(tr.execs()) == w.task_count()
+        for s in range(3):
+            lead = 0
+            for e in sorted((e for e in tr.execs() if e.stage == s), key=lambda e: e.t_end):
+                lead += 1 if e.direction == "F" else -1
+                assert 0 <= lead <= limit
+
+
+def test_weight_split_runs_all_w():
+    w = P.generate_workload(_spec(3, 4, decompose_backward=True), 4)
+    tr, m = run_gpu(w, "bfw", 32, time_scale=1.0, seed=4)
+    assert sum(s.n_w for s in m.per_stage) == 12
+    viol = O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=1.0)
+    assert not viol, viol[:5]
+
+
+def test_interleaved_chunks_and_jitter_valid():
+    spec = P.GeneratorSpec(num_stages=3, num_microbatches=4, num_chunks=2,
+                           forward=P.uniform(100, 200), backward=P.uniform(100, 200),
+                           comm_delay=P.CommDelay(kind="uniform", lo=5, hi=40, seed=3))
+    w = P.generate_workload(spec, 6)
+    jit = P.JITTER_PRESETS["J1"]
+    tr, m = run_gpu(w, "bf", 4, time_scale=0.1, seed=6, jitter=jit)
+    inj = O.injection_table(_oracle_w(w), "J1", 6)
+    viol = O.validate(_tuples(tr), _oracle_w(w), inj, slack=SLACK, clock="wall", scale=0.1)
+    assert not viol, viol[:5]
+
+
+def test_tp_order_identical_across_ranks():
+    spec = P.GeneratorSpec(num_stages=3, num_microbatches=6, tp_group_size=2,
+                           forward=P.uniform(100, 300), backward=P.uniform(100, 300))
+    w = P.generate_workload(spec, 7)
+    tp = P.TpGroup(group_size=2, coordination_round_cost=5, skew_lo=0, skew_hi=60)
+    tr, m = run_gpu(w, "bf", 32, time_scale=1.0, seed=7, tp=tp)
+    assert len(tr.execs()) == 2 * w.task_count()
+    for s in range(3):
+        seqs = [[(e.direction, e.microbatch) for e in sorted(tr.execs(rank=r), key=lambda e: e.t_start)
+                 if e.stage == s] for r in (0, 1)]
+        assert seqs[0] == seqs[1]
+    assert m.agreed_rounds > 0
+
+
+def test_watchdog_fires_on_impossible_schedule():
+    # a fixed order whose heads wait on each other (B before its F) never finishes
+    w = P.generate_workload(_spec(2, 2), 0)
+    bad = P.FixedSchedule(tuple(
+        tuple(sorted(st, key=lambda t: t.direction)) for st in P.build_1f1b_schedule(w).per_stage_order))
+    from paper_2605_18750_b200.runtime import LiveWatchdogError
+    with pytest.raises(LiveWatchdogError):
+        run_gpu(w, "bf", 32, time_scale=1.0, mode="fixed", schedule=bad, watchdog_secs=2)
