@@ -1,0 +1,338 @@
+"""Benchmark: readiness-driven pipeline iteration of synthetic GPT-1.3B on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--hint bf|bfw|1f1b] [--mb 32] [--jitter J0..J3] [--layers 24]
+
+N=1 runs PP=1 (the single-GPU configuration of BASELINE.json configs[1]);
+under torchrun each rank is one pipeline stage (PP=N, one stage per GPU,
+mailboxes over CUDA IPC / NVLink).  A step = one training iteration over
+M=32 microbatches (F + B (+W) for every microbatch, fp32 weight-gradient
+accumulation), launched as ONE graph per stage whose device dispatcher picks
+every task.  Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iter/s & tokens/s at PP=2/4/8 under jitter vs fixed-order 1F1B; bubble %"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TASK_TIMES = os.path.join(ROOT, "profiles", "task_times_gpt1p3b.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p["bf16_tflops_sustained"], p["bf16_tflops"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1400.0, 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = sorted(int(r[0]) for r in self.rows if r and r[0].isdigit())
+        mx = max((int(r[1]) for r in self.rows if len(r) > 1 and r[1].isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference's CPU runtime (live.run_live restated in oracle/) on this
+    host, executing the same iteration's task graph with the per-task
+    durations our kernels take on the B200 (profiles/task_times_gpt1p3b.json)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rrfp_oracle as O
+    n = max(1, args.gpus)
+    times = default_task_times(n, args.layers)
+    lat = {}
+    dec = args.hint == "bfw"
+    for s in range(n):
+        for mb in range(args.mb):
+            lat[("F", s, mb, 0)] = int(times["F"][s])
+            if dec:
+                lat[("B", s, mb, 0)] = int(times["Bin"][s])
+                lat[("W", s, mb, 0)] = int(times["W"][s])
+            else:
+                lat[("B", s, mb, 0)] = int(times["B"][s])
+    w = {"N": n, "M": args.mb, "C": 1, "R": 1, "lat": lat, "comm": {"kind": "constant", "value": 0},
+         "dec": dec, "beta": 0.5}
+    hint = "bf" if args.hint == "1f1b" else args.hint
+    for _ in range(args.warmup):
+        O.run_live(w, hint, 32, 1.0, seed=0, jitter=args.jitter)
+    t0 = time.perf_counter()
+    mks = []
+    for _ in range(args.steps):
+        _, mk = O.run_live(w, hint, 32, 1.0, seed=0, jitter=args.jitter)
+        mks.append(mk)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = 1.0 / dt
+    cores = len(os.sched_getaffinity(0))
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "iter/s", "impl": "reference",
+            "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "tokens_per_s": round(v * args.mb * 2048, 1),
+            "config": workload_config(args, n),
+            "cpu_baseline": {"value": round(v, 4), "unit": "iter/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle.run_live: {3 * n} threads, {n}x{args.mb} tasks, "
+                                       f"task durations = B200-measured GPT-1.3B per-task times"},
+            "e2e": {"value": round(v, 4), "unit": "iter/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def default_task_times(n_stages, n_layer=24):
+    """Per-stage F/B/Bin/W task times (µs) of GPT-1.3B on B200, measured by
+    this bench (profiles/task_times_gpt1p3b.json) or estimated before that."""
+    try:
+        with open(TASK_TIMES) as f:
+            t = json.load(f)
+        row = t.get(str(n_stages))
+        if row:
+            return row
+    except Exception:
+        pass
+    per_layer_f = 260.0
+    lp = n_layer / n_stages
+    f = [per_layer_f * lp for _ in range(n_stages)]
+    f[-1] += 500.0
+    return {"F": f, "B": [2.1 * x for x in f], "Bin": [1.15 * x for x in f], "W": [0.95 * x for x in f]}
+
+
+def workload_config(args, n):
+    return {"workload": f"GPT-1.3B synthetic (L={args.layers}, d=2048, h=16, ffn=8192, V=50304, "
+                        f"s=2048, mbs=1), PP={n}, M={args.mb}",
+            "model": "gpt-1.3b-synthetic", "global_batch": args.mb, "seq_len": 2048,
+            "parallelism": f"pp{n}", "hint": args.hint, "jitter": args.jitter,
+            "buffer_limit": 32, "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
+
+
+# ------------------------------------------------------------------ our arm
+def gemm_roofline(cfg, peak_tf):
+    """Time the dominant kernel (the stage GEMMs) with CUDA events on its own
+    launch stream, shapes and epilogues exactly as one layer's F/B/W issue them."""
+    import torch
+    from paper_2605_18750_b200 import kernels as K
+    S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
+    bf = torch.bfloat16
+    dev = "cuda"
+    x, w_qkv, w_o, w_1, w_2 = (torch.randn(S, D, device=dev).to(bf), torch.randn(3 * D, D, device=dev).to(bf),
+                               torch.randn(D, D, device=dev).to(bf), torch.randn(Fd, D, device=dev).to(bf),
+                               torch.randn(D, Fd, device=dev).to(bf))
+    bias = torch.zeros(Fd, device=dev).to(bf)
+    qkv, y, pre, act = (torch.empty(S, 3 * D, device=dev, dtype=bf), torch.empty(S, D, device=dev, dtype=bf),
+                        torch.empty(S, Fd, device=dev, dtype=bf), torch.empty(S, Fd, device=dev, dtype=bf))
+    gq, g1, g2 = torch.zeros(3 * D, D, device=dev), torch.zeros(Fd, D, device=dev), torch.zeros(D, Fd, device=dev)
+    calls = [
+        (lambda: K.gemm(x, w_qkv, qkv, bias=bias[:3 * D]), 2 * S * D * 3 * D),
+        (lambda: K.gemm(x, w_o, y, epi=K.EPI_RESID, bias=bias[:D], r=x), 2 * S * D * D),
+        (lambda: K.gemm(x, w_1, pre, epi=K.EPI_BIAS_GELU, c2=act, bias=bias), 2 * S * D * Fd),
+        (lambda: K.gemm(act, w_2, y, epi=K.EPI_RESID, bias=bias[:D], r=x), 2 * S * D * Fd),
+        (lambda: K.gemm(x, w_2, pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre), 2 * S * D * Fd),
+        (lambda: K.gemm(pre, w_1, y, b_mn=True), 2 * S * D * Fd),
+        (lambda: K.gemm(qkv, w_qkv, y, b_mn=True), 2 * S * D * 3 * D),
+        (lambda: K.gemm(x, act, g2, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * Fd),
+        (lambda: K.gemm(pre, x, g1, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * Fd),
+        (lambda: K.gemm(qkv, x, gq, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * 3 * D),
+    ]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for fn, _ in calls:
+            fn()
+        st.synchronize()
+        reps = 10
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            for fn, _ in calls:
+                fn()
+        e1.record(st)
+        st.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * len(calls))
+    flops = sum(f for _, f in calls) / len(calls)
+    achieved = flops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": round(achieved / peak_tf, 3), "traffic": None,
+            "kernel": "gemm_bf16_sm100 (tcgen05.mma 128x256x16, TMA 4-stage, TMEM x2)",
+            "per_launch": "mean over one layer's 10 F/B/W GEMMs (2048 tokens, d=2048, ffn=8192)",
+            "avg_launch_us": round(ms * 1e3, 1)}
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("multi-GPU pipeline bench: see bench_mp (not in this build)")
+    torch.cuda.set_device(local)
+    from paper_2605_18750_b200.model import GPTConfig
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from paper_2605_18750_b200.jitter import PRESETS
+    cfg = GPTConfig(n_layer=args.layers)
+    n = 1
+    hint = "bf" if args.hint == "1f1b" else args.hint
+    mode = "fixed" if args.hint == "1f1b" else "free"
+    t_build = time.perf_counter()
+    pipe = GpuPipeline(cfg, n, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
+    t_build = time.perf_counter() - t_build
+    st0, last = pipe.stages[0], pipe.stages[-1]
+    # host inputs for the end-to-end leg (pinned)
+    tok_h = st0.tokens.cpu().pin_memory()
+    tgt_h = last.targets.cpu().pin_memory()
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    for _ in range(args.warmup):
+        pipe.step()
+    torch.cuda.synchronize()
+    lane_stream = pipe.group.streams[(0, 0)]
+    peak_sus, peak_burst, hbm, peak_kind = load_peaks()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lane_stream)
+        for _ in range(args.steps):
+            pipe.launch()
+            pipe.wait()
+        e1.record(lane_stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        # end-to-end through the public API with host buffers
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st0.tokens.copy_(tok_h, non_blocking=True)
+            last.targets.copy_(tgt_h, non_blocking=True)
+            loss = pipe.step()
+            loss_h.copy_(loss.reshape(1), non_blocking=False)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+    tr, met = pipe.trace()
+    bubble = met.bubble_fraction()
+    it_s = 1000.0 / ms
+    tok = args.mb * cfg.seq
+    # per-task times for the reference arm / replay tables
+    execs = tr.execs()
+    f_us = sum(e.t_end - e.t_start for e in execs if e.direction == "F") / max(1, sum(e.direction == "F" for e in execs))
+    b_us = sum(e.t_end - e.t_start for e in execs if e.direction == "B") / max(1, sum(e.direction == "B" for e in execs))
+    roof = gemm_roofline(cfg, peak_sus)
+    roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
+    # iteration roofline: sum of stage FLOPs / (N * peak)
+    fF, fB, fW = cfg.flops_per_layer()
+    it_flops = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
+    t_roof = it_flops / (n * peak_sus * 1e12)
+    launches_per_task = sum(pipe.stages[0].kernel_counts.values()) / max(1, len(pipe.stages[0].kernel_counts))
+    line = {"metric": METRIC, "value": round(it_s, 4), "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, uniform tokens)",
+            "config": workload_config(args, n),
+            "tokens_per_s": round(it_s * tok, 1), "bubble_fraction": round(bubble, 4),
+            "iteration_roofline": {"t_roof_ms": round(t_roof * 1e3, 2), "frac": round(t_roof * 1e3 / ms, 3),
+                                   "definition": "sum stage FLOPs / (N * sustained bf16 peak) + P2P/NVLink"},
+            "roofline": roof,
+            "task_us": {"F": round(f_us, 1), "B": round(b_us, 1)},
+            "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
+                    "h2d_bytes_per_step": int(tok_h.numel() * 4 + tgt_h.numel() * 4),
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": int(pipe.kernel_launches_per_step()),
+            "build_s": round(t_build, 1),
+            "clocks": clk.summary()}
+    if rank == 0 and args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, f_us, b_us)
+    print(json.dumps(line), flush=True)
+    pipe.close()
+
+
+def cpu_baseline(args, f_us, b_us):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rrfp_oracle as O
+    lat = {}
+    for mb in range(args.mb):
+        lat[("F", 0, mb, 0)] = int(f_us)
+        lat[("B", 0, mb, 0)] = int(b_us)
+    w = {"N": 1, "M": args.mb, "C": 1, "R": 1, "lat": lat, "comm": {"kind": "constant", "value": 0},
+         "dec": False, "beta": 0.5}
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 10.0 or k < 1:
+        O.run_live(w, "bf", 32, 1.0, seed=0)
+        k += 1
+    dt = (time.perf_counter() - t0) / k
+    return {"value": round(1.0 / dt, 4), "unit": "iter/s", "cores": 3, "kind": "port",
+            "sample": f"{k} iterations of oracle.run_live (3 threads) with this run's measured "
+                      f"F={f_us:.0f}us / B={b_us:.0f}us task times, M={args.mb}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--hint", default="bf", choices=["bf", "bfw", "fb", "bprio", "fprio", "1f1b"])
+    ap.add_argument("--mb", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=24)
+    ap.add_argument("--jitter", default="J0")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

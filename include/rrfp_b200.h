@@ -194,10 +194,11 @@ int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst_inboxes, void* c
  * skew_ns[2*KEYS*R] (arrival skew per destination rank), fixed order. */
 int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
                              const int64_t* skew_ns, const rrfp_task_t* fixed);
-/* Register caller-captured compute bodies (cudaGraph_t for F, B, W; W may be
- * NULL when not decomposed).  The bodies read the current task from
- * rrfp_runtime_task_ptr().  Must be called before the first iteration. */
-int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* graph_f, void* graph_b, void* graph_w);
+/* Register caller-captured compute bodies: graphs[kind * M + mb] is the
+ * cudaGraph_t run for task (kind, mb) (kind: 0 = B, 1 = F, 2 = W; NULL = no
+ * work), n = 3 * M.  The dispatcher selects the branch with
+ * cudaGraphSetConditional.  Must be called before the first launch. */
+int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* const* graphs, int32_t n);
 int rrfp_runtime_task_ptr(rrfp_runtime* rt, void** dev_ptr);
 /* Build (first call) and launch one iteration's executor graph on the lane's
  * stream; epoch must increase by one per iteration. Asynchronous. */

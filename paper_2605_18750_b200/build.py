@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
          "-Xptxas", "-v", "-DNDEBUG"]
-LIBS = ["-lcuda", "-lcudart"]
+LIBS = ["-lcudart"]
 
 
 def _sources():

@@ -1,0 +1,397 @@
+// gemm_sm100.cu -- hand-written tcgen05 + TMA bf16 GEMM for the synthetic
+// GPT stage compute, with fused epilogues (K8 bias+GELU,
+// residual add, GELU backward, fp32 weight-grad accumulation).
+//
+//   C[M,N] = sum_k A[m,k] * B[n,k]      (bf16 in, fp32 accumulate in TMEM)
+//
+// Operand majors are template parameters so the three GEMM families of a
+// transformer block map onto the tensor cores without transposes:
+//   forward  Y  = X  . W^T   A K-major  (X [T,K]),  B K-major  (W [N,K])
+//   dgrad    dX = dY . W     A K-major  (dY [T,N]), B MN-major (W [N,K] read as [K x N])
+//   wgrad    dW = dY^T . X   A MN-major (dY [T,N]), B MN-major (X [T,K])
+//
+// Warp-specialised persistent CTA (256 threads, 1 CTA/SM):
+//   warp 0  TMA producer  (4-stage smem ring, mbarrier full/empty)
+//   warp 1  MMA issuer    (one thread, tcgen05.mma 128x256x16, accumulators in TMEM)
+//   warp 2  TMEM allocator (512 columns = 2 accumulator buffers)
+//   warps 4-7 epilogue    (tcgen05.ld -> fused epilogue -> global)
+// The epilogue of tile i overlaps the MMAs of tile i+1 (double-buffered TMEM).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/rrfp_b200.h"
+#include "rrfp_common.h"
+#include "sm100_ptx.cuh"
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 + 256;
+constexpr int TMEM_COLS = 2 * BN;            // two fp32 accumulators of 128 x 256
+
+enum Epi : int {
+  EPI_BF16 = 0,        // C = acc (+ bias)                         -> bf16
+  EPI_BIAS_GELU = 1,   // C = acc + bias (pre-act), C2 = gelu(C)   -> bf16, bf16
+  EPI_RESID = 2,       // C = acc (+ bias) + R                     -> bf16
+  EPI_ACC_F32 = 3,     // C (f32) (+)= acc                         -> f32
+  EPI_GELU_BWD = 4,    // C = acc * gelu'(R)                       -> bf16
+  EPI_F32 = 5,         // C = acc                                  -> f32
+};
+
+struct GemmArgs {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  void* C;
+  long long ldc;
+  void* C2;
+  long long ldc2;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* R;
+  long long ldr;
+  int accumulate;
+  int vec;   // 1 when C/C2/R rows are 16-byte aligned (vector epilogue path allowed)
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float u = k0 * (x + k1 * x * x * x);
+  return 0.5f * x * (1.f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float x2 = x * x;
+  float u = k0 * (x + k1 * x2 * x);
+  float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0,
+                                               uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (row >= g.M) return;
+  const bool full = g.vec && col0 + 32 <= g.N;
+  if (EPI == EPI_ACC_F32 || EPI == EPI_F32) {
+    float* c = reinterpret_cast<float*>(g.C) + (size_t)row * g.ldc + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (EPI == EPI_ACC_F32 && g.accumulate) {
+          float4 p = *reinterpret_cast<const float4*>(c + j);
+          o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(c + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < g.N; ++j)
+        c[j] = (EPI == EPI_ACC_F32 && g.accumulate) ? c[j] + v[j] : v[j];
+    }
+    return;
+  }
+  if (g.bias && EPI != EPI_GELU_BWD) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < g.N) v[j] += __bfloat162float(g.bias[col0 + j]);
+  }
+  if (EPI == EPI_RESID || EPI == EPI_GELU_BWD) {
+    const __nv_bfloat16* rp = g.R + (size_t)row * g.ldr + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 q = *reinterpret_cast<const uint4*>(rp + j);
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          float x = __bfloat162float(h[t]);
+          if (EPI == EPI_RESID) v[j + t] += x;
+          else v[j + t] *= gelu_tanh_grad(x);
+        }
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < g.N; ++j) {
+        float x = __bfloat162float(rp[j]);
+        if (EPI == EPI_RESID) v[j] += x;
+        else v[j] *= gelu_tanh_grad(x);
+      }
+    }
+  }
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(g.C) + (size_t)row * g.ldc + col0;
+  __nv_bfloat16* c2 = EPI == EPI_BIAS_GELU
+                          ? reinterpret_cast<__nv_bfloat16*>(g.C2) + (size_t)row * g.ldc2 + col0
+                          : nullptr;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4 o;
+      o.x = pack_bf16(v[j], v[j + 1]); o.y = pack_bf16(v[j + 2], v[j + 3]);
+      o.z = pack_bf16(v[j + 4], v[j + 5]); o.w = pack_bf16(v[j + 6], v[j + 7]);
+      *reinterpret_cast<uint4*>(c + j) = o;
+      if (EPI == EPI_BIAS_GELU) {
+        uint4 q;
+        q.x = pack_bf16(gelu_tanh(v[j]), gelu_tanh(v[j + 1]));
+        q.y = pack_bf16(gelu_tanh(v[j + 2]), gelu_tanh(v[j + 3]));
+        q.z = pack_bf16(gelu_tanh(v[j + 4]), gelu_tanh(v[j + 5]));
+        q.w = pack_bf16(gelu_tanh(v[j + 6]), gelu_tanh(v[j + 7]));
+        *reinterpret_cast<uint4*>(c2 + j) = q;
+      }
+    }
+  } else {
+    for (int j = 0; j < 32 && col0 + j < g.N; ++j) {
+      c[j] = __float2bfloat16(v[j]);
+      if (EPI == EPI_BIAS_GELU) c2[j] = __float2bfloat16(gelu_tanh(v[j]));
+    }
+  }
+}
+
+template <int EPI, int A_MN, int B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint64_t* full = bars;                  // [STAGES]
+  uint64_t* empty = bars + STAGES;        // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;    // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 128); }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc<TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = g.tiles_m * g.tiles_n;
+  const int kblocks = (g.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+          uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
+          if (!A_MN) {
+            sm100::tma_load_2d(a_dst, &tmA, &full[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              sm100::tma_load_2d(a_dst + j * 64 * BK * 2, &tmA, &full[stage], mb * BM + j * 64, kb * BK);
+          }
+          if (!B_MN) {
+            sm100::tma_load_2d(b_dst, &tmB, &full[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              sm100::tma_load_2d(b_dst + j * 64 * BK * 2, &tmB, &full[stage], nb * BN + j * 64, kb * BK);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a_base = sm100::smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_base = sm100::smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = A_MN ? sm100::umma_desc_sw128(a_base + k * 16 * 128, 64 * BK * 2, 1024)
+                               : sm100::umma_desc_sw128(a_base + k * 32, 16, 1024);
+            uint64_t bd = B_MN ? sm100::umma_desc_sw128(b_base + k * 16 * 128, 64 * BK * 2, 1024)
+                               : sm100::umma_desc_sw128(b_base + k * 32, 16, 1024);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const int row = mb * BM + ew * 32 + lane;
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld32(t_row + c, r);
+        sm100::tmem_ld_wait();
+        if (nb * BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * BN + c, r);
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------- host
+typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn_t get_encode() {
+  static encode_fn_t fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (encode_fn_t)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading dim ld
+// (elements); box = {box_cols, box_rows}, 128-byte swizzle.
+int make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld,
+             int box_cols, int box_rows) {
+  encode_fn_t enc = get_encode();
+  if (!enc) return rrfp_fail(RRFP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return rrfp_fail(RRFP_E_INVALID, "tensor map encode failed (%d): rows=%lld cols=%lld ld=%lld", (int)r,
+                     rows, cols, ld);
+  return RRFP_OK;
+}
+
+int g_num_sms = 0;
+int g_reserve_sms = 0;
+
+template <int EPI, int A_MN, int B_MN>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st) {
+  auto kern = gemm_bf16_sm100<EPI, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr = true;
+  }
+  if (!g_num_sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int tiles = g.tiles_m * g.tiles_n;
+  int sms = g_num_sms - g_reserve_sms;
+  if (sms < 1) sms = 1;
+  int grid = tiles < sms ? tiles : sms;
+  kern<<<grid, 256, SMEM_BYTES, st>>>(ta, tb, g);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+template <int EPI>
+int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                    const GemmArgs& g, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
+  if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
+  if (a_mn && b_mn) return launch<EPI, 1, 1>(ta, tb, g, st);
+  return launch<EPI, 1, 0>(ta, tb, g, st);
+}
+
+}  // namespace
+
+// C[M,N] = sum_k A(m,k) B(n,k) with
+//   A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k]
+//   B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k]
+extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A,
+                              long long lda, const void* B, long long ldb, void* C, long long ldc,
+                              void* C2, long long ldc2, const void* bias, const void* R,
+                              long long ldr, int accumulate, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C) return rrfp_fail(RRFP_E_INVALID, "bad gemm args");
+  if ((lda * 2) % 16 || (ldb * 2) % 16) return rrfp_fail(RRFP_E_INVALID, "leading dims must be 16-byte multiples");
+  if (epi == EPI_BIAS_GELU && !C2) return rrfp_fail(RRFP_E_INVALID, "gelu epilogue needs C2");
+  if ((epi == EPI_RESID || epi == EPI_GELU_BWD) && !R) return rrfp_fail(RRFP_E_INVALID, "epilogue needs R");
+  CUtensorMap ta, tb;
+  int rc = a_mn ? make_map(&ta, A, K, M, lda, 64, BK) : make_map(&ta, A, M, K, lda, BK, BM);
+  if (rc) return rc;
+  rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, BK) : make_map(&tb, B, N, K, ldb, BK, BN);
+  if (rc) return rc;
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.tiles_m = (M + BM - 1) / BM;
+  g.tiles_n = (N + BN - 1) / BN;
+  g.C = C; g.ldc = ldc; g.C2 = C2; g.ldc2 = ldc2;
+  g.bias = (const __nv_bfloat16*)bias;
+  g.R = (const __nv_bfloat16*)R; g.ldr = ldr;
+  g.accumulate = accumulate;
+  const int esz = (epi == EPI_ACC_F32 || epi == EPI_F32) ? 4 : 2;
+  g.vec = ((uintptr_t)C % 16 == 0) && ((ldc * esz) % 16 == 0) &&
+          (!C2 || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
+          (!R || (((uintptr_t)R % 16 == 0) && (ldr * 2) % 16 == 0));
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (epi) {
+    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, g, st);
+  }
+  return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
+}
+
+extern "C" int rrfp_gemm_reserve_sms(int n) {
+  g_reserve_sms = n < 0 ? 0 : n;
+  return RRFP_OK;
+}

@@ -1,0 +1,336 @@
+// ops.cu -- HBM-bound stage-compute kernels of the synthetic GPT block
+// (SURVEY.md K7 LayerNorm fwd/bwd, K10 softmax cross-entropy, embedding,
+// bias-gradient reduction).  bf16 I/O, fp32 statistics and accumulation.
+// Each kernel is a single pass over its tensors: one warp per row, 16-byte
+// vector loads, per-block partial reductions for parameter gradients.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rrfp_b200.h"
+#include "rrfp_common.h"
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
+  uint4 q = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+// ------------------------------------------------------------- LayerNorm
+// y = (x - mean) * rstd * g + b; one warp per row; D = 256 * NV.
+template <int NV>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ g,
+                                                     const __nv_bfloat16* __restrict__ b,
+                                                     __nv_bfloat16* __restrict__ y,
+                                                     float* __restrict__ mean_out,
+                                                     float* __restrict__ rstd_out, int rows,
+                                                     float eps) {
+  constexpr int D = 256 * NV;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const __nv_bfloat16* xr = x + (size_t)warp * D;
+  float v[NV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    load8(xr + (i * 32 + lane) * 8, v[i]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[i][j];
+  }
+  const float mean = warp_sum(s) * (1.f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { float d = v[i][j] - mean; q += d * d; }
+  const float rstd = rsqrtf(warp_sum(q) * (1.f / D) + eps);
+  __nv_bfloat16* yr = y + (size_t)warp * D;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    float gg[8], bb[8], o[8];
+    load8(g + c, gg);
+    load8(b + c, bb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mean) * rstd * gg[j] + bb[j];
+    store8(yr + c, o);
+  }
+  if (lane == 0) { mean_out[warp] = mean; rstd_out[warp] = rstd; }
+}
+
+// dx = rstd * (dxh - xhat * mean(dxh * xhat) - mean(dxh)) + dres, dxh = dy * g
+// dg += sum_rows dy * xhat, db += sum_rows dy.  Two passes over a row (the
+// second hits L1/L2) keep registers low; parameter-gradient partials go to
+// shared memory, then one global atomicAdd per column per block.
+template <int NV>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+    const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db, int rows) {
+  constexpr int D = 256 * NV;
+  __shared__ float s_dg[D], s_db[D];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) { s_dg[i] = 0.f; s_db[i] = 0.f; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps_total) {
+    const float mean = mean_in[row], rstd = rstd_in[row];
+    const __nv_bfloat16* xr = x + (size_t)row * D;
+    const __nv_bfloat16* dr = dy + (size_t)row * D;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 2
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      float xv[8], dv[8], gv[8];
+      load8(xr + c, xv);
+      load8(dr + c, dv);
+      load8(g + c, gv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[j] - mean) * rstd, dh = dv[j] * gv[j];
+        s1 += dh * xh;
+        s2 += dh;
+      }
+    }
+    s1 = warp_sum(s1) * (1.f / D);
+    s2 = warp_sum(s2) * (1.f / D);
+#pragma unroll 2
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      float xv[8], dv[8], gv[8], o[8], rv[8];
+      load8(xr + c, xv);
+      load8(dr + c, dv);
+      load8(g + c, gv);
+      if (dres) load8(dres + (size_t)row * D + c, rv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[j] - mean) * rstd, dh = dv[j] * gv[j];
+        o[j] = rstd * (dh - xh * s1 - s2) + (dres ? rv[j] : 0.f);
+        atomicAdd(&s_dg[c + j], dv[j] * xh);
+        atomicAdd(&s_db[c + j], dv[j]);
+      }
+      store8(dx + (size_t)row * D + c, o);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    if (dg) atomicAdd(&dg[i], s_dg[i]);
+    if (db) atomicAdd(&db[i], s_db[i]);
+  }
+}
+
+// ------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
+                                 const __nv_bfloat16* __restrict__ P, __nv_bfloat16* __restrict__ x,
+                                 int rows, int D) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const __nv_bfloat16* e = E + (size_t)tok[row] * D;
+  const __nv_bfloat16* p = P + (size_t)row * D;
+  for (int c = lane * 8; c < D; c += 256) {
+    float a[8], b[8];
+    load8(e + c, a);
+    load8(p + c, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += b[j];
+    store8(x + (size_t)row * D + c, a);
+  }
+}
+
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
+                                 float* __restrict__ dE, float* __restrict__ dP, int rows, int D) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float* e = dE + (size_t)tok[row] * D;
+  float* p = dP + (size_t)row * D;
+  for (int c = lane * 8; c < D; c += 256) {
+    float a[8];
+    load8(dx + (size_t)row * D + c, a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      atomicAdd(e + c + j, a[j]);
+      p[c + j] += a[j];
+    }
+  }
+}
+
+// ------------------------------------------------------- bias gradients
+// db[n] += sum_r dy[r, n]; block = 256 columns x a slab of rows
+__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ld, float* __restrict__ db,
+                              int rows, int cols, int rows_per_block) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += __bfloat162float(dy[(size_t)r * ld + c]);
+  atomicAdd(&db[c], s);
+}
+
+// ------------------------------------------------------- cross entropy
+// one 512-thread block per row; loss[r] = lse - logit[target]
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
+  v = is_max ? warp_max(v) : warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float t = threadIdx.x < nw ? sh[threadIdx.x] : (is_max ? -INFINITY : 0.f);
+  if (w == 0) t = is_max ? warp_max(t) : warp_sum(t);
+  if (threadIdx.x == 0) sh[0] = t;
+  __syncthreads();
+  float r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(512) xent_fwd_kernel(const __nv_bfloat16* __restrict__ logits, long long ld,
+                                                       const int32_t* __restrict__ target, int V,
+                                                       float* __restrict__ loss, float* __restrict__ lse_out) {
+  __shared__ float sh[32];
+  const __nv_bfloat16* row = logits + (size_t)blockIdx.x * ld;
+  float m = -INFINITY;
+  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+    float f[8];
+    load8(row + c, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if (c + j < V) m = fmaxf(m, f[j]);
+  }
+  m = block_reduce(m, true, sh);
+  float s = 0.f;
+  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+    float f[8];
+    load8(row + c, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if (c + j < V) s += __expf(f[j] - m);
+  }
+  s = block_reduce(s, false, sh);
+  if (threadIdx.x == 0) {
+    const float lse = m + __logf(s);
+    lse_out[blockIdx.x] = lse;
+    loss[blockIdx.x] = lse - __bfloat162float(row[target[blockIdx.x]]);
+  }
+}
+
+// dlogits = (softmax - onehot) * scale, written in place
+__global__ void __launch_bounds__(512) xent_bwd_kernel(__nv_bfloat16* __restrict__ logits, long long ld,
+                                                       const int32_t* __restrict__ target, int V,
+                                                       const float* __restrict__ lse_in, float scale) {
+  __nv_bfloat16* row = logits + (size_t)blockIdx.x * ld;
+  const float lse = lse_in[blockIdx.x];
+  const int t = target[blockIdx.x];
+  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+    float f[8];
+    load8(row + c, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = (__expf(f[j] - lse) - (c + j == t ? 1.f : 0.f)) * scale;
+    store8(row + c, f);
+  }
+}
+
+}  // namespace
+
+#define LAUNCH_NV(KERNEL, D, ...)                                             \
+  switch ((D) / 256) {                                                        \
+    case 1: KERNEL<1><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
+    case 2: KERNEL<2><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
+    case 4: KERNEL<4><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
+    case 8: KERNEL<8><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
+    case 16: KERNEL<16><<<grid, 256, 0, st>>>(__VA_ARGS__); break;            \
+    default: return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported", (int)(D)); \
+  }
+
+extern "C" int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean,
+                                  float* rstd, int rows, int D, float eps, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((rows + 7) / 8);
+  LAUNCH_NV(ln_fwd_kernel, D, (const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
+            (const __nv_bfloat16*)b, (__nv_bfloat16*)y, mean, rstd, rows, eps);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                                  const void* g, const void* dres, void* dx, float* dg, float* db,
+                                  int rows, int D, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int blocks = (rows + 63) / 64;   // 8 warps x 8 rows per block
+  if (blocks > 148) blocks = 148;
+  dim3 grid(blocks);
+  if (D > 4096) return rrfp_fail(RRFP_E_INVALID, "LayerNorm bwd width %d too large", D);
+  LAUNCH_NV(ln_bwd_kernel, D, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd,
+            (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, dg, db, rows);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x, int rows,
+                                  int D, void* stream) {
+  if (D % 8) return rrfp_fail(RRFP_E_INVALID, "embedding width must be a multiple of 8");
+  embed_fwd_kernel<<<(rows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      tok, (const __nv_bfloat16*)E, (const __nv_bfloat16*)P, (__nv_bfloat16*)x, rows, D);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP, int rows,
+                                  int D, void* stream) {
+  if (D % 8) return rrfp_fail(RRFP_E_INVALID, "embedding width must be a multiple of 8");
+  embed_bwd_kernel<<<(rows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      tok, (const __nv_bfloat16*)dx, dE, dP, rows, D);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows, int cols, void* stream) {
+  const int rpb = 128;
+  dim3 grid((cols + 255) / 256, (rows + rpb - 1) / rpb);
+  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)dy, ld, db, rows, cols, rpb);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* target, int rows, int V,
+                             float* loss, float* lse, void* stream) {
+  if (V % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "vocab / ld must be multiples of 8");
+  xent_fwd_kernel<<<rows, 512, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)logits, ld, target, V,
+                                                          loss, lse);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, int V,
+                             const float* lse, float scale, void* stream) {
+  if (V % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "vocab / ld must be multiples of 8");
+  xent_bwd_kernel<<<rows, 512, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)logits, ld, target, V, lse,
+                                                          scale);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
     if (s_exit) {
       if (lane == 0) {
         L->cur_kind = LANE_NONE;
-        cudaGraphSetConditional(L->h_switch, LANE_NONE);
+        cudaGraphSetConditional(L->h_switch, 0xFFFFFFFFu);
         cudaGraphSetConditional(L->h_while, 0);
       }
       return;
@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
       }
       if (s_kind >= 0 && s_kind != RRFP_WAIT) {
         L->t_start = gtimer();
-        cudaGraphSetConditional(L->h_switch, (unsigned)s_kind);
+        unsigned branch = (unsigned)s_kind;
+        if (d.compute_kind == 1) branch = (unsigned)(s_kind * d.M + rrfp_task_mb(L->cur_task));
+        cudaGraphSetConditional(L->h_switch, branch);
       }
     }
     __syncwarp();
@@ -457,7 +459,7 @@ struct rrfp_runtime {
   int32_t* abort_dev;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
-  cudaGraph_t body[3];
+  std::vector<cudaGraph_t> bodies;   // [3 * M] per-(kind, mb) compute graphs
   bool built;
   cudaEvent_t done_ev;
   int KEYS;
@@ -603,12 +605,12 @@ extern "C" int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns,
   return RRFP_OK;
 }
 
-extern "C" int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* graph_f, void* graph_b, void* graph_w) {
-  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+extern "C" int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* const* graphs, int32_t n) {
+  if (!rt || !graphs) return rrfp_fail(RRFP_E_INVALID, "null argument");
   if (rt->built) return rrfp_fail(RRFP_E_INVALID, "bodies must be set before the first launch");
-  rt->body[RRFP_DIR_F] = (cudaGraph_t)graph_f;
-  rt->body[RRFP_DIR_B] = (cudaGraph_t)graph_b;
-  rt->body[RRFP_DIR_W] = (cudaGraph_t)graph_w;
+  if (n != 3 * rt->d.M) return rrfp_fail(RRFP_E_INVALID, "need 3*M body graphs, got %d", n);
+  rt->bodies.assign(n, nullptr);
+  for (int i = 0; i < n; ++i) rt->bodies[i] = (cudaGraph_t)graphs[i];
   return RRFP_OK;
 }
 
@@ -647,22 +649,24 @@ static int build_graph(rrfp_runtime* rt) {
   RRFP_CUDA_TRY(cudaGraphAddNode(&n_while, g, &n_init, 1, &cp));
   cudaGraph_t loop = cp.conditional.phGraph_out[0];
   if ((rc = add_kernel(&n_dec, loop, nullptr, 0, (void*)lane_dispatch_kernel, rt->L))) return rc;
-  RRFP_CUDA_TRY(cudaGraphConditionalHandleCreate(&hs, loop, LANE_NONE, cudaGraphCondAssignDefault));
+  RRFP_CUDA_TRY(cudaGraphConditionalHandleCreate(&hs, loop, 0xFFFFFFFFu, cudaGraphCondAssignDefault));
   cudaGraphNodeParams sp = {};
   sp.type = cudaGraphNodeTypeConditional;
   sp.conditional.handle = hs;
   sp.conditional.type = cudaGraphCondTypeSwitch;
-  sp.conditional.size = 3;
+  const bool per_mb = rt->d.compute_kind == 1;
+  const int nb = per_mb ? 3 * rt->d.M : 3;
+  sp.conditional.size = nb;
   RRFP_CUDA_TRY(cudaGraphAddNode(&n_sw, loop, &n_dec, 1, &sp));
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < nb; ++k) {
     cudaGraph_t b = sp.conditional.phGraph_out[k];
     cudaGraphNode_t n;
-    if (rt->d.compute_kind == 1 && rt->body[k]) {
-      RRFP_CUDA_TRY(cudaGraphAddChildGraphNode(&n, b, nullptr, 0, rt->body[k]));
-    } else if (rt->d.compute_kind == 0) {
-      if ((rc = add_kernel(&n, b, nullptr, 0, (void*)lane_spin_body_kernel, rt->L))) return rc;
+    if (per_mb) {
+      cudaGraph_t body = k < (int)rt->bodies.size() ? rt->bodies[k] : nullptr;
+      if (body) RRFP_CUDA_TRY(cudaGraphAddChildGraphNode(&n, b, nullptr, 0, body));
+      else RRFP_CUDA_TRY(cudaGraphAddEmptyNode(&n, b, nullptr, 0));
     } else {
-      RRFP_CUDA_TRY(cudaGraphAddEmptyNode(&n, b, nullptr, 0));
+      if ((rc = add_kernel(&n, b, nullptr, 0, (void*)lane_spin_body_kernel, rt->L))) return rc;
     }
   }
   if ((rc = add_kernel(&n_comp, loop, &n_sw, 1, (void*)lane_complete_kernel, rt->L))) return rc;

@@ -1,0 +1,55 @@
+"""ctypes front-end of the stage-compute kernels (csrc/*.cu) on torch tensors.
+
+All entry points take torch CUDA tensors, pass raw device pointers through
+the C ABI and launch on torch's current stream (so torch.cuda.graph capture
+records them).  No fallback: a missing library raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+
+EPI_BF16, EPI_BIAS_GELU, EPI_RESID, EPI_ACC_F32, EPI_GELU_BWD, EPI_F32 = range(6)
+
+# number of our own kernel launches issued through this module (graph bodies
+# count them at capture time; bench.py reports launches per step)
+LAUNCHES = [0]
+
+
+def note(n: int = 1):
+    LAUNCHES[0] += n
+
+
+def _p(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ld(t, mn_major=False):
+    return t.stride(0)
+
+
+def gemm(a, b, c, *, epi=EPI_BF16, a_mn=False, b_mn=False, c2=None, bias=None, r=None,
+         accumulate=False, m=None, n=None, k=None):
+    """c = op(a) . op(b)^T with fused epilogue (see csrc/gemm_sm100.cu).
+
+    a: [M, K] (or [K, M] if a_mn); b: [N, K] (or [K, N] if b_mn); row-major, unit inner stride.
+    """
+    M = m if m is not None else (a.shape[1] if a_mn else a.shape[0])
+    K = k if k is not None else (a.shape[0] if a_mn else a.shape[1])
+    N = n if n is not None else (b.shape[1] if b_mn else b.shape[0])
+    L = _lib.lib()
+    note()
+    _lib.check(L.rrfp_gemm_bf16(
+        epi, int(a_mn), int(b_mn), M, N, K, _p(a), C.c_longlong(a.stride(0)), _p(b),
+        C.c_longlong(b.stride(0)), _p(c), C.c_longlong(c.stride(0)), _p(c2),
+        C.c_longlong(c2.stride(0) if c2 is not None else 0), _p(bias), _p(r),
+        C.c_longlong(r.stride(0) if r is not None else 0), int(accumulate), _stream()))
+    return c

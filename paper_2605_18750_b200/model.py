@@ -1,0 +1,448 @@
+"""Synthetic GPT stage compute: the F / B / W task bodies.
+
+A ``StageCompute`` owns one pipeline stage's slice of a GPT stack (embedding
+on stage 0, LM head + softmax cross-entropy on the last stage), its bf16
+weights, fp32 gradient accumulators, per-microbatch activation slots and the
+mailbox buffers its neighbours write into.  ``forward(mb)``,
+``backward_input(mb)`` and ``backward_weight(mb)`` enqueue the task's kernels
+on the current stream; ``capture_bodies()`` records one CUDA graph per
+(kind, mb) that the device dispatcher (csrc/rrfp_exec.cu) selects with a
+SWITCH node, so no host is involved per task.
+
+Kernels: tcgen05/TMA GEMMs with fused bias / GELU / residual / GELU'
+epilogues (csrc/gemm_sm100.cu), LayerNorm fwd/bwd, embedding and softmax
+cross-entropy (csrc/ops.cu).  The attention core is the cuDNN SDPA kernel
+(library, SURVEY.md K9 "library first").
+
+The last kernel of a forward task writes its activation straight into the
+next stage's mailbox slot (peer memory when stages live on different GPUs);
+the last kernel of a backward task does the same with the input gradient.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from . import kernels as K
+
+
+@dataclass(frozen=True)
+class GPTConfig:
+    n_layer: int = 24
+    d_model: int = 2048
+    n_head: int = 16
+    d_ff: int = 8192
+    vocab: int = 50304
+    seq: int = 2048
+    eps: float = 1e-5
+    init_std: float = 0.02
+
+    @property
+    def d_head(self):
+        return self.d_model // self.n_head
+
+    def flops_per_layer(self):
+        """(F, B-input, W) matmul FLOPs of one layer for one microbatch."""
+        s, d, f = self.seq, self.d_model, self.d_ff
+        gemm = 2 * s * d * (3 * d + d + 2 * f)
+        attn = 2 * 2 * s * s * d / 2           # QK^T and PV, causal half
+        return gemm + attn, gemm + 2 * attn, gemm
+
+    def flops_head(self):
+        return 2 * self.seq * self.d_model * self.vocab
+
+
+GPT_1P3B = GPTConfig()
+GPT_7B = GPTConfig(n_layer=32, d_model=4096, n_head=32, d_ff=16384)
+
+
+def split_layers(n_layer: int, n_stages: int, stage: int):
+    base, extra = divmod(n_layer, n_stages)
+    lo = stage * base + min(stage, extra)
+    return list(range(lo, lo + base + (1 if stage < extra else 0)))
+
+
+def _gen(device, seed):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return g
+
+
+def init_layer_params(cfg: GPTConfig, layer: int, device, seed: int):
+    """Deterministic per GLOBAL layer index, so every PP split sees the same model."""
+    g = _gen(device, seed * 100003 + layer)
+    d, f = cfg.d_model, cfg.d_ff
+    std, out_std = cfg.init_std, cfg.init_std / math.sqrt(2 * cfg.n_layer)
+    bf = torch.bfloat16
+
+    def n(*shape, s=std):
+        return (torch.randn(*shape, generator=g, device=device) * s).to(bf)
+
+    def small(*shape):
+        return (torch.randn(*shape, generator=g, device=device) * 0.02).to(bf)
+
+    return {
+        "ln1_g": (1.0 + small(d).float()).to(bf), "ln1_b": small(d),
+        "w_qkv": n(3 * d, d), "b_qkv": small(3 * d),
+        "w_o": n(d, d, s=out_std), "b_o": small(d),
+        "ln2_g": (1.0 + small(d).float()).to(bf), "ln2_b": small(d),
+        "w_1": n(f, d), "b_1": small(f),
+        "w_2": n(d, f, s=out_std), "b_2": small(d),
+    }
+
+
+def init_embed_params(cfg: GPTConfig, device, seed: int):
+    g = _gen(device, seed * 100003 + 77777)
+    bf = torch.bfloat16
+    return {"wte": (torch.randn(cfg.vocab, cfg.d_model, generator=g, device=device) * cfg.init_std).to(bf),
+            "wpe": (torch.randn(cfg.seq, cfg.d_model, generator=g, device=device) * cfg.init_std).to(bf)}
+
+
+def init_head_params(cfg: GPTConfig, device, seed: int):
+    g = _gen(device, seed * 100003 + 99991)
+    bf = torch.bfloat16
+    d = cfg.d_model
+    return {"lnf_g": (1.0 + 0.02 * torch.randn(d, generator=g, device=device)).to(bf),
+            "lnf_b": (0.02 * torch.randn(d, generator=g, device=device)).to(bf),
+            "w_lm": (torch.randn(cfg.vocab, d, generator=g, device=device) * cfg.init_std).to(bf)}
+
+
+def synthetic_batch(cfg: GPTConfig, n_mb: int, seed: int, device):
+    """Tokens / next-token targets uniform in [0, V) from torch.Generator(seed)."""
+    g = _gen(device, seed)
+    toks = torch.randint(0, cfg.vocab, (n_mb, cfg.seq + 1), generator=g, device=device,
+                         dtype=torch.int32)
+    return toks[:, :-1].contiguous(), toks[:, 1:].contiguous()
+
+
+def _ln_fwd(x, g, b, y, mean, rstd, eps):
+    K.note()
+    L = _lib.lib()
+    _lib.check(L.rrfp_layernorm_fwd(K._p(x), K._p(g), K._p(b), K._p(y), K._p(mean), K._p(rstd),
+                                    x.shape[0], x.shape[1], C.c_float(eps), K._stream()))
+
+
+def _ln_bwd(dy, x, mean, rstd, g, dres, dx, dg, db):
+    K.note()
+    L = _lib.lib()
+    _lib.check(L.rrfp_layernorm_bwd(K._p(dy), K._p(x), K._p(mean), K._p(rstd), K._p(g),
+                                    K._p(dres), K._p(dx), K._p(dg), K._p(db), x.shape[0],
+                                    x.shape[1], K._stream()))
+
+
+def _bias_grad(dy, db):
+    K.note()
+    _lib.check(_lib.lib().rrfp_bias_grad(K._p(dy), C.c_longlong(dy.stride(0)), K._p(db),
+                                         dy.shape[0], dy.shape[1], K._stream()))
+
+
+class RawBuffer:
+    """A device buffer given by address (e.g. a peer mailbox opened over CUDA IPC)."""
+
+    def __init__(self, ptr: int, shape, stride0):
+        self.ptr, self.shape, self._s0 = ptr, tuple(shape), stride0
+
+    def data_ptr(self):
+        return self.ptr
+
+    def stride(self, i):
+        return self._s0 if i == 0 else 1
+
+
+class StageCompute:
+    def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
+                 decompose: bool = False, seed: int = 1234, data_seed: int = 0):
+        self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
+        self.device = torch.device(device)
+        self.first, self.last = stage == 0, stage == n_stages - 1
+        self.decompose = decompose
+        self.layers = split_layers(cfg.n_layer, n_stages, stage)
+        S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
+        dev, bf = self.device, torch.bfloat16
+        with torch.no_grad():
+            self.p = [init_layer_params(cfg, l, dev, seed) for l in self.layers]
+            self.emb = init_embed_params(cfg, dev, seed) if self.first else None
+            self.head = init_head_params(cfg, dev, seed) if self.last else None
+        self.g = [{k: torch.zeros(v.shape, device=dev) for k, v in p.items()} for p in self.p]
+        self.g_emb = {k: torch.zeros(v.shape, device=dev) for k, v in self.emb.items()} if self.first else None
+        self.g_head = {k: torch.zeros(v.shape, device=dev) for k, v in self.head.items()} if self.last else None
+        # synthetic data (stage 0 reads tokens, last stage reads targets)
+        toks, tgts = synthetic_batch(cfg, n_mb, data_seed, dev)
+        self.tokens = toks if self.first else None
+        self.targets = tgts if self.last else None
+        # mailboxes written by neighbours: F input (stage > 0), B input (stage < N-1)
+        self.fwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf) if not self.first else None
+        self.bwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf) if not self.last else None
+        self.fwd_out = None   # per-mb destination buffers (set by connect_outputs)
+        self.bwd_out = None
+        # activation slots, one per microbatch (static addresses for graph capture)
+        nl = len(self.layers)
+        e = lambda *s: torch.empty(*s, device=dev, dtype=bf)
+        f32 = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
+        self.x0 = e(n_mb, S, D) if self.first else None
+        self.h1, self.qkv, self.o, self.x2 = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D), e(n_mb, nl, S, D), e(n_mb, nl, S, D)
+        self.h2, self.pre, self.act, self.y = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd), e(n_mb, nl, S, Fd), e(n_mb, nl, S, D)
+        self.m1, self.r1, self.m2, self.r2 = f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S)
+        self.attn_aux = [[None] * nl for _ in range(n_mb)]
+        if self.last:
+            self.hf, self.mf, self.rf = e(n_mb, S, D), f32(n_mb, S), f32(n_mb, S)
+            self.logits = e(n_mb, S, V)
+            self.loss = torch.zeros(n_mb, S, device=dev)
+            self.lse = f32(n_mb, S)
+        # scratch shared by all bodies of this stage (bodies never overlap on a lane)
+        self.d_a = e(S, D)
+        self.d_b = e(S, D)
+        self.d_big = e(S, Fd)
+        self.d_qkv_s = e(S, 3 * D)
+        self.d_head = e(S, D)
+        if decompose:   # gradients kept per (mb, layer) for the deferred W task
+            self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd)
+            self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D)
+            if self.first:
+                self.gx0 = e(n_mb, S, D)
+        self.graphs = {}
+        self.kernel_counts = {}   # (kind, mb) -> our kernel launches in that body
+
+    # ------------------------------------------------------------ wiring
+    def connect_outputs(self, fwd_out=None, bwd_out=None):
+        """fwd_out / bwd_out: per-mb destination (tensor or RawBuffer) in the
+        next / previous stage's mailbox."""
+        self.fwd_out, self.bwd_out = fwd_out, bwd_out
+
+    def param_bytes(self):
+        return sum(t.numel() * 2 for p in self.p for t in p.values())
+
+    # ------------------------------------------------------------ forward
+    def _attn_fwd(self, qkv, mb, li):
+        S, H, Dh, D = self.cfg.seq, self.cfg.n_head, self.cfg.d_head, self.cfg.d_model
+        q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        v = qkv[:, 2 * D:].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        out = torch.ops.aten._scaled_dot_product_cudnn_attention(
+            q, k, v, None, True, 0.0, True, False, scale=1.0 / math.sqrt(Dh))
+        o4, lse = out[0], out[1]
+        self.attn_aux[mb][li] = (o4, lse, out[2], out[3], out[4], out[5], out[6], out[7])
+        self.o[mb, li].view(S, H, Dh).copy_(o4[0].transpose(0, 1))
+
+    def forward(self, mb: int):
+        cfg = self.cfg
+        S, D = cfg.seq, cfg.d_model
+        if self.first:
+            K.note()
+            _lib.check(_lib.lib().rrfp_embedding_fwd(
+                K._p(self.tokens[mb]), K._p(self.emb["wte"]), K._p(self.emb["wpe"]),
+                K._p(self.x0[mb]), S, D, K._stream()))
+            x = self.x0[mb]
+        else:
+            x = self.fwd_in[mb]
+        nl = len(self.layers)
+        for li, p in enumerate(self.p):
+            _ln_fwd(x, p["ln1_g"], p["ln1_b"], self.h1[mb, li], self.m1[mb, li], self.r1[mb, li], cfg.eps)
+            K.gemm(self.h1[mb, li], p["w_qkv"], self.qkv[mb, li], bias=p["b_qkv"])
+            self._attn_fwd(self.qkv[mb, li], mb, li)
+            K.gemm(self.o[mb, li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
+            _ln_fwd(self.x2[mb, li], p["ln2_g"], p["ln2_b"], self.h2[mb, li], self.m2[mb, li],
+                    self.r2[mb, li], cfg.eps)
+            K.gemm(self.h2[mb, li], p["w_1"], self.pre[mb, li], epi=K.EPI_BIAS_GELU,
+                   c2=self.act[mb, li], bias=p["b_1"])
+            out = self._layer_output(mb, li)    # last layer: the next stage's mailbox slot
+            K.gemm(self.act[mb, li], p["w_2"], out, epi=K.EPI_RESID, bias=p["b_2"], r=self.x2[mb, li],
+                   m=S, n=D, k=cfg.d_ff)
+            x = out
+        if self.last:
+            h = self.head
+            _ln_fwd(x, h["lnf_g"], h["lnf_b"], self.hf[mb], self.mf[mb], self.rf[mb], cfg.eps)
+            K.gemm(self.hf[mb], h["w_lm"], self.logits[mb])
+            K.note()
+            _lib.check(_lib.lib().rrfp_xent_fwd(
+                K._p(self.logits[mb]), C.c_longlong(cfg.vocab), K._p(self.targets[mb]), S,
+                cfg.vocab, K._p(self.loss[mb]), K._p(self.lse[mb]), K._stream()))
+
+    def _layer_input(self, mb, li):
+        if li > 0:
+            return self.y[mb, li - 1]
+        return self.x0[mb] if self.first else self.fwd_in[mb]
+
+    def _layer_output(self, mb, li):
+        if li == len(self.layers) - 1 and not self.last and self.fwd_out is not None:
+            return self.fwd_out[mb]
+        return self.y[mb, li]
+
+    # ----------------------------------------------------------- backward
+    def backward_input(self, mb: int):
+        """B task: input gradients (plus weight gradients unless decomposed).
+
+        Gradient buffers: dy of layer li lives in ``d_a`` (or the mailbox /
+        the decomposed slot ``gy[mb, li]``); d_x2 in ``d_b`` (or ``gx2``); the
+        layer-input gradient is written where the next-lower layer reads its
+        dy, and for layer 0 straight into the previous stage's mailbox.
+        """
+        cfg = self.cfg
+        S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
+        fused_w = not self.decompose
+        nl = len(self.layers)
+        dec = self.decompose
+
+        def dy_slot(li):
+            return self.gy[mb, li] if dec else self.d_a
+
+        if self.last:
+            h, gh = self.head, self.g_head
+            scale = 1.0 / (S * self.M)
+            K.note()
+            _lib.check(_lib.lib().rrfp_xent_bwd(
+                K._p(self.logits[mb]), C.c_longlong(V), K._p(self.targets[mb]), S, V,
+                K._p(self.lse[mb]), C.c_float(scale), K._stream()))
+            K.gemm(self.logits[mb], h["w_lm"], self.d_head, b_mn=True, m=S, n=D, k=V)
+            if fused_w:
+                K.gemm(self.logits[mb], self.hf[mb], gh["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=V, n=D, k=S)
+            dy = dy_slot(nl - 1)
+            _ln_bwd(self.d_head, self.y[mb, nl - 1], self.mf[mb], self.rf[mb], h["lnf_g"], None, dy,
+                    gh["lnf_g"], gh["lnf_b"])
+        else:
+            dy = self.bwd_in[mb]
+            if dec:
+                self.gy[mb, nl - 1].copy_(dy)
+                dy = self.gy[mb, nl - 1]
+        for li in reversed(range(nl)):
+            p, g = self.p[li], self.g[li]
+            x = self._layer_input(mb, li)
+            # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)
+            d_pre = self.gpre[mb, li] if dec else self.d_big
+            K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=self.pre[mb, li],
+                   m=S, n=Fd, k=D)
+            if fused_w:
+                K.gemm(dy, self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                       accumulate=True, m=D, n=Fd, k=S)
+                _bias_grad(dy, g["b_2"])
+            # FC1 dgrad -> LN2 backward (+ residual grad dy)
+            K.gemm(d_pre, p["w_1"], self.d_head, b_mn=True, m=S, n=D, k=Fd)
+            if fused_w:
+                K.gemm(d_pre, self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                       accumulate=True, m=Fd, n=D, k=S)
+                _bias_grad(d_pre, g["b_1"])
+            d_x2 = self.gx2[mb, li] if dec else self.d_b
+            _ln_bwd(self.d_head, self.x2[mb, li], self.m2[mb, li], self.r2[mb, li], p["ln2_g"], dy,
+                    d_x2, g["ln2_g"], g["ln2_b"])
+            # out-proj dgrad -> attention backward -> QKV dgrad
+            K.gemm(d_x2, p["w_o"], self.d_head, b_mn=True, m=S, n=D, k=D)
+            if fused_w:
+                K.gemm(d_x2, self.o[mb, li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                       accumulate=True, m=D, n=D, k=S)
+                _bias_grad(d_x2, g["b_o"])
+            d_qkv = self.gqkv[mb, li] if dec else self.d_qkv_s
+            self._attn_bwd(mb, li, self.d_head, d_qkv)
+            K.gemm(d_qkv, p["w_qkv"], self.d_head, b_mn=True, m=S, n=D, k=3 * D)
+            if fused_w:
+                K.gemm(d_qkv, self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                       accumulate=True, m=3 * D, n=D, k=S)
+                _bias_grad(d_qkv, g["b_qkv"])
+            # LN1 backward (+ residual d_x2) -> gradient of the layer input
+            if li > 0:
+                dx = dy_slot(li - 1)
+            elif not self.first:
+                dx = self.bwd_out[mb] if self.bwd_out is not None else self.d_a
+            else:
+                dx = self.gx0[mb] if dec else self.d_a
+            _ln_bwd(self.d_head, x, self.m1[mb, li], self.r1[mb, li], p["ln1_g"], d_x2, dx,
+                    g["ln1_g"], g["ln1_b"])
+            dy = dx
+        if self.first and fused_w:
+            K.note()
+            _lib.check(_lib.lib().rrfp_embedding_bwd(
+                K._p(self.tokens[mb]), K._p(dy), K._p(self.g_emb["wte"]), K._p(self.g_emb["wpe"]),
+                S, D, K._stream()))
+
+    def _attn_bwd(self, mb, li, d_o, d_qkv):
+        cfg = self.cfg
+        S, H, Dh, D = cfg.seq, cfg.n_head, cfg.d_head, cfg.d_model
+        qkv = self.qkv[mb, li]
+        q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        v = qkv[:, 2 * D:].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        o4, lse, cq, ck, mq, mk, ps, po = self.attn_aux[mb][li]
+        go = d_o.view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+            go, q, k, v, o4, lse, ps, po, torch.empty(0, device=self.device), cq, ck, mq, mk, 0.0,
+            True, scale=1.0 / math.sqrt(Dh))
+        d_qkv[:, :D].view(S, H, Dh).copy_(dq[0].transpose(0, 1))
+        d_qkv[:, D:2 * D].view(S, H, Dh).copy_(dk[0].transpose(0, 1))
+        d_qkv[:, 2 * D:].view(S, H, Dh).copy_(dv[0].transpose(0, 1))
+
+    def backward_weight(self, mb: int):
+        """W task (decomposed backward): weight gradients from saved inputs/grads."""
+        if not self.decompose:
+            return
+        cfg = self.cfg
+        S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
+        for li in reversed(range(len(self.layers))):
+            g = self.g[li]
+            K.gemm(self.gy[mb, li], self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
+                   b_mn=True, accumulate=True, m=D, n=Fd, k=S)
+            _bias_grad(self.gy[mb, li], g["b_2"])
+            K.gemm(self.gpre[mb, li], self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
+                   b_mn=True, accumulate=True, m=Fd, n=D, k=S)
+            _bias_grad(self.gpre[mb, li], g["b_1"])
+            K.gemm(self.gx2[mb, li], self.o[mb, li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
+                   b_mn=True, accumulate=True, m=D, n=D, k=S)
+            _bias_grad(self.gx2[mb, li], g["b_o"])
+            K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                   b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
+            _bias_grad(self.gqkv[mb, li], g["b_qkv"])
+        if self.last:
+            K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
+                   b_mn=True, accumulate=True, m=cfg.vocab, n=D, k=S)
+        if self.first:
+            K.note()
+            _lib.check(_lib.lib().rrfp_embedding_bwd(
+                K._p(self.tokens[mb]), K._p(self.gx0[mb]), K._p(self.g_emb["wte"]),
+                K._p(self.g_emb["wpe"]), S, D, K._stream()))
+
+    def zero_grads(self):
+        for gd in self.g + ([self.g_emb] if self.g_emb else []) + ([self.g_head] if self.g_head else []):
+            for t in gd.values():
+                t.zero_()
+        if self.last:
+            self.loss.zero_()
+
+    # ----------------------------------------------------------- capture
+    def run_task(self, kind: str, mb: int):
+        if kind == "F":
+            self.forward(mb)
+        elif kind == "B":
+            self.backward_input(mb)
+        else:
+            self.backward_weight(mb)
+
+    def capture_bodies(self, stream=None):
+        """One CUDA graph per (kind, mb); returns 3*M raw cudaGraph_t handles
+        indexed kind*M + mb with kind B=0, F=1, W=2 (None where no work)."""
+        kinds = ["B", "F", "W"] if self.decompose else ["B", "F"]
+        stream = stream or torch.cuda.Stream(self.device)
+        # warm-up: run every body once eagerly (cuDNN plan selection, module loads)
+        with torch.cuda.stream(stream):
+            for mb in range(self.M):
+                for kind in ("F", "B", "W") if self.decompose else ("F", "B"):
+                    self.run_task(kind, mb)
+        stream.synchronize()
+        self.zero_grads()
+        raw = [None] * (3 * self.M)
+        for kind in kinds:
+            ki = {"B": 0, "F": 1, "W": 2}[kind]
+            for mb in range(self.M):
+                g = torch.cuda.CUDAGraph()
+                before = K.LAUNCHES[0]
+                with torch.cuda.graph(g, stream=stream):
+                    self.run_task(kind, mb)
+                self.kernel_counts[(kind, mb)] = K.LAUNCHES[0] - before
+                self.graphs[(kind, mb)] = g
+                raw[ki * self.M + mb] = g.raw_cuda_graph()
+        torch.cuda.synchronize(self.device)
+        return raw
+

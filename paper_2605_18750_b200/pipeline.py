@@ -1,0 +1,115 @@
+"""Readiness-driven pipeline training iteration of the synthetic GPT on device lanes.
+
+``GpuPipeline`` ties the pieces together for one process:
+  * one ``StageCompute`` per local stage (model.py) -- weights, grads, slots,
+    mailboxes; neighbours' mailboxes are wired so the last kernel of a task
+    writes its payload straight into the receiver's slot;
+  * one CUDA graph per (kind, microbatch) per stage, captured once;
+  * one device lane per stage (runtime.LaneGroup, compute_kind=1) whose
+    dispatcher arbitrates (mode "free"), follows 1F1B ("fixed") or follows
+    the replayed virtual-clock order ("replay") and launches the captured
+    bodies through a SWITCH node.
+
+``step()`` = one training iteration (all M microbatches: F, B and, with the
+BFW hint, W) -> mean loss; the host launches ONE graph per lane per step.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .arbitration import HintOrder, TpGroup
+from .jitter import JitterConfig
+from .model import GPTConfig, RawBuffer, StageCompute
+from .runtime import LaneGroup, wall_trace
+from .workload import BACKWARD, FORWARD, WEIGHT, TaskId, Workload
+
+
+def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
+                     f_us=None, b_us=None, w_us=None) -> Workload:
+    """A Workload describing the GPT iteration (latencies = nominal per-task µs).
+
+    Only the structure matters to the free-running lanes (real kernels set
+    the durations); the latency values feed the jitter EMA and the
+    replay-mode virtual clock.
+    """
+    lat = {}
+    for s in range(n_stages):
+        for mb in range(n_mb):
+            lat[TaskId(s, mb, 0, FORWARD)] = int(f_us[s] if f_us else 1000)
+            lat[TaskId(s, mb, 0, BACKWARD)] = int(b_us[s] if b_us else 2000)
+            if decompose:
+                lat[TaskId(s, mb, 0, WEIGHT)] = int(w_us[s] if w_us else 1000)
+    return Workload(num_stages=n_stages, num_microbatches=n_mb, num_chunks=1, tp_group_size=1,
+                    latency=lat, decompose_backward=decompose)
+
+
+class GpuPipeline:
+    def __init__(self, cfg: GPTConfig, n_stages: int, n_mb: int, *, hint="bf", buffer_limit=32,
+                 mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
+                 devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
+                 schedule=None, comm_delay=None):
+        if isinstance(hint, str):
+            hint = HintOrder.parse(hint)
+        if decompose is None:
+            decompose = hint.kind == "bfw"
+        self.cfg, self.N, self.M, self.hint = cfg, n_stages, n_mb, hint
+        devices = devices or [0] * n_stages
+        f_us, b_us, w_us = stage_latency_us or (None, None, None)
+        w = nominal_workload(cfg, n_stages, n_mb, decompose, f_us, b_us, w_us)
+        if comm_delay is not None:
+            w = Workload(num_stages=w.num_stages, num_microbatches=w.num_microbatches,
+                         num_chunks=1, tp_group_size=1, latency=w.latency, comm_delay=comm_delay,
+                         decompose_backward=decompose)
+        self.workload = w
+        self.stages = [StageCompute(cfg, s, n_stages, n_mb, torch.device("cuda", devices[s]),
+                                    decompose=decompose, seed=model_seed, data_seed=data_seed)
+                       for s in range(n_stages)]
+        for s, st in enumerate(self.stages):
+            nxt = self.stages[s + 1] if s + 1 < n_stages else None
+            prv = self.stages[s - 1] if s > 0 else None
+            st.connect_outputs(fwd_out=[nxt.fwd_in[mb] for mb in range(n_mb)] if nxt else None,
+                               bwd_out=[prv.bwd_in[mb] for mb in range(n_mb)] if prv else None)
+        bodies = {(s, 0): st.capture_bodies() for s, st in enumerate(self.stages)}
+        self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
+                               placement=[[d] for d in devices], bodies=bodies, compute_kind=1,
+                               schedule=schedule)
+        self.last_events = None
+
+    def step(self, watchdog_secs: float = 120.0, zero_grads: bool = True):
+        """One iteration; returns (loss tensor on device, raw events, t0)."""
+        if zero_grads:
+            for st in self.stages:
+                st.zero_grads()
+        events, t0s = self.group.run_iteration(watchdog_secs)
+        self.last_events = (events, min(t0s))
+        last = self.stages[-1]
+        return last.loss.sum() / (self.cfg.seq * self.M)
+
+    def launch(self, zero_grads: bool = True):
+        """Asynchronous step (for timing loops): enqueue, do not wait."""
+        if zero_grads:
+            for st in self.stages:
+                st.zero_grads()
+        self.group.launch()
+
+    def wait(self, watchdog_secs: float = 120.0):
+        events, t0s = self.group.wait(watchdog_secs)
+        self.last_events = (events, min(t0s))
+        return events
+
+    def kernel_launches_per_step(self):
+        """Our kernels launched per iteration: every task body (captured counts)
+        plus the lane's dispatch + complete kernels per task and init/final."""
+        n = 0
+        for st in self.stages:
+            n += sum(st.kernel_counts.values())
+            n += 2 * len(st.kernel_counts) + 2
+        return n
+
+    def trace(self):
+        ev, t0 = self.last_events
+        return wall_trace(self.workload, ev, t0)
+
+    def close(self):
+        self.group.close()

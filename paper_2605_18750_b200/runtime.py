@@ -143,8 +143,9 @@ class LaneGroup:
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
                                                       _ptr(fixed)))
             if bodies is not None:
-                gf, gb, gw = bodies[(s, k)]
-                _lib.check(self.L.rrfp_runtime_set_bodies(h, gf, gb, gw))
+                arr = bodies[(s, k)]          # 3*M raw cudaGraph_t handles (kind*M + mb)
+                carr = (C.c_void_p * len(arr))(*[C.c_void_p(x or 0) for x in arr])
+                _lib.check(self.L.rrfp_runtime_set_bodies(h, carr, len(arr)))
         self.cap = cap
         self.epoch = 0
         if len(self.local) == n * r:
@@ -197,8 +198,11 @@ class LaneGroup:
         self.connect(inboxes)
 
     def launch(self):
+        import torch
         self.epoch += 1
         for lane, h in self.lanes.items():
+            st = self.streams[lane]
+            st.wait_stream(torch.cuda.current_stream(st.device))
             _lib.check(self.L.rrfp_runtime_launch(h, self.epoch,
                                                   C.c_void_p(self.streams[lane].cuda_stream)))
 

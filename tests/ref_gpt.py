@@ -1,0 +1,73 @@
+"""Plain PyTorch fp32 reference of the synthetic GPT (numerics oracle for the
+floating-point stage compute): same weights (upcast), same tokens, no pipeline."""
+import math
+
+import torch
+import torch.nn.functional as F
+
+
+def ln(x, g, b, eps):
+    return F.layer_norm(x, (x.shape[-1],), g, b, eps)
+
+
+def reference_loss_and_grads(cfg, stages):
+    """stages: list of StageCompute (any PP split).  Returns (loss, {name: grad})."""
+    params = {}
+    for st in stages:
+        for li, lid in enumerate(st.layers):
+            for k, v in st.p[li].items():
+                params[f"L{lid}.{k}"] = v.float().clone().requires_grad_(True)
+        if st.first:
+            for k, v in st.emb.items():
+                params[k] = v.float().clone().requires_grad_(True)
+        if st.last:
+            for k, v in st.head.items():
+                params[k] = v.float().clone().requires_grad_(True)
+    first, last = stages[0], stages[-1]
+    M, S, D, H = first.M, cfg.seq, cfg.d_model, cfg.n_head
+    Dh = D // H
+    total = 0.0
+    for mb in range(M):
+        tok = first.tokens[mb].long()
+        x = params["wte"][tok] + params["wpe"]
+        for lid in range(cfg.n_layer):
+            p = {k.split(".", 1)[1]: v for k, v in params.items() if k.startswith(f"L{lid}.")}
+            h = ln(x, p["ln1_g"], p["ln1_b"], cfg.eps)
+            qkv = h @ p["w_qkv"].t() + p["b_qkv"]
+            q, k, v = (qkv[:, i * D:(i + 1) * D].view(S, H, Dh).transpose(0, 1) for i in range(3))
+            o = F.scaled_dot_product_attention(q, k, v, is_causal=True, scale=1 / math.sqrt(Dh))
+            o = o.transpose(0, 1).reshape(S, D)
+            x2 = x + o @ p["w_o"].t() + p["b_o"]
+            h2 = ln(x2, p["ln2_g"], p["ln2_b"], cfg.eps)
+            a = F.gelu(h2 @ p["w_1"].t() + p["b_1"], approximate="tanh")
+            x = x2 + a @ p["w_2"].t() + p["b_2"]
+        hf = ln(x, params["lnf_g"], params["lnf_b"], cfg.eps)
+        logits = hf @ params["w_lm"].t()
+        total = total + F.cross_entropy(logits, last.targets[mb].long(), reduction="sum")
+    loss = total / (M * S)
+    loss.backward()
+    return loss.item(), {k: v.grad for k, v in params.items()}
+
+
+def device_grads(stages):
+    out = {}
+    for st in stages:
+        for li, lid in enumerate(st.layers):
+            for k, v in st.g[li].items():
+                out[f"L{lid}.{k}"] = v
+        if st.first:
+            out.update(st.g_emb)
+        if st.last:
+            out.update(st.g_head)
+    return out
+
+
+def compare(ref, got, cos_min=0.99, rel_max=0.05):
+    bad = []
+    for k, r in ref.items():
+        g = got[k].float()
+        cos = torch.nn.functional.cosine_similarity(r.flatten(), g.flatten(), dim=0).item()
+        rel = ((r - g).norm() / (r.norm() + 1e-12)).item()
+        if cos < cos_min or rel > rel_max:
+            bad.append((k, round(cos, 4), round(rel, 4)))
+    return bad

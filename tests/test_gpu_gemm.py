@@ -1,0 +1,74 @@
+"""tcgen05/TMA GEMM numerics against a torch fp32 reference of the same op."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(*shape, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
+
+
+def _close(got, want, tol=2e-2):
+    err = (got.float() - want).abs().max().item()
+    ref = want.abs().max().item() + 1e-6
+    assert err / ref < tol, (err, ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (2048, 6144, 2048),
+                                   (384, 300, 192), (200, 256, 128)])
+def test_gemm_forward_kk(M, N, K):
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(0)
+    a, b = _rand(M, K), _rand(N, K)
+    bias = _rand(N)
+    c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    Kn.gemm(a, b, c, bias=bias)
+    torch.cuda.synchronize()
+    _close(c, a.float() @ b.float().t() + bias.float())
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (2048, 2048, 8192)])
+def test_gemm_dgrad_kmn(M, N, K):
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(1)
+    dy, w = _rand(M, K), _rand(K, N)       # dX[M,N] = dY[M,K] . W[K,N]
+    c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    Kn.gemm(dy, w, c, b_mn=True)
+    torch.cuda.synchronize()
+    _close(c, dy.float() @ w.float())
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (6144, 2048, 2048)])
+def test_gemm_wgrad_mnmn_accumulate(M, N, K):
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(2)
+    dy, x = _rand(K, M), _rand(K, N)       # dW[M,N] += dY^T . X, contraction over K tokens
+    acc = torch.randn(M, N, device="cuda")
+    want = acc + dy.float().t() @ x.float()
+    Kn.gemm(dy, x, acc, epi=Kn.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True)
+    torch.cuda.synchronize()
+    _close(acc, want, 1e-2)
+
+
+def test_gemm_fused_epilogues():
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(3)
+    M, N, K = 256, 512, 256
+    a, b, bias, res = _rand(M, K), _rand(N, K), _rand(N), _rand(M, N)
+    ref = a.float() @ b.float().t() + bias.float()
+    pre = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty_like(pre)
+    Kn.gemm(a, b, pre, epi=Kn.EPI_BIAS_GELU, c2=act, bias=bias)
+    out = torch.empty_like(pre)
+    Kn.gemm(a, b, out, epi=Kn.EPI_RESID, bias=bias, r=res)
+    gb = torch.empty_like(pre)
+    Kn.gemm(a, b, gb, epi=Kn.EPI_GELU_BWD, r=res)
+    torch.cuda.synchronize()
+    _close(pre, ref)
+    _close(act, torch.nn.functional.gelu(ref, approximate="tanh"))
+    _close(out, ref + res.float())
+    x = res.float()
+    t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+    g = 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+    _close(gb, (a.float() @ b.float().t()) * g)
