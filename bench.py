@@ -217,103 +217,156 @@ def gemm_roofline(cfg, peak_tf):
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
-    if world > 1:
-        raise SystemExit("multi-GPU pipeline bench: see bench_mp (not in this build)")
     torch.cuda.set_device(local)
     from paper_2605_18750_b200.model import GPTConfig
-    from paper_2605_18750_b200.pipeline import GpuPipeline
     from paper_2605_18750_b200.jitter import PRESETS
     cfg = GPTConfig(n_layer=args.layers)
-    n = 1
+    n = world
     hint = "bf" if args.hint == "1f1b" else args.hint
     mode = "fixed" if args.hint == "1f1b" else "free"
+    dist = None
     t_build = time.perf_counter()
-    pipe = GpuPipeline(cfg, n, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2605_18750_b200.distributed import DistPipeline
+        pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
+        stages = [pipe.stage]
+    else:
+        from paper_2605_18750_b200.pipeline import GpuPipeline
+        pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
+        stages = pipe.stages
     t_build = time.perf_counter() - t_build
-    st0, last = pipe.stages[0], pipe.stages[-1]
-    # host inputs for the end-to-end leg (pinned)
-    tok_h = st0.tokens.cpu().pin_memory()
-    tgt_h = last.targets.cpu().pin_memory()
+    first = stages[0] if stages[0].first else None
+    last = stages[-1] if stages[-1].last else None
+    tok_h = first.tokens.cpu().pin_memory() if first else None
+    tgt_h = last.targets.cpu().pin_memory() if last else None
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
     for _ in range(args.warmup):
         pipe.step()
-    torch.cuda.synchronize()
-    lane_stream = pipe.group.streams[(0, 0)]
+    barrier()
+    lane_stream = pipe.group.streams[next(iter(pipe.group.streams))]
     peak_sus, peak_burst, hbm, peak_kind = load_peaks()
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(lane_stream)
         for _ in range(args.steps):
             pipe.launch()
             pipe.wait()
         e1.record(lane_stream)
-        torch.cuda.synchronize()
+        barrier()
         ms = e0.elapsed_time(e1) / args.steps
         # end-to-end through the public API with host buffers
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            st0.tokens.copy_(tok_h, non_blocking=True)
-            last.targets.copy_(tgt_h, non_blocking=True)
+            if first is not None:
+                first.tokens.copy_(tok_h, non_blocking=True)
+            if last is not None:
+                last.targets.copy_(tgt_h, non_blocking=True)
             loss = pipe.step()
-            loss_h.copy_(loss.reshape(1), non_blocking=False)
-        torch.cuda.synchronize()
+            if loss is not None:
+                loss_h.copy_(loss.reshape(1), non_blocking=False)
+        barrier()
         e2e_s = (time.perf_counter() - t0) / args.steps
-    tr, met = pipe.trace()
+    if dist:
+        t = torch.tensor([ms, e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = t[0].item(), t[1].item()
+    from paper_2605_18750_b200.runtime import wall_trace
+    ev, t0n = pipe.last_events
+    if dist:
+        allev = [None] * world
+        dist.all_gather_object(allev, ([(e.t0, e.t1, e.kind, e.stage, e.rank, e.task) for e in ev], t0n))
+        from paper_2605_18750_b200 import _lib
+        ev = []
+        for lst, _ in allev:
+            for t in lst:
+                x = _lib.Event()
+                x.t0, x.t1, x.kind, x.stage, x.rank, x.task = t
+                ev.append(x)
+        t0n = min(t for _, t in allev)
+    tr, met = wall_trace(pipe.workload, ev, t0n)
     bubble = met.bubble_fraction()
     it_s = 1000.0 / ms
     tok = args.mb * cfg.seq
-    # per-task times for the reference arm / replay tables
     execs = tr.execs()
-    f_us = sum(e.t_end - e.t_start for e in execs if e.direction == "F") / max(1, sum(e.direction == "F" for e in execs))
-    b_us = sum(e.t_end - e.t_start for e in execs if e.direction == "B") / max(1, sum(e.direction == "B" for e in execs))
+    task_us = {}
+    for d in ("F", "B", "W"):
+        per = []
+        for s_ in range(n):
+            xs = [e.t_end - e.t_start for e in execs if e.direction == d and e.stage == s_]
+            per.append(round(sum(xs) / len(xs), 1) if xs else 0.0)
+        task_us[d] = per
     roof = gemm_roofline(cfg, peak_sus)
     roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
-    # iteration roofline: sum of stage FLOPs / (N * peak)
     fF, fB, fW = cfg.flops_per_layer()
     it_flops = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
-    t_roof = it_flops / (n * peak_sus * 1e12)
-    launches_per_task = sum(pipe.stages[0].kernel_counts.values()) / max(1, len(pipe.stages[0].kernel_counts))
+    p2p = 2 * args.mb * cfg.seq * cfg.d_model * 2 if n > 1 else 0
+    t_roof = it_flops / (n * peak_sus * 1e12) + p2p / 770e9
+    launches = pipe.kernel_launches_per_step() if hasattr(pipe, "kernel_launches_per_step") else 0
+    if dist:
+        lt = torch.tensor([launches], device="cuda")
+        dist.all_reduce(lt)
+        launches = int(lt.item())
     line = {"metric": METRIC, "value": round(it_s, 4), "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, uniform tokens)",
             "config": workload_config(args, n),
             "tokens_per_s": round(it_s * tok, 1), "bubble_fraction": round(bubble, 4),
-            "iteration_roofline": {"t_roof_ms": round(t_roof * 1e3, 2), "frac": round(t_roof * 1e3 / ms, 3),
-                                   "definition": "sum stage FLOPs / (N * sustained bf16 peak) + P2P/NVLink"},
+            "iteration_roofline": {"t_roof_ms": round(t_roof * 1e3, 2),
+                                   "frac": round(t_roof * 1e3 / ms, 3),
+                                   "definition": "sum stage FLOPs / (N * sustained bf16 peak) "
+                                                 "+ per-GPU P2P bytes / 770 GB/s"},
             "roofline": roof,
-            "task_us": {"F": round(f_us, 1), "B": round(b_us, 1)},
+            "task_us": task_us,
             "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
-                    "h2d_bytes_per_step": int(tok_h.numel() * 4 + tgt_h.numel() * 4),
-                    "d2h_bytes_per_step": 4},
-            "gpu_launches": int(pipe.kernel_launches_per_step()),
+                    "h2d_bytes_per_step": int(2 * args.mb * cfg.seq * 4), "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches),
             "build_s": round(t_build, 1),
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, f_us, b_us)
-    print(json.dumps(line), flush=True)
+        line["cpu_baseline"] = cpu_baseline(args, n, task_us)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     pipe.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
-def cpu_baseline(args, f_us, b_us):
+def cpu_baseline(args, n, task_us):
+    """oracle.run_live (the reference's threaded CPU runtime, restated) driving the
+    same task graph with this run's measured per-task times; ~10 s sample."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import rrfp_oracle as O
+    dec = args.hint == "bfw"
     lat = {}
-    for mb in range(args.mb):
-        lat[("F", 0, mb, 0)] = int(f_us)
-        lat[("B", 0, mb, 0)] = int(b_us)
-    w = {"N": 1, "M": args.mb, "C": 1, "R": 1, "lat": lat, "comm": {"kind": "constant", "value": 0},
-         "dec": False, "beta": 0.5}
+    for s_ in range(n):
+        for mb in range(args.mb):
+            lat[("F", s_, mb, 0)] = max(1, int(task_us["F"][s_]))
+            lat[("B", s_, mb, 0)] = max(1, int(task_us["B"][s_]))
+            if dec:
+                lat[("W", s_, mb, 0)] = max(1, int(task_us["W"][s_]))
+    w = {"N": n, "M": args.mb, "C": 1, "R": 1, "lat": lat, "comm": {"kind": "constant", "value": 0},
+         "dec": dec, "beta": 0.5}
+    hint = "bf" if args.hint == "1f1b" else args.hint
     t0 = time.perf_counter()
     k = 0
     while time.perf_counter() - t0 < 10.0 or k < 1:
-        O.run_live(w, "bf", 32, 1.0, seed=0)
+        O.run_live(w, hint, 32, 1.0, seed=0)
         k += 1
     dt = (time.perf_counter() - t0) / k
-    return {"value": round(1.0 / dt, 4), "unit": "iter/s", "cores": 3, "kind": "port",
-            "sample": f"{k} iterations of oracle.run_live (3 threads) with this run's measured "
-                      f"F={f_us:.0f}us / B={b_us:.0f}us task times, M={args.mb}"}
+    return {"value": round(1.0 / dt, 4), "unit": "iter/s", "cores": 3 * n, "kind": "port",
+            "sample": f"{k} iterations of oracle.run_live ({3 * n} threads, GIL-bound) on this run's "
+                      f"measured per-task times, PP={n}, M={args.mb}"}
 
 
 def main():

@@ -184,6 +184,10 @@ int rrfp_runtime_inbox(rrfp_runtime* rt, void** dev_ptr, size_t* bytes);
 int rrfp_runtime_inbox_ipc(rrfp_runtime* rt, void* handle64);
 /* Open a peer's IPC handle; returns a device pointer usable in this process. */
 int rrfp_ipc_open(const void* handle64, void** dev_ptr);
+/* cudaMalloc'd (IPC-exportable) buffer for mailbox slots; handle of such a buffer. */
+int rrfp_ipc_alloc(size_t bytes, void** dev_ptr);
+int rrfp_ipc_handle(void* dev_ptr, void* handle64);
+void rrfp_ipc_free(void* dev_ptr);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */
@@ -200,6 +204,9 @@ int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int6
  * cudaGraphSetConditional.  Must be called before the first launch. */
 int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* const* graphs, int32_t n);
 int rrfp_runtime_task_ptr(rrfp_runtime* rt, void** dev_ptr);
+/* Build, instantiate and upload the lane graph (call for every lane of the job
+ * before the first launch of any lane). */
+int rrfp_runtime_prepare(rrfp_runtime* rt, void* stream);
 /* Build (first call) and launch one iteration's executor graph on the lane's
  * stream; epoch must increase by one per iteration. Asynchronous. */
 int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream);

@@ -79,8 +79,8 @@ EXPORTS = [
     "rrfp_arbitrate", "rrfp_update_backpressure", "rrfp_replay_workspace_bytes",
     "rrfp_replay_event_capacity", "rrfp_replay_host", "rrfp_replay_device",
     "rrfp_runtime_create", "rrfp_runtime_destroy", "rrfp_runtime_inbox", "rrfp_runtime_inbox_ipc",
-    "rrfp_ipc_open", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
-    "rrfp_runtime_task_ptr", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status",
+    "rrfp_ipc_open", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
+    "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status",
     "rrfp_spin", "rrfp_last_error", "rrfp_abi_version",
 ]
 
@@ -103,8 +103,8 @@ def lib():
         L.rrfp_last_error.restype = C.c_char_p
         L.rrfp_replay_workspace_bytes.restype = C.c_size_t
         L.rrfp_replay_event_capacity.restype = C.c_int32
-        if hasattr(L, 'rrfp_runtime_destroy'):
-            L.rrfp_runtime_destroy.restype = None
+        L.rrfp_runtime_destroy.restype = None
+        L.rrfp_ipc_free.restype = None
         _lib = L
     return _lib
 

@@ -71,6 +71,7 @@ struct lane_state {
   rrfp_event* ring;
   int32_t ring_n, ring_cap;
   volatile int32_t* abort_flag;             // host-mapped
+  volatile int32_t* mon;                    // host-mapped monitor: [0] where, [1] task, [2] remaining, [3] epoch
   cudaGraphConditionalHandle h_while, h_switch;
   uint32_t doneF[RRFP_MAX_WORDS], doneB[RRFP_MAX_WORDS], wpend[RRFP_MAX_WORDS];
   uint32_t fdisp[RRFP_MAX_WORDS], bdisp[RRFP_MAX_WORDS];
@@ -141,6 +142,7 @@ __global__ void lane_init_kernel(lane_state* L) {
     L->fixed_head = 0; L->status = 0; L->cur_kind = LANE_NONE;
     L->ring_n = 0;
     L->t_iter0 = gtimer();
+    L->mon[0] = 1; L->mon[2] = L->remaining; L->mon[3] = (int32_t)L->epoch;
   }
   for (int i = lane; i < RRFP_MAX_WORDS; i += 32) {
     L->doneF[i] = L->doneB[i] = L->wpend[i] = 0;
@@ -151,6 +153,7 @@ __global__ void lane_init_kernel(lane_state* L) {
 
 __global__ void lane_final_kernel(lane_state* L) {
   if (threadIdx.x == 0) {
+    L->mon[0] = 4;
     L->t_iter1 = gtimer();
     __threadfence_system();
     st_release_sys(&L->inbox->done_epoch, L->epoch);
@@ -336,6 +339,8 @@ __global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
         if (s_kind == RRFP_WAIT) s_kind = -1;
       }
       if (s_kind >= 0 && s_kind != RRFP_WAIT) {
+        L->mon[0] = 2;
+        L->mon[1] = (int32_t)L->cur_task;
         L->t_start = gtimer();
         unsigned branch = (unsigned)s_kind;
         if (d.compute_kind == 1) branch = (unsigned)(s_kind * d.M + rrfp_task_mb(L->cur_task));
@@ -431,6 +436,8 @@ __global__ void lane_complete_kernel(lane_state* L) {
   unsigned long long end = gtimer();
   ring_emit(L, 0, L->t_start, end, d.R > 1 ? d.rank : -1, t);
   L->remaining -= 1;
+  L->mon[0] = 3;
+  L->mon[2] = L->remaining;
   if (kind == RRFP_DIR_F) {
     bit_set(L->doneF, k);
     L->n_f += 1;
@@ -457,6 +464,8 @@ struct rrfp_runtime {
   rrfp_event* ring;         // device
   int32_t* abort_host;      // mapped host memory
   int32_t* abort_dev;
+  int32_t* mon_host;        // mapped monitor block (readable while the GPU is busy)
+  int32_t* mon_dev;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
   std::vector<cudaGraph_t> bodies;   // [3 * M] per-(kind, mb) compute graphs
@@ -503,6 +512,9 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   RRFP_CUDA_TRY(cudaHostAlloc(&rt->abort_host, sizeof(int32_t), cudaHostAllocMapped));
   *rt->abort_host = 0;
   RRFP_CUDA_TRY(cudaHostGetDevicePointer(&rt->abort_dev, rt->abort_host, 0));
+  RRFP_CUDA_TRY(cudaHostAlloc(&rt->mon_host, 16 * sizeof(int32_t), cudaHostAllocMapped));
+  memset(rt->mon_host, 0, 16 * sizeof(int32_t));
+  RRFP_CUDA_TRY(cudaHostGetDevicePointer(&rt->mon_dev, rt->mon_host, 0));
   RRFP_CUDA_TRY(cudaEventCreateWithFlags(&rt->done_ev, cudaEventDisableTiming));
   // host image of the lane state
   lane_state h;
@@ -519,6 +531,7 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   h.ring = rt->ring;
   h.ring_cap = desc->trace_cap;
   h.abort_flag = rt->abort_dev;
+  h.mon = rt->mon_dev;
   h.n_lanes = 1;
   h.all[0] = rt->inbox;
   for (int r = 0; r < RRFP_MAX_RANKS; ++r) h.fwd_dst[r] = h.bwd_dst[r] = h.tp_peer[r] = rt->inbox;
@@ -534,7 +547,8 @@ extern "C" void rrfp_runtime_destroy(rrfp_runtime* rt) {
   if (rt->graph) cudaGraphDestroy(rt->graph);
   for (void* p : rt->opened) cudaIpcCloseMemHandle(p);
   cudaFree(rt->L); cudaFree(rt->inbox); cudaFree(rt->tables); cudaFree(rt->fixed);
-  cudaFree(rt->ring); cudaFreeHost(rt->abort_host); cudaEventDestroy(rt->done_ev);
+  cudaFree(rt->ring); cudaFreeHost(rt->abort_host); cudaFreeHost(rt->mon_host);
+  cudaEventDestroy(rt->done_ev);
   delete rt;
 }
 
@@ -560,6 +574,25 @@ extern "C" int rrfp_ipc_open(const void* handle64, void** dev_ptr) {
   memcpy(&h, handle64, sizeof(h));
   RRFP_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
   return RRFP_OK;
+}
+
+extern "C" int rrfp_ipc_alloc(size_t bytes, void** dev_ptr) {
+  if (!dev_ptr || !bytes) return rrfp_fail(RRFP_E_INVALID, "bad ipc alloc");
+  RRFP_CUDA_TRY(cudaMalloc(dev_ptr, bytes));
+  RRFP_CUDA_TRY(cudaMemset(*dev_ptr, 0, bytes));
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_ipc_handle(void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  RRFP_CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle64, &h, sizeof(h));
+  return RRFP_OK;
+}
+
+extern "C" void rrfp_ipc_free(void* dev_ptr) {
+  if (dev_ptr) cudaFree(dev_ptr);
 }
 
 // all_lanes: N*R inbox pointers (lane index = stage*R + rank), used for the
@@ -682,6 +715,21 @@ static int build_graph(rrfp_runtime* rt) {
   return RRFP_OK;
 }
 
+// Build + instantiate + upload the lane graph while the device is idle (every
+// lane of a job must be prepared before any lane is launched: a running lane
+// spins on its peers, and graph instantiation/upload must not queue behind it).
+extern "C" int rrfp_runtime_prepare(rrfp_runtime* rt, void* stream) {
+  if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  if (!rt->built) {
+    int rc = build_graph(rt);
+    if (rc) return rc;
+  }
+  RRFP_CUDA_TRY(cudaGraphUpload(rt->exec, (cudaStream_t)stream));
+  RRFP_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return RRFP_OK;
+}
+
 extern "C" int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream) {
   if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
   RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
@@ -713,6 +761,16 @@ extern "C" int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_ev
       *(volatile int32_t*)rt->abort_host = 1;  // dispatcher exits its loop
       fired = true;
     }
+    if (fired && el > watchdog_secs + 10.0) {
+      volatile int32_t* m = rt->mon_host;
+      const char* where[] = {"?", "dispatch", "body", "complete", "final"};
+      int w = m[0] >= 0 && m[0] <= 4 ? m[0] : 0;
+      rrfp_task_t t = (rrfp_task_t)m[1];
+      return rrfp_fail(RRFP_E_WATCHDOG,
+                       "lane stage %d rank %d stuck in %s (task %c mb %d chunk %d), remaining %d, epoch %d",
+                       rt->d.stage, rt->d.rank, where[w], "BFW?"[rrfp_task_dir(t)], rrfp_task_mb(t),
+                       rrfp_task_chunk(t), m[2], m[3]);
+    }
     struct timespec ts = {0, 20000};
     nanosleep(&ts, nullptr);
   }
@@ -731,17 +789,17 @@ extern "C" int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_ev
   return RRFP_OK;
 }
 
+// Reads only the host-mapped monitor block: safe while the GPU is busy or hung.
 extern "C" int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap) {
   if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
-  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
-  lane_state h;
-  RRFP_CUDA_TRY(cudaMemcpy(&h, rt->L, sizeof(h), cudaMemcpyDeviceToHost));
+  volatile int32_t* m = rt->mon_host;
+  const char* where[] = {"idle", "dispatch", "body", "complete", "final"};
+  int w = m[0] >= 0 && m[0] <= 4 ? m[0] : 0;
+  rrfp_task_t t = (rrfp_task_t)m[1];
   if (dump && cap)
-    snprintf(dump, cap,
-             "stage %d rank %d: epoch=%u remaining=%d mode=%d D=%d n_w=%d next_adm=%d "
-             "fixed_head=%d status=%d tp_round=%llu",
-             rt->d.stage, rt->d.rank, h.epoch, h.remaining, h.mode, h.n_f - h.n_b, h.n_w,
-             h.next_adm, h.fixed_head, h.status, (unsigned long long)h.tp_round);
+    snprintf(dump, cap, "stage %d rank %d: epoch=%d where=%s last_task=%c%d.%d remaining=%d",
+             rt->d.stage, rt->d.rank, m[3], where[w], "BFW?"[rrfp_task_dir(t)], rrfp_task_mb(t),
+             rrfp_task_chunk(t), m[2]);
   return RRFP_OK;
 }
 

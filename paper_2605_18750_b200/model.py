@@ -156,7 +156,8 @@ class RawBuffer:
 
 class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
-                 decompose: bool = False, seed: int = 1234, data_seed: int = 0):
+                 decompose: bool = False, seed: int = 1234, data_seed: int = 0,
+                 fwd_in=None, bwd_in=None):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
         self.first, self.last = stage == 0, stage == n_stages - 1
@@ -176,8 +177,12 @@ class StageCompute:
         self.tokens = toks if self.first else None
         self.targets = tgts if self.last else None
         # mailboxes written by neighbours: F input (stage > 0), B input (stage < N-1)
-        self.fwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf) if not self.first else None
-        self.bwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf) if not self.last else None
+        # (the caller may pass IPC-exportable buffers, distributed.py)
+        if fwd_in is None and not self.first:
+            fwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf)
+        if bwd_in is None and not self.last:
+            bwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf)
+        self.fwd_in, self.bwd_in = fwd_in, bwd_in
         self.fwd_out = None   # per-mb destination buffers (set by connect_outputs)
         self.bwd_out = None
         # activation slots, one per microbatch (static addresses for graph capture)
@@ -369,7 +374,7 @@ class StageCompute:
         o4, lse, cq, ck, mq, mk, ps, po = self.attn_aux[mb][li]
         go = d_o.view(S, H, Dh).transpose(0, 1).unsqueeze(0)
         dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
-            go, q, k, v, o4, lse, ps, po, torch.empty(0, device=self.device), cq, ck, mq, mk, 0.0,
+            go, q, k, v, o4, lse, ps, po, None, cq, ck, mq, mk, 0.0,
             True, scale=1.0 / math.sqrt(Dh))
         d_qkv[:, :D].view(S, H, Dh).copy_(dq[0].transpose(0, 1))
         d_qkv[:, D:2 * D].view(S, H, Dh).copy_(dk[0].transpose(0, 1))
@@ -423,7 +428,9 @@ class StageCompute:
     def capture_bodies(self, stream=None):
         """One CUDA graph per (kind, mb); returns 3*M raw cudaGraph_t handles
         indexed kind*M + mb with kind B=0, F=1, W=2 (None where no work)."""
-        kinds = ["B", "F", "W"] if self.decompose else ["B", "F"]
+        # F is captured before B/W: the B graph must bind the attention outputs
+        # (o, lse) that the CAPTURED F graph writes, not the warm-up's.
+        kinds = ["F", "B", "W"] if self.decompose else ["F", "B"]
         stream = stream or torch.cuda.Stream(self.device)
         # warm-up: run every body once eagerly (cuDNN plan selection, module loads)
         with torch.cuda.stream(stream):
@@ -436,7 +443,7 @@ class StageCompute:
         for kind in kinds:
             ki = {"B": 0, "F": 1, "W": 2}[kind]
             for mb in range(self.M):
-                g = torch.cuda.CUDAGraph()
+                g = torch.cuda.CUDAGraph(keep_graph=True)
                 before = K.LAUNCHES[0]
                 with torch.cuda.graph(g, stream=stream):
                     self.run_task(kind, mb)

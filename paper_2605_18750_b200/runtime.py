@@ -65,7 +65,7 @@ class LaneGroup:
                  time_scale: float = 1.0, *, seed: int = 0, jitter: JitterConfig | None = None,
                  tp: TpGroup | None = None, mode: str = "free", schedule: FixedSchedule | None = None,
                  placement=None, local=None, bodies=None, compute_kind: int = 0,
-                 trace_cap: int | None = None, pad_table_us=None):
+                 trace_cap: int | None = None, pad_table_us=None, defer_bodies: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("run_gpu needs a CUDA device (B200)")
@@ -148,8 +148,13 @@ class LaneGroup:
                 _lib.check(self.L.rrfp_runtime_set_bodies(h, carr, len(arr)))
         self.cap = cap
         self.epoch = 0
-        if len(self.local) == n * r:
+        if len(self.local) == n * r and not defer_bodies:
             self.connect_local()
+
+    def set_bodies(self, bodies: dict):
+        for lane, arr in bodies.items():
+            carr = (C.c_void_p * len(arr))(*[C.c_void_p(x or 0) for x in arr])
+            _lib.check(self.L.rrfp_runtime_set_bodies(self.lanes[lane], carr, len(arr)))
 
     def inbox(self, lane):
         p = C.c_void_p()
@@ -197,8 +202,16 @@ class LaneGroup:
                 inboxes[lane] = p.value
         self.connect(inboxes)
 
+    def prepare(self):
+        """Instantiate + upload every local lane graph while nothing runs."""
+        for lane, h in self.lanes.items():
+            _lib.check(self.L.rrfp_runtime_prepare(h, C.c_void_p(self.streams[lane].cuda_stream)))
+        self.prepared = True
+
     def launch(self):
         import torch
+        if not getattr(self, "prepared", False):
+            self.prepare()
         self.epoch += 1
         for lane, h in self.lanes.items():
             st = self.streams[lane]

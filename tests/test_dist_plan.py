@@ -1,0 +1,71 @@
+"""Multi-process host logic (one stage per process) on CPU with gloo, world_size 2:
+topology plan, handle exchange and identical replay schedules on every rank."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2605_18750_b200 as P
+    from paper_2605_18750_b200.distributed import plan_peers
+    from paper_2605_18750_b200 import tables
+    peers = plan_peers(rank, world)
+    fake = {"stage": rank, "fwd": bytes([rank + 1]) * 64 if rank > 0 else None,
+            "bwd": bytes([rank + 11]) * 64 if rank < world - 1 else None}
+    allh = [None] * world
+    dist.all_gather_object(allh, fake)
+    opened = {}
+    if peers["writes_fwd_mailbox"]:
+        opened["fwd"] = allh[rank + 1]["fwd"]
+    if peers["writes_bwd_mailbox"]:
+        opened["bwd"] = allh[rank - 1]["bwd"]
+    # every rank lowers the same workload independently -> identical tables / schedules
+    spec = P.GeneratorSpec(num_stages=world, num_microbatches=8, forward=P.uniform(50, 150),
+                           backward=P.uniform(80, 200))
+    w = P.generate_workload(spec, 5)
+    tr, m = P.run_rrfp(w, "bf", 32, 5, jitter=P.JITTER_PRESETS["J2"], device="cpu")
+    order = [(e.stage, e.direction, e.microbatch, e.t_start) for e in tr.execs()]
+    tb = tables.lower(w, P.HintOrder("bf"), 32, 5, P.JITTER_PRESETS["J2"])
+    allo = [None] * world
+    dist.all_gather_object(allo, (order, int(tb.dur.sum()), int(tb.comm.sum())))
+    q.put((rank, peers, opened, allo[0] == allo[-1]))
+    dist.destroy_process_group()
+
+
+def test_two_process_plan_and_exchange():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    r0, r1 = res
+    assert r0[1]["fwd"] == [(1, 0)] and r0[1]["writes_fwd_mailbox"] and not r0[1]["writes_bwd_mailbox"]
+    assert r1[1]["bwd"] == [(0, 0)] and r1[1]["writes_bwd_mailbox"] and not r1[1]["writes_fwd_mailbox"]
+    assert r0[2]["fwd"] == bytes([2]) * 64      # rank 0 writes into rank 1's F mailbox
+    assert r1[2]["bwd"] == bytes([11]) * 64     # rank 1 writes into rank 0's B mailbox
+    assert r0[3] and r1[3]                      # identical schedules/tables on both ranks
+
+
+def test_plan_wraps_for_interleaved_chunks():
+    from paper_2605_18750_b200.distributed import plan_peers
+    p = plan_peers(3, 4, 2)
+    assert p["fwd"] == [(0, 0), (0, 1)] and p["bwd"] == [(2, 0), (2, 1)]
+    assert not p["writes_fwd_mailbox"] and p["writes_bwd_mailbox"]
