@@ -217,6 +217,31 @@ int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap);
 
 /* ---- stage-compute kernel entry points (unit-test surface) ------------- */
 
+/* Stage GEMM (tcgen05/TMA, csrc/gemm_sm100.cu): C[M,N] = sum_k A(m,k) B(n,k),
+ * A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k], B(n,k) = b_mn ? B[k*ldb+n] : B[n*ldb+k];
+ * epi: 0 bf16 (+bias), 1 bias+GELU (C=pre, C2=gelu), 2 +bias+R, 3 f32 (+)=,
+ * 4 *gelu'(R), 5 f32.  Replaces the timed no-op compute (engine.py:272-273). */
+int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda,
+                   const void* B, long long ldb, void* C, long long ldc, void* C2, long long ldc2,
+                   const void* bias, const void* R, long long ldr, int accumulate, void* stream);
+int rrfp_gemm_set_variant(int pair);
+int rrfp_gemm_reserve_sms(int n);
+/* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
+int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
+                       int rows, int D, float eps, void* stream);
+int rrfp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                       const void* g, const void* dres, void* dx, float* dg, float* db, int rows,
+                       int D, void* stream);
+int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x, int rows, int D,
+                       void* stream);
+int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP, int rows, int D,
+                       void* stream);
+int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows, int cols, void* stream);
+int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* target, int rows, int V,
+                  float* loss, float* lse, void* stream);
+int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, int V,
+                  const float* lse, float scale, void* stream);
+
 /* Synthetic spin task: busy-wait `ns` on the device (%globaltimer). */
 int rrfp_spin(int64_t ns, void* stream);
 

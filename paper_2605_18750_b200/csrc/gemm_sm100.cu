@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/rrfp_b200.h"
@@ -55,6 +56,7 @@ struct GemmArgs {
   long long ldr;
   int accumulate;
   int vec;   // 1 when C/C2/R rows are 16-byte aligned (vector epilogue path allowed)
+  int vec_bias;
 };
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -75,6 +77,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Pull this thread's residual / pre-activation row segment of the next tile
+// into L2 before the accumulator is ready (hides the epilogue's load latency).
+template <int EPI>
+__device__ __forceinline__ void epilogue_prefetch(const GemmArgs& g, int row, int col0, int ncols) {
+  if (EPI != EPI_RESID && EPI != EPI_GELU_BWD) return;
+  if (row >= g.M) return;
+  const char* p = reinterpret_cast<const char*>(g.R + (size_t)row * g.ldr + col0);
+  const int bytes = min(ncols, g.N - col0) * 2;
+  for (int b = 0; b < bytes; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0,
                                                uint32_t (&r)[32]) {
@@ -88,12 +101,14 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
     if (full) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
-        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         if (EPI == EPI_ACC_F32 && g.accumulate) {
-          float4 p = *reinterpret_cast<const float4*>(c + j);
-          o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+          // fire-and-forget vector reduction in L2: no load latency in the epilogue
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(c + j), "f"(v[j]),
+                       "f"(v[j + 1]), "f"(v[j + 2]), "f"(v[j + 3])
+                       : "memory");
+        } else {
+          *reinterpret_cast<float4*>(c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
-        *reinterpret_cast<float4*>(c + j) = o;
       }
     } else {
       for (int j = 0; j < 32 && col0 + j < g.N; ++j)
@@ -102,9 +117,23 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
     return;
   }
   if (g.bias && EPI != EPI_GELU_BWD) {
+    if (full && g.vec_bias) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (col0 + j < g.N) v[j] += __bfloat162float(g.bias[col0 + j]);
+      for (int j = 0; j < 32; j += 8) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(g.bias + col0 + j));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float2 f = __bfloat1622float2(h[t]);
+          v[j + 2 * t] += f.x;
+          v[j + 2 * t + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < g.N) v[j] += __bfloat162float(g.bias[col0 + j]);
+    }
   }
   if (EPI == EPI_RESID || EPI == EPI_GELU_BWD) {
     const __nv_bfloat16* rp = g.R + (size_t)row * g.ldr + col0;
@@ -254,9 +283,10 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+      const int row = mb * BM + ew * 32 + lane;
+      epilogue_prefetch<EPI>(g, row, nb * BN, BN);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
-      const int row = mb * BM + ew * 32 + lane;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -275,6 +305,151 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x 256
+// tile with tcgen05.mma.cta_group::2 (UMMA M = 256).  Each CTA loads its own
+// 128 rows of A and 128 rows (half of N) of B, so a CTA moves 32 KB per
+// 64-deep k-block instead of 48 KB: 1.5x the arithmetic intensity of the
+// 1-CTA 128x256 tile against the L2 (the 1-CTA kernel is L2-bandwidth bound).
+// The leader CTA issues the MMAs; TMA completions of both CTAs land on the
+// leader's full barrier; MMA commits multicast to both CTAs' empty / tmem-full
+// barriers; both epilogues release the leader's tmem-empty barrier.
+constexpr int P_BM = 256, P_BN = 256, P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2;      // this CTA's 128 rows of A
+constexpr int P_B_BYTES = 128 * BK * 2;      // this CTA's 128 rows (N/2) of B
+constexpr int P_SMEM_BYTES = P_STAGES * (P_A_BYTES + P_B_BYTES) + 1024 + 256;
+constexpr int P_TMEM_COLS = 2 * P_BN;
+
+template <int EPI, int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_bf16_sm100_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P_STAGES * P_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_B_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + P_STAGES;
+  uint64_t* tfull = bars + 2 * P_STAGES;
+  uint64_t* tempty = bars + 2 * P_STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P_STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+    for (int s = 0; s < P_STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc_pair<P_TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = g.tiles_m * g.tiles_n;
+  const int kblocks = (g.K + BK - 1) / BK;
+  const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t lead_full0 = sm100::mapa_shared(sm100::smem_u32(&full[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+        const int m0 = mb * P_BM + rank * 128, n0 = nb * P_BN + rank * 128;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2 * (P_A_BYTES + P_B_BYTES));
+          const uint32_t bar = lead_full0 + stage * 8;
+          uint8_t* a_dst = sA + stage * P_A_BYTES;
+          uint8_t* b_dst = sB + stage * P_B_BYTES;
+          if (!A_MN) {
+            sm100::tma_load_2d_pair(a_dst, &tmA, bar, kb * BK, m0);
+          } else {
+            sm100::tma_load_2d_pair(a_dst, &tmA, bar, m0, kb * BK);
+            sm100::tma_load_2d_pair(a_dst + 64 * BK * 2, &tmA, bar, m0 + 64, kb * BK);
+          }
+          if (!B_MN) {
+            sm100::tma_load_2d_pair(b_dst, &tmB, bar, kb * BK, n0);
+          } else {
+            sm100::tma_load_2d_pair(b_dst, &tmB, bar, n0, kb * BK);
+            sm100::tma_load_2d_pair(b_dst + 64 * BK * 2, &tmB, bar, n0 + 64, kb * BK);
+          }
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(P_BM, P_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * P_BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a_base = sm100::smem_u32(sA + stage * P_A_BYTES);
+          const uint32_t b_base = sm100::smem_u32(sB + stage * P_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = A_MN ? sm100::umma_desc_sw128(a_base + k * 16 * 128, 64 * BK * 2, 1024)
+                               : sm100::umma_desc_sw128(a_base + k * 32, 16, 1024);
+            uint64_t bd = B_MN ? sm100::umma_desc_sw128(b_base + k * 16 * 128, 64 * BK * 2, 1024)
+                               : sm100::umma_desc_sw128(b_base + k * 32, 16, 1024);
+            sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          sm100::mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+        sm100::mma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const uint32_t lead_tempty0 = sm100::mapa_shared(sm100::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+      const int row = mb * P_BM + rank * 128 + ew * 32 + lane;
+      epilogue_prefetch<EPI>(g, row, nb * P_BN, P_BN);
+      sm100::mbar_wait(&tfull[acc], acc_phase);
+      sm100::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * P_BN;
+#pragma unroll 1
+      for (int c = 0; c < P_BN; c += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld32(t_row + c, r);
+        sm100::tmem_ld_wait();
+        if (nb * P_BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * P_BN + c, r);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_cluster(lead_tempty0 + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair<P_TMEM_COLS>(tmem_base);
   }
 }
 
@@ -317,6 +492,34 @@ int make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, lo
 
 int g_num_sms = 0;
 int g_reserve_sms = 0;
+int g_pair = -1;   // 1: use the CTA-pair kernel (env RRFP_GEMM_PAIR, default on)
+
+bool use_pair() {
+  if (g_pair < 0) {
+    const char* e = getenv("RRFP_GEMM_PAIR");
+    g_pair = e ? atoi(e) : 1;
+  }
+  return g_pair != 0;
+}
+
+template <int EPI, int A_MN, int B_MN>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs g, cudaStream_t st) {
+  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES));
+    attr = true;
+  }
+  g.tiles_m = (g.M + P_BM - 1) / P_BM;
+  g.tiles_n = (g.N + P_BN - 1) / P_BN;
+  int tiles = g.tiles_m * g.tiles_n;
+  int pairs = (g_num_sms - g_reserve_sms) / 2;
+  if (pairs < 1) pairs = 1;
+  int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, 256, P_SMEM_BYTES, st>>>(ta, tb, g);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
 
 template <int EPI, int A_MN, int B_MN>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st) {
@@ -325,11 +528,6 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
   if (!attr) {
     RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
-  }
-  if (!g_num_sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int tiles = g.tiles_m * g.tiles_n;
   int sms = g_num_sms - g_reserve_sms;
@@ -343,6 +541,17 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
 template <int EPI>
 int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
                     const GemmArgs& g, cudaStream_t st) {
+  if (!g_num_sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (use_pair()) {
+    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0>(ta, tb, g, st);
+    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1>(ta, tb, g, st);
+    if (a_mn && b_mn) return launch_pair<EPI, 1, 1>(ta, tb, g, st);
+    return launch_pair<EPI, 1, 0>(ta, tb, g, st);
+  }
   if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
   if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
   if (a_mn && b_mn) return launch<EPI, 1, 1>(ta, tb, g, st);
@@ -363,9 +572,10 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   if (epi == EPI_BIAS_GELU && !C2) return rrfp_fail(RRFP_E_INVALID, "gelu epilogue needs C2");
   if ((epi == EPI_RESID || epi == EPI_GELU_BWD) && !R) return rrfp_fail(RRFP_E_INVALID, "epilogue needs R");
   CUtensorMap ta, tb;
+  const int brows = use_pair() ? 128 : BN;   // rows of B per CTA (the pair splits N)
   int rc = a_mn ? make_map(&ta, A, K, M, lda, 64, BK) : make_map(&ta, A, M, K, lda, BK, BM);
   if (rc) return rc;
-  rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, BK) : make_map(&tb, B, N, K, ldb, BK, BN);
+  rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, BK) : make_map(&tb, B, N, K, ldb, BK, brows);
   if (rc) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
@@ -379,6 +589,7 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   g.vec = ((uintptr_t)C % 16 == 0) && ((ldc * esz) % 16 == 0) &&
           (!C2 || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
           (!R || (((uintptr_t)R % 16 == 0) && (ldr * 2) % 16 == 0));
+  g.vec_bias = ((uintptr_t)bias % 16) == 0;
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, g, st);
@@ -389,6 +600,12 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
     case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, g, st);
   }
   return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
+}
+
+// 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel
+extern "C" int rrfp_gemm_set_variant(int pair) {
+  g_pair = pair ? 1 : 0;
+  return RRFP_OK;
 }
 
 extern "C" int rrfp_gemm_reserve_sms(int n) {

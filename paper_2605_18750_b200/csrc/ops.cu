@@ -85,64 +85,89 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 }
 
 // dx = rstd * (dxh - xhat * mean(dxh * xhat) - mean(dxh)) + dres, dxh = dy * g
-// dg += sum_rows dy * xhat, db += sum_rows dy.  Two passes over a row (the
-// second hits L1/L2) keep registers low; parameter-gradient partials go to
-// shared memory, then one global atomicAdd per column per block.
+// One warp per row, the row held in registers (single pass over x, dy).
 template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
     const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
-    __nv_bfloat16* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db, int rows) {
+    __nv_bfloat16* __restrict__ dx, int rows) {
   constexpr int D = 256 * NV;
-  __shared__ float s_dg[D], s_db[D];
-  for (int i = threadIdx.x; i < D; i += blockDim.x) { s_dg[i] = 0.f; s_db[i] = 0.f; }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warps_total = gridDim.x * (blockDim.x >> 5);
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps_total) {
-    const float mean = mean_in[row], rstd = rstd_in[row];
-    const __nv_bfloat16* xr = x + (size_t)row * D;
-    const __nv_bfloat16* dr = dy + (size_t)row * D;
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll 2
-    for (int i = 0; i < NV; ++i) {
-      const int c = (i * 32 + lane) * 8;
-      float xv[8], dv[8], gv[8];
-      load8(xr + c, xv);
-      load8(dr + c, dv);
-      load8(g + c, gv);
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float mean = mean_in[row], rstd = rstd_in[row];
+  const __nv_bfloat16* xr = x + (size_t)row * D;
+  const __nv_bfloat16* dr = dy + (size_t)row * D;
+  float xh[NV][8], dh[NV][8];
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xh = (xv[j] - mean) * rstd, dh = dv[j] * gv[j];
-        s1 += dh * xh;
-        s2 += dh;
-      }
-    }
-    s1 = warp_sum(s1) * (1.f / D);
-    s2 = warp_sum(s2) * (1.f / D);
-#pragma unroll 2
-    for (int i = 0; i < NV; ++i) {
-      const int c = (i * 32 + lane) * 8;
-      float xv[8], dv[8], gv[8], o[8], rv[8];
-      load8(xr + c, xv);
-      load8(dr + c, dv);
-      load8(g + c, gv);
-      if (dres) load8(dres + (size_t)row * D + c, rv);
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    float xv[8], dv[8], gv[8];
+    load8(xr + c, xv);
+    load8(dr + c, dv);
+    load8(g + c, gv);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float xh = (xv[j] - mean) * rstd, dh = dv[j] * gv[j];
-        o[j] = rstd * (dh - xh * s1 - s2) + (dres ? rv[j] : 0.f);
-        atomicAdd(&s_dg[c + j], dv[j] * xh);
-        atomicAdd(&s_db[c + j], dv[j]);
-      }
-      store8(dx + (size_t)row * D + c, o);
+    for (int j = 0; j < 8; ++j) {
+      xh[i][j] = (xv[j] - mean) * rstd;
+      dh[i][j] = dv[j] * gv[j];
+      s1 += dh[i][j] * xh[i][j];
+      s2 += dh[i][j];
     }
   }
+  s1 = warp_sum(s1) * (1.f / D);
+  s2 = warp_sum(s2) * (1.f / D);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    float o[8], rv[8];
+    if (dres) load8(dres + (size_t)row * D + c, rv);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = rstd * (dh[i][j] - xh[i][j] * s1 - s2) + (dres ? rv[j] : 0.f);
+    store8(dx + (size_t)row * D + c, o);
+  }
+}
+
+// dg[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r];  db[c] += sum_r dy[r,c]
+// Block = 8 warps over a slab of rows; each thread owns 8 consecutive columns
+// (16-byte loads, a warp covers 256 columns per row); warps reduce via smem,
+// then one atomicAdd per column per block.
+__global__ void __launch_bounds__(256) ln_param_grad_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dg,
+    float* __restrict__ db, int rows, int D, int rows_per_block) {
+  __shared__ float sg[8][256], sb[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 256 + lane * 8;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  float ag[8], ab[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { ag[j] = 0.f; ab[j] = 0.f; }
+  if (c0 < D) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      float xv[8], dv[8];
+      load8(x + (size_t)r * D + c0, xv);
+      load8(dy + (size_t)r * D + c0, dv);
+      const float m = mean_in[r], rs = rstd_in[r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ag[j] += dv[j] * (xv[j] - m) * rs;
+        ab[j] += dv[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { sg[warp][lane * 8 + j] = ag[j]; sb[warp][lane * 8 + j] = ab[j]; }
   __syncthreads();
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    if (dg) atomicAdd(&dg[i], s_dg[i]);
-    if (db) atomicAdd(&db[i], s_db[i]);
+  const int t = threadIdx.x;   // one column of this block's 256
+  float tg = 0.f, tb = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) { tg += sg[w][t]; tb += sb[w][t]; }
+  const int c = blockIdx.x * 256 + t;
+  if (c < D) {
+    if (dg) atomicAdd(&dg[c], tg);
+    if (db) atomicAdd(&db[c], tb);
   }
 }
 
@@ -182,16 +207,35 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 }
 
 // ------------------------------------------------------- bias gradients
-// db[n] += sum_r dy[r, n]; block = 256 columns x a slab of rows
-__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ld, float* __restrict__ db,
-                              int rows, int cols, int rows_per_block) {
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= cols) return;
+// db[n] += sum_r dy[r, n]; each thread owns 8 consecutive columns (16-byte
+// loads), 8 warps split a slab of rows, smem reduction, 1 atomic / column / block.
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ld,
+                                                     float* __restrict__ db, int rows, int cols,
+                                                     int rows_per_block) {
+  __shared__ float sb[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 256 + lane * 8;
   const int r0 = blockIdx.y * rows_per_block;
   const int r1 = min(rows, r0 + rows_per_block);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += __bfloat162float(dy[(size_t)r * ld + c]);
-  atomicAdd(&db[c], s);
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 0.f;
+  if (c0 < cols) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      float v[8];
+      load8(dy + (size_t)r * ld + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += v[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sb[warp][lane * 8 + j] = a[j];
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) t += sb[w][threadIdx.x];
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < cols) atomicAdd(&db[c], t);
 }
 
 // ------------------------------------------------------- cross entropy
@@ -281,13 +325,18 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
                                   const void* g, const void* dres, void* dx, float* dg, float* db,
                                   int rows, int D, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  int blocks = (rows + 63) / 64;   // 8 warps x 8 rows per block
-  if (blocks > 148) blocks = 148;
-  dim3 grid(blocks);
+  dim3 grid((rows + 7) / 8);
   if (D > 4096) return rrfp_fail(RRFP_E_INVALID, "LayerNorm bwd width %d too large", D);
-  LAUNCH_NV(ln_bwd_kernel, D, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd,
-            (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, dg, db, rows);
+  LAUNCH_NV(ln_bwd_dx_kernel, D, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd,
+            (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, rows);
   RRFP_CUDA_TRY(cudaGetLastError());
+  if (dg || db) {
+    const int rpb = 64;
+    dim3 g2((D + 255) / 256, (rows + rpb - 1) / rpb);
+    ln_param_grad_kernel<<<g2, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
+                                             rstd, dg, db, rows, D, rpb);
+    RRFP_CUDA_TRY(cudaGetLastError());
+  }
   return RRFP_OK;
 }
 
@@ -310,7 +359,8 @@ extern "C" int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE,
 }
 
 extern "C" int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows, int cols, void* stream) {
-  const int rpb = 128;
+  if (cols % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "bias grad needs cols, ld multiples of 8");
+  const int rpb = 64;
   dim3 grid((cols + 255) / 256, (rows + rpb - 1) / rpb);
   colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)dy, ld, db, rows, cols, rpb);
   RRFP_CUDA_TRY(cudaGetLastError());

@@ -190,10 +190,12 @@ class StageCompute:
         e = lambda *s: torch.empty(*s, device=dev, dtype=bf)
         f32 = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
         self.x0 = e(n_mb, S, D) if self.first else None
-        self.h1, self.qkv, self.o, self.x2 = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D), e(n_mb, nl, S, D), e(n_mb, nl, S, D)
+        self.h1, self.qkv, self.x2 = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D), e(n_mb, nl, S, D)
+        # (the attention output lives in cuDNN's BSHD output buffer, see _attn_fwd)
         self.h2, self.pre, self.act, self.y = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd), e(n_mb, nl, S, Fd), e(n_mb, nl, S, D)
         self.m1, self.r1, self.m2, self.r2 = f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S)
         self.attn_aux = [[None] * nl for _ in range(n_mb)]
+        self.o_view = [[None] * nl for _ in range(n_mb)]   # attention output as [S, D]
         if self.last:
             self.hf, self.mf, self.rf = e(n_mb, S, D), f32(n_mb, S), f32(n_mb, S)
             self.logits = e(n_mb, S, V)
@@ -232,7 +234,13 @@ class StageCompute:
             q, k, v, None, True, 0.0, True, False, scale=1.0 / math.sqrt(Dh))
         o4, lse = out[0], out[1]
         self.attn_aux[mb][li] = (o4, lse, out[2], out[3], out[4], out[5], out[6], out[7])
-        self.o[mb, li].view(S, H, Dh).copy_(o4[0].transpose(0, 1))
+        o_sd = o4[0].transpose(0, 1)
+        if o_sd.is_contiguous():          # cuDNN writes BSHD: use it in place as [S, D]
+            self.o_view[mb][li] = o_sd.reshape(S, D)
+        else:
+            o = torch.empty(S, D, device=self.device, dtype=torch.bfloat16)
+            o.view(S, H, Dh).copy_(o_sd)
+            self.o_view[mb][li] = o
 
     def forward(self, mb: int):
         cfg = self.cfg
@@ -250,7 +258,7 @@ class StageCompute:
             _ln_fwd(x, p["ln1_g"], p["ln1_b"], self.h1[mb, li], self.m1[mb, li], self.r1[mb, li], cfg.eps)
             K.gemm(self.h1[mb, li], p["w_qkv"], self.qkv[mb, li], bias=p["b_qkv"])
             self._attn_fwd(self.qkv[mb, li], mb, li)
-            K.gemm(self.o[mb, li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
+            K.gemm(self.o_view[mb][li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
             _ln_fwd(self.x2[mb, li], p["ln2_g"], p["ln2_b"], self.h2[mb, li], self.m2[mb, li],
                     self.r2[mb, li], cfg.eps)
             K.gemm(self.h2[mb, li], p["w_1"], self.pre[mb, li], epi=K.EPI_BIAS_GELU,
@@ -338,7 +346,7 @@ class StageCompute:
             # out-proj dgrad -> attention backward -> QKV dgrad
             K.gemm(d_x2, p["w_o"], self.d_head, b_mn=True, m=S, n=D, k=D)
             if fused_w:
-                K.gemm(d_x2, self.o[mb, li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                K.gemm(d_x2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
                        accumulate=True, m=D, n=D, k=S)
                 _bias_grad(d_x2, g["b_o"])
             d_qkv = self.gqkv[mb, li] if dec else self.d_qkv_s
@@ -394,7 +402,7 @@ class StageCompute:
             K.gemm(self.gpre[mb, li], self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
                    b_mn=True, accumulate=True, m=Fd, n=D, k=S)
             _bias_grad(self.gpre[mb, li], g["b_1"])
-            K.gemm(self.gx2[mb, li], self.o[mb, li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
+            K.gemm(self.gx2[mb, li], self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
                    b_mn=True, accumulate=True, m=D, n=D, k=S)
             _bias_grad(self.gx2[mb, li], g["b_o"])
             K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,

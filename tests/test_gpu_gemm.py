@@ -5,6 +5,14 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=[1, 0], ids=["pair", "single"], autouse=True)
+def variant(request):
+    from paper_2605_18750_b200 import _lib
+    _lib.lib().rrfp_gemm_set_variant(request.param)
+    yield request.param
+    _lib.lib().rrfp_gemm_set_variant(1)
+
+
 def _rand(*shape, scale=1.0):
     return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
 
@@ -16,7 +24,7 @@ def _close(got, want, tol=2e-2):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (2048, 6144, 2048),
-                                   (384, 300, 192), (200, 256, 128)])
+                                   (384, 300, 192), (200, 256, 128), (2048, 50304, 2048)])
 def test_gemm_forward_kk(M, N, K):
     from paper_2605_18750_b200 import kernels as Kn
     torch.manual_seed(0)
