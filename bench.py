@@ -214,9 +214,16 @@ def gemm_roofline(cfg, peak_tf):
             "avg_launch_us": round(ms * 1e3, 1)}
 
 
+def _log(msg):
+    sys.stderr.write(f"[bench {time.strftime('%H:%M:%S')}] {msg}\n")
+    sys.stderr.flush()
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
+    if os.environ.get("RRFP_SAME_DEVICE") == "1":     # 1-GPU test of the multi-process path
+        local = 0
     torch.cuda.set_device(local)
     from paper_2605_18750_b200.model import GPTConfig
     from paper_2605_18750_b200.jitter import PRESETS
@@ -228,7 +235,8 @@ def run_ours(args):
     t_build = time.perf_counter()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # plumbing only (handle exchange, barriers, max-over-ranks): gloo on host tensors
+        dist.init_process_group("gloo")
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
         stages = [pipe.stage]
@@ -237,6 +245,7 @@ def run_ours(args):
         pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
         stages = pipe.stages
     t_build = time.perf_counter() - t_build
+    _log(f"built in {t_build:.1f}s")
     first = stages[0] if stages[0].first else None
     last = stages[-1] if stages[-1].last else None
     tok_h = first.tokens.cpu().pin_memory() if first else None
@@ -251,6 +260,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         pipe.step()
     barrier()
+    _log("warm-up done")
     lane_stream = pipe.group.streams[next(iter(pipe.group.streams))]
     peak_sus, peak_burst, hbm, peak_kind = load_peaks()
     with ClockSampler(local) as clk:
@@ -276,7 +286,7 @@ def run_ours(args):
         barrier()
         e2e_s = (time.perf_counter() - t0) / args.steps
     if dist:
-        t = torch.tensor([ms, e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_s = t[0].item(), t[1].item()
     from paper_2605_18750_b200.runtime import wall_trace
@@ -292,6 +302,7 @@ def run_ours(args):
                 x.t0, x.t1, x.kind, x.stage, x.rank, x.task = t
                 ev.append(x)
         t0n = min(t for _, t in allev)
+    _log("timed region done")
     tr, met = wall_trace(pipe.workload, ev, t0n)
     bubble = met.bubble_fraction()
     it_s = 1000.0 / ms
@@ -305,6 +316,7 @@ def run_ours(args):
             per.append(round(sum(xs) / len(xs), 1) if xs else 0.0)
         task_us[d] = per
     roof = gemm_roofline(cfg, peak_sus)
+    _log("roofline done")
     roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
     fF, fB, fW = cfg.flops_per_layer()
     it_flops = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
@@ -312,7 +324,7 @@ def run_ours(args):
     t_roof = it_flops / (n * peak_sus * 1e12) + p2p / 770e9
     launches = pipe.kernel_launches_per_step() if hasattr(pipe, "kernel_launches_per_step") else 0
     if dist:
-        lt = torch.tensor([launches], device="cuda")
+        lt = torch.tensor([launches], dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt.item())
     line = {"metric": METRIC, "value": round(it_s, 4), "unit": "iter/s", "n_gpus": world,

@@ -225,6 +225,8 @@ int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, const void*
                    const void* B, long long ldb, void* C, long long ldc, void* C2, long long ldc2,
                    const void* bias, const void* R, long long ldr, int accumulate, void* stream);
 int rrfp_gemm_set_variant(int pair);
+/* Programmatic dependent launch for the stage kernels (default on; env RRFP_PDL=0 disables). */
+int rrfp_set_pdl(int on);
 int rrfp_gemm_reserve_sms(int n);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
@@ -237,6 +239,8 @@ int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x
 int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP, int rows, int D,
                        void* stream);
 int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows, int cols, void* stream);
+int rrfp_copy_rows(void* dst, long long ldd_bytes, const void* src, long long lds_bytes, int rows,
+                   long long width_bytes, void* stream);
 int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* target, int rows, int V,
                   float* loss, float* lse, void* stream);
 int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, int V,

@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  sm100::griddep_launch();
+  sm100::griddep_wait();
 
   const int num_tiles = g.tiles_m * g.tiles_n;
   const int kblocks = (g.K + BK - 1) / BK;
@@ -354,6 +356,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   sm100::cluster_sync();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  sm100::griddep_launch();
+  sm100::griddep_wait();
 
   const int num_tiles = g.tiles_m * g.tiles_n;
   const int kblocks = (g.K + BK - 1) / BK;
@@ -516,8 +520,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs g, cudaSt
   int pairs = (g_num_sms - g_reserve_sms) / 2;
   if (pairs < 1) pairs = 1;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, 256, P_SMEM_BYTES, st>>>(ta, tb, g);
-  RRFP_CUDA_TRY(cudaGetLastError());
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, g));
   return RRFP_OK;
 }
 
@@ -533,8 +536,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
   int sms = g_num_sms - g_reserve_sms;
   if (sms < 1) sms = 1;
   int grid = tiles < sms ? tiles : sms;
-  kern<<<grid, 256, SMEM_BYTES, st>>>(ta, tb, g);
-  RRFP_CUDA_TRY(cudaGetLastError());
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), SMEM_BYTES, st, ta, tb, g));
   return RRFP_OK;
 }
 

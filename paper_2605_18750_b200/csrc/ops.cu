@@ -9,6 +9,7 @@
 
 #include "../../include/rrfp_b200.h"
 #include "rrfp_common.h"
+#include "sm100_ptx.cuh"
 
 namespace {
 
@@ -51,6 +52,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
                                                      float* __restrict__ mean_out,
                                                      float* __restrict__ rstd_out, int rows,
                                                      float eps) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   constexpr int D = 256 * NV;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -92,6 +95,8 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
     const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
     __nv_bfloat16* __restrict__ dx, int rows) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   constexpr int D = 256 * NV;
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -136,6 +141,8 @@ __global__ void __launch_bounds__(256) ln_param_grad_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ dg,
     float* __restrict__ db, int rows, int D, int rows_per_block) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   __shared__ float sg[8][256], sb[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * 256 + lane * 8;
@@ -175,6 +182,8 @@ __global__ void __launch_bounds__(256) ln_param_grad_kernel(
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
                                  const __nv_bfloat16* __restrict__ P, __nv_bfloat16* __restrict__ x,
                                  int rows, int D) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   const __nv_bfloat16* e = E + (size_t)tok[row] * D;
@@ -191,6 +200,8 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 
 __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
                                  float* __restrict__ dE, float* __restrict__ dP, int rows, int D) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= rows) return;
   float* e = dE + (size_t)tok[row] * D;
@@ -212,6 +223,8 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ld,
                                                      float* __restrict__ db, int rows, int cols,
                                                      int rows_per_block) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   __shared__ float sb[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * 256 + lane * 8;
@@ -258,6 +271,8 @@ __device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
 __global__ void __launch_bounds__(512) xent_fwd_kernel(const __nv_bfloat16* __restrict__ logits, long long ld,
                                                        const int32_t* __restrict__ target, int V,
                                                        float* __restrict__ loss, float* __restrict__ lse_out) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   __shared__ float sh[32];
   const __nv_bfloat16* row = logits + (size_t)blockIdx.x * ld;
   float m = -INFINITY;
@@ -287,6 +302,8 @@ __global__ void __launch_bounds__(512) xent_fwd_kernel(const __nv_bfloat16* __re
 __global__ void __launch_bounds__(512) xent_bwd_kernel(__nv_bfloat16* __restrict__ logits, long long ld,
                                                        const int32_t* __restrict__ target, int V,
                                                        const float* __restrict__ lse_in, float scale) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
   __nv_bfloat16* row = logits + (size_t)blockIdx.x * ld;
   const float lse = lse_in[blockIdx.x];
   const int t = target[blockIdx.x];
@@ -299,15 +316,29 @@ __global__ void __launch_bounds__(512) xent_bwd_kernel(__nv_bfloat16* __restrict
   }
 }
 
+// strided 2-D copy, 16-byte vectors: dst[r, :w] = src[r, :w]   (w in bytes)
+__global__ void copy_rows_kernel(char* __restrict__ dst, long long ldd, const char* __restrict__ src,
+                                 long long lds, int rows, int w16) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = (long long)rows * w16;
+  for (long long k = i; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long r = k / w16, c = k % w16;
+    *reinterpret_cast<uint4*>(dst + r * ldd + c * 16) =
+        __ldg(reinterpret_cast<const uint4*>(src + r * lds + c * 16));
+  }
+}
+
 }  // namespace
 
-#define LAUNCH_NV(KERNEL, D, ...)                                             \
-  switch ((D) / 256) {                                                        \
-    case 1: KERNEL<1><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
-    case 2: KERNEL<2><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
-    case 4: KERNEL<4><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
-    case 8: KERNEL<8><<<grid, 256, 0, st>>>(__VA_ARGS__); break;              \
-    case 16: KERNEL<16><<<grid, 256, 0, st>>>(__VA_ARGS__); break;            \
+#define LAUNCH_NV(KERNEL, D, ...)                                                          \
+  switch ((D) / 256) {                                                                     \
+    case 1: RRFP_CUDA_TRY(rrfp_launch(KERNEL<1>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 2: RRFP_CUDA_TRY(rrfp_launch(KERNEL<2>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 4: RRFP_CUDA_TRY(rrfp_launch(KERNEL<4>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 8: RRFP_CUDA_TRY(rrfp_launch(KERNEL<8>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 16: RRFP_CUDA_TRY(rrfp_launch(KERNEL<16>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     default: return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported", (int)(D)); \
   }
 
@@ -333,8 +364,8 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
   if (dg || db) {
     const int rpb = 64;
     dim3 g2((D + 255) / 256, (rows + rpb - 1) / rpb);
-    ln_param_grad_kernel<<<g2, 256, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
-                                             rstd, dg, db, rows, D, rpb);
+    RRFP_CUDA_TRY(rrfp_launch(ln_param_grad_kernel, g2, dim3(256), 0, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
+                                             rstd, dg, db, rows, D, rpb));
     RRFP_CUDA_TRY(cudaGetLastError());
   }
   return RRFP_OK;
@@ -343,8 +374,7 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
 extern "C" int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x, int rows,
                                   int D, void* stream) {
   if (D % 8) return rrfp_fail(RRFP_E_INVALID, "embedding width must be a multiple of 8");
-  embed_fwd_kernel<<<(rows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      tok, (const __nv_bfloat16*)E, (const __nv_bfloat16*)P, (__nv_bfloat16*)x, rows, D);
+  RRFP_CUDA_TRY(rrfp_launch(embed_fwd_kernel, dim3((rows + 7) / 8), dim3(256), 0, (cudaStream_t)stream, tok, (const __nv_bfloat16*)E, (const __nv_bfloat16*)P, (__nv_bfloat16*)x, rows, D));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }
@@ -352,8 +382,7 @@ extern "C" int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void*
 extern "C" int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP, int rows,
                                   int D, void* stream) {
   if (D % 8) return rrfp_fail(RRFP_E_INVALID, "embedding width must be a multiple of 8");
-  embed_bwd_kernel<<<(rows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      tok, (const __nv_bfloat16*)dx, dE, dP, rows, D);
+  RRFP_CUDA_TRY(rrfp_launch(embed_bwd_kernel, dim3((rows + 7) / 8), dim3(256), 0, (cudaStream_t)stream, tok, (const __nv_bfloat16*)dx, dE, dP, rows, D));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }
@@ -362,7 +391,7 @@ extern "C" int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows,
   if (cols % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "bias grad needs cols, ld multiples of 8");
   const int rpb = 64;
   dim3 grid((cols + 255) / 256, (rows + rpb - 1) / rpb);
-  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)dy, ld, db, rows, cols, rpb);
+  RRFP_CUDA_TRY(rrfp_launch(colsum_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)dy, ld, db, rows, cols, rpb));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }
@@ -370,8 +399,8 @@ extern "C" int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows,
 extern "C" int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* target, int rows, int V,
                              float* loss, float* lse, void* stream) {
   if (V % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "vocab / ld must be multiples of 8");
-  xent_fwd_kernel<<<rows, 512, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)logits, ld, target, V,
-                                                          loss, lse);
+  RRFP_CUDA_TRY(rrfp_launch(xent_fwd_kernel, dim3(rows), dim3(512), 0, (cudaStream_t)stream, (const __nv_bfloat16*)logits, ld, target, V,
+                                                          loss, lse));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }
@@ -379,8 +408,22 @@ extern "C" int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* ta
 extern "C" int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, int V,
                              const float* lse, float scale, void* stream) {
   if (V % 8 || ld % 8) return rrfp_fail(RRFP_E_INVALID, "vocab / ld must be multiples of 8");
-  xent_bwd_kernel<<<rows, 512, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)logits, ld, target, V, lse,
-                                                          scale);
+  RRFP_CUDA_TRY(rrfp_launch(xent_bwd_kernel, dim3(rows), dim3(512), 0, (cudaStream_t)stream, (__nv_bfloat16*)logits, ld, target, V, lse,
+                                                          scale));
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_copy_rows(void* dst, long long ldd_bytes, const void* src, long long lds_bytes,
+                              int rows, long long width_bytes, void* stream) {
+  if (width_bytes % 16 || ldd_bytes % 16 || lds_bytes % 16 || (uintptr_t)dst % 16 || (uintptr_t)src % 16)
+    return rrfp_fail(RRFP_E_INVALID, "copy_rows needs 16-byte aligned rows");
+  const int w16 = (int)(width_bytes / 16);
+  long long n = (long long)rows * w16;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  RRFP_CUDA_TRY(rrfp_launch(copy_rows_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, (char*)dst, ldd_bytes, (const char*)src,
+                                                              lds_bytes, rows, w16));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }

@@ -13,6 +13,7 @@
 // event times.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <string>
 
@@ -32,6 +33,19 @@ int rrfp_fail(int code, const char* fmt, ...) {
   return code;
 }
 extern "C" int rrfp_abi_version(void) { return 1; }
+
+static int g_pdl = -1;
+bool rrfp_pdl() {
+  if (g_pdl < 0) {
+    const char* e = getenv("RRFP_PDL");
+    g_pdl = e ? atoi(e) : 1;
+  }
+  return g_pdl != 0;
+}
+extern "C" int rrfp_set_pdl(int on) {
+  g_pdl = on ? 1 : 0;
+  return RRFP_OK;
+}
 
 static int check_desc(const rrfp_iter_desc* d) {
   if (!d) return rrfp_fail(RRFP_E_INVALID, "null iter desc");

@@ -185,4 +185,14 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// ------------------------------------------- programmatic dependent launch
+// wait until the preceding grid has completed and its writes are visible
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// allow the next grid on the stream to be scheduled (it still waits in griddep_wait)
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace sm100

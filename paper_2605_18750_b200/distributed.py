@@ -122,7 +122,14 @@ class DistPipeline:
         raw = self.stage.capture_bodies()
         self.group.set_bodies({(s, 0): raw})
         self.group.connect_ipc({(h["stage"], 0): h["lane"] for h in allh})
+        torch.cuda.synchronize()
         dist.barrier(group=group)
+        # every rank instantiates + uploads its lane graph before ANY rank launches
+        self.group.prepare()
+        dist.barrier(group=group)
+
+    def kernel_launches_per_step(self):
+        return sum(self.stage.kernel_counts.values()) + 2 * len(self.stage.kernel_counts) + 2
 
     def step(self, watchdog_secs=120.0):
         self.stage.zero_grads()

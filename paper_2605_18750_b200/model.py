@@ -202,11 +202,15 @@ class StageCompute:
             self.loss = torch.zeros(n_mb, S, device=dev)
             self.lse = f32(n_mb, S)
         # scratch shared by all bodies of this stage (bodies never overlap on a lane)
-        self.d_a = e(S, D)
-        self.d_b = e(S, D)
-        self.d_big = e(S, Fd)
-        self.d_qkv_s = e(S, 3 * D)
+        # two parity sets (layer li uses set li % 2) so the weight-gradient
+        # GEMMs of layer li can run on the side stream while layer li-1's
+        # input-gradient chain proceeds on the main stream
+        self.sd_a = [e(S, D), e(S, D)]
+        self.sd_b = [e(S, D), e(S, D)]
+        self.sd_big = [e(S, Fd), e(S, Fd)]
+        self.sd_qkv = [e(S, 3 * D), e(S, 3 * D)]
         self.d_head = e(S, D)
+        self.side = torch.cuda.Stream(dev)
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
             self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd)
             self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D)
@@ -288,21 +292,35 @@ class StageCompute:
 
     # ----------------------------------------------------------- backward
     def backward_input(self, mb: int):
-        """B task: input gradients (plus weight gradients unless decomposed).
+        """B task: input gradients, plus (unless decomposed) weight gradients.
 
-        Gradient buffers: dy of layer li lives in ``d_a`` (or the mailbox /
-        the decomposed slot ``gy[mb, li]``); d_x2 in ``d_b`` (or ``gx2``); the
-        layer-input gradient is written where the next-lower layer reads its
-        dy, and for layer 0 straight into the previous stage's mailbox.
+        Two streams: the input-gradient chain (dgrad GEMMs, LayerNorm and
+        attention backward) runs on the main stream; each layer's four
+        weight-gradient GEMMs + bias reductions run on a side stream as soon as
+        their inputs exist, so they fill the tail waves of the dgrad GEMMs.
+        Scratch comes in two parity sets; the main stream only rewrites a set
+        after the side stream finished reading it (events).
         """
         cfg = self.cfg
         S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
-        fused_w = not self.decompose
-        nl = len(self.layers)
         dec = self.decompose
+        fused_w = not dec
+        nl = len(self.layers)
+        main, side = torch.cuda.current_stream(), self.side
+        side_done = {}
 
-        def dy_slot(li):
-            return self.gy[mb, li] if dec else self.d_a
+        def ev():
+            e = torch.cuda.Event()
+            e.record(main)
+            return e
+
+        def on_side(after, fn):
+            with torch.cuda.stream(side):
+                side.wait_event(after)
+                fn()
+
+        def dy_buf(li):           # where layer li reads its output gradient
+            return self.gy[mb, li] if dec else self.sd_a[li % 2]
 
         if self.last:
             h, gh = self.head, self.g_head
@@ -311,11 +329,11 @@ class StageCompute:
             _lib.check(_lib.lib().rrfp_xent_bwd(
                 K._p(self.logits[mb]), C.c_longlong(V), K._p(self.targets[mb]), S, V,
                 K._p(self.lse[mb]), C.c_float(scale), K._stream()))
-            K.gemm(self.logits[mb], h["w_lm"], self.d_head, b_mn=True, m=S, n=D, k=V)
             if fused_w:
-                K.gemm(self.logits[mb], self.hf[mb], gh["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=V, n=D, k=S)
-            dy = dy_slot(nl - 1)
+                on_side(ev(), lambda: K.gemm(self.logits[mb], self.hf[mb], gh["w_lm"], epi=K.EPI_ACC_F32,
+                                             a_mn=True, b_mn=True, accumulate=True, m=V, n=D, k=S))
+            K.gemm(self.logits[mb], h["w_lm"], self.d_head, b_mn=True, m=S, n=D, k=V)
+            dy = dy_buf(nl - 1)
             _ln_bwd(self.d_head, self.y[mb, nl - 1], self.mf[mb], self.rf[mb], h["lnf_g"], None, dy,
                     gh["lnf_g"], gh["lnf_b"])
         else:
@@ -326,51 +344,68 @@ class StageCompute:
         for li in reversed(range(nl)):
             p, g = self.p[li], self.g[li]
             x = self._layer_input(mb, li)
+            q = li % 2
+            if li + 2 in side_done:          # set q was last read by layer li+2's side work
+                main.wait_event(side_done[li + 2])
+            d_pre = self.gpre[mb, li] if dec else self.sd_big[q]
+            d_x2 = self.gx2[mb, li] if dec else self.sd_b[q]
+            d_qkv = self.gqkv[mb, li] if dec else self.sd_qkv[q]
+            if fused_w:
+                dyy = dy
+                on_side(ev(), lambda: (K.gemm(dyy, self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fd, k=S),
+                                       _bias_grad(dyy, g["b_2"])))
             # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)
-            d_pre = self.gpre[mb, li] if dec else self.d_big
             K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=self.pre[mb, li],
                    m=S, n=Fd, k=D)
             if fused_w:
-                K.gemm(dy, self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
-                       accumulate=True, m=D, n=Fd, k=S)
-                _bias_grad(dy, g["b_2"])
+                on_side(ev(), lambda: (K.gemm(d_pre, self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=Fd, n=D, k=S),
+                                       _bias_grad(d_pre, g["b_1"])))
             # FC1 dgrad -> LN2 backward (+ residual grad dy)
             K.gemm(d_pre, p["w_1"], self.d_head, b_mn=True, m=S, n=D, k=Fd)
-            if fused_w:
-                K.gemm(d_pre, self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
-                       accumulate=True, m=Fd, n=D, k=S)
-                _bias_grad(d_pre, g["b_1"])
-            d_x2 = self.gx2[mb, li] if dec else self.d_b
             _ln_bwd(self.d_head, self.x2[mb, li], self.m2[mb, li], self.r2[mb, li], p["ln2_g"], dy,
                     d_x2, g["ln2_g"], g["ln2_b"])
+            if fused_w:
+                on_side(ev(), lambda: (K.gemm(d_x2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=D, k=S),
+                                       _bias_grad(d_x2, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
             K.gemm(d_x2, p["w_o"], self.d_head, b_mn=True, m=S, n=D, k=D)
-            if fused_w:
-                K.gemm(d_x2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
-                       accumulate=True, m=D, n=D, k=S)
-                _bias_grad(d_x2, g["b_o"])
-            d_qkv = self.gqkv[mb, li] if dec else self.d_qkv_s
             self._attn_bwd(mb, li, self.d_head, d_qkv)
-            K.gemm(d_qkv, p["w_qkv"], self.d_head, b_mn=True, m=S, n=D, k=3 * D)
             if fused_w:
-                K.gemm(d_qkv, self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
-                       accumulate=True, m=3 * D, n=D, k=S)
-                _bias_grad(d_qkv, g["b_qkv"])
+                def qkv_w(d_qkv=d_qkv, li=li, g=g):
+                    K.gemm(d_qkv, self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
+                    _bias_grad(d_qkv, g["b_qkv"])
+                on_side(ev(), qkv_w)
+                done = torch.cuda.Event()
+                done.record(side)
+                side_done[li] = done
+            K.gemm(d_qkv, p["w_qkv"], self.d_head, b_mn=True, m=S, n=D, k=3 * D)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             if li > 0:
-                dx = dy_slot(li - 1)
+                dx = dy_buf(li - 1)
+                if fused_w and li + 1 in side_done:   # layer li+1's side work read this buffer
+                    main.wait_event(side_done[li + 1])
             elif not self.first:
-                dx = self.bwd_out[mb] if self.bwd_out is not None else self.d_a
+                dx = self.bwd_out[mb] if self.bwd_out is not None else self.sd_a[1]
             else:
-                dx = self.gx0[mb] if dec else self.d_a
+                dx = self.gx0[mb] if dec else self.sd_a[1]
+                if fused_w and 1 in side_done:
+                    main.wait_event(side_done[1])
             _ln_bwd(self.d_head, x, self.m1[mb, li], self.r1[mb, li], p["ln1_g"], d_x2, dx,
                     g["ln1_g"], g["ln1_b"])
             dy = dx
         if self.first and fused_w:
-            K.note()
-            _lib.check(_lib.lib().rrfp_embedding_bwd(
-                K._p(self.tokens[mb]), K._p(dy), K._p(self.g_emb["wte"]), K._p(self.g_emb["wpe"]),
-                S, D, K._stream()))
+            dyy = dy
+            on_side(ev(), lambda: (K.note(), _lib.check(_lib.lib().rrfp_embedding_bwd(
+                K._p(self.tokens[mb]), K._p(dyy), K._p(self.g_emb["wte"]), K._p(self.g_emb["wpe"]),
+                S, D, K._stream()))))
+        if fused_w:
+            join = torch.cuda.Event()
+            join.record(side)
+            main.wait_event(join)
 
     def _attn_bwd(self, mb, li, d_o, d_qkv):
         cfg = self.cfg
@@ -384,38 +419,55 @@ class StageCompute:
         dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
             go, q, k, v, o4, lse, ps, po, None, cq, ck, mq, mk, 0.0,
             True, scale=1.0 / math.sqrt(Dh))
-        d_qkv[:, :D].view(S, H, Dh).copy_(dq[0].transpose(0, 1))
-        d_qkv[:, D:2 * D].view(S, H, Dh).copy_(dk[0].transpose(0, 1))
-        d_qkv[:, 2 * D:].view(S, H, Dh).copy_(dv[0].transpose(0, 1))
+        for i, t in enumerate((dq, dk, dv)):
+            t_sd = t[0].transpose(0, 1)
+            if t_sd.is_contiguous():       # cuDNN returns BSHD: a row-major [S, D] matrix
+                K.note()
+                _lib.check(_lib.lib().rrfp_copy_rows(
+                    C.c_void_p(d_qkv.data_ptr() + i * D * 2), C.c_longlong(d_qkv.stride(0) * 2),
+                    C.c_void_p(t.data_ptr()), C.c_longlong(D * 2), S, C.c_longlong(D * 2), K._stream()))
+            else:
+                d_qkv[:, i * D:(i + 1) * D].view(S, H, Dh).copy_(t_sd)
 
     def backward_weight(self, mb: int):
-        """W task (decomposed backward): weight gradients from saved inputs/grads."""
+        """W task (decomposed backward): weight gradients from saved inputs/grads.
+        Layers alternate between the main and the side stream (independent GEMMs
+        fill each other's tail waves); joined at the end."""
         if not self.decompose:
             return
         cfg = self.cfg
         S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
+        main, side = torch.cuda.current_stream(), self.side
+        fork = torch.cuda.Event()
+        fork.record(main)
+        side.wait_event(fork)
         for li in reversed(range(len(self.layers))):
             g = self.g[li]
-            K.gemm(self.gy[mb, li], self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
-                   b_mn=True, accumulate=True, m=D, n=Fd, k=S)
-            _bias_grad(self.gy[mb, li], g["b_2"])
-            K.gemm(self.gpre[mb, li], self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
-                   b_mn=True, accumulate=True, m=Fd, n=D, k=S)
-            _bias_grad(self.gpre[mb, li], g["b_1"])
-            K.gemm(self.gx2[mb, li], self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
-                   b_mn=True, accumulate=True, m=D, n=D, k=S)
-            _bias_grad(self.gx2[mb, li], g["b_o"])
-            K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                   b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
-            _bias_grad(self.gqkv[mb, li], g["b_qkv"])
-        if self.last:
-            K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
-                   b_mn=True, accumulate=True, m=cfg.vocab, n=D, k=S)
-        if self.first:
-            K.note()
-            _lib.check(_lib.lib().rrfp_embedding_bwd(
-                K._p(self.tokens[mb]), K._p(self.gx0[mb]), K._p(self.g_emb["wte"]),
-                K._p(self.g_emb["wpe"]), S, D, K._stream()))
+            with torch.cuda.stream(side if li % 2 else main):
+                K.gemm(self.gy[mb, li], self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=D, n=Fd, k=S)
+                _bias_grad(self.gy[mb, li], g["b_2"])
+                K.gemm(self.gpre[mb, li], self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=Fd, n=D, k=S)
+                _bias_grad(self.gpre[mb, li], g["b_1"])
+                K.gemm(self.gx2[mb, li], self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=D, n=D, k=S)
+                _bias_grad(self.gx2[mb, li], g["b_o"])
+                K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
+                _bias_grad(self.gqkv[mb, li], g["b_qkv"])
+        with torch.cuda.stream(side):
+            if self.last:
+                K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=cfg.vocab, n=D, k=S)
+            if self.first:
+                K.note()
+                _lib.check(_lib.lib().rrfp_embedding_bwd(
+                    K._p(self.tokens[mb]), K._p(self.gx0[mb]), K._p(self.g_emb["wte"]),
+                    K._p(self.g_emb["wpe"]), S, D, K._stream()))
+        join = torch.cuda.Event()
+        join.record(side)
+        main.wait_event(join)
 
     def zero_grads(self):
         for gd in self.g + ([self.g_emb] if self.g_emb else []) + ([self.g_head] if self.g_head else []):

@@ -1,0 +1,48 @@
+"""Multi-process pipeline check (one stage per process) -- run under torchrun.
+
+With RRFP_SAME_DEVICE=1 every rank uses cuda:0 (CUDA IPC between processes on
+one GPU) so the IPC mailbox / peer-flag path can be exercised on a 1-GPU box.
+Prints the last stage's loss and the single-process PP=1 loss of the same model.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import torch.distributed as dist
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    same = os.environ.get("RRFP_SAME_DEVICE") == "1"
+    dev = 0 if same else int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
+    from paper_2605_18750_b200.model import GPTConfig
+    from paper_2605_18750_b200.distributed import DistPipeline
+    cfg = GPTConfig(n_layer=4, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=256)
+    hint = sys.argv[1] if len(sys.argv) > 1 else "bf"
+    pipe = DistPipeline(cfg, 4, hint=hint)
+    losses = []
+    for _ in range(2):
+        loss = pipe.step(watchdog_secs=60)
+        dist.barrier()
+        losses.append(None if loss is None else loss.item())
+    ev, t0 = pipe.last_events
+    n_exec = sum(1 for e in ev if e.kind == 0)
+    out = [None] * world
+    dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec})
+    pipe.close()
+    if rank == 0:
+        from paper_2605_18750_b200.pipeline import GpuPipeline
+        ref = GpuPipeline(cfg, 1, 4, hint=hint)
+        ref_loss = ref.step().item()
+        ref.close()
+        print(json.dumps({"ranks": out, "single_process_pp1_loss": ref_loss}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
