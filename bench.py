@@ -232,18 +232,12 @@ def run_ours(args):
     hint = "bf" if args.hint == "1f1b" else args.hint
     mode = "fixed" if args.hint == "1f1b" else "free"
     dist = None
-    t_build = time.perf_counter()
     if world > 1:
         import torch.distributed as dist
         # plumbing only (handle exchange, barriers, max-over-ranks): gloo on host tensors
         dist.init_process_group("gloo")
-        from paper_2605_18750_b200.distributed import DistPipeline
-        pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
-        stages = [pipe.stage]
-    else:
-        from paper_2605_18750_b200.pipeline import GpuPipeline
-        pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.jitter])
-        stages = pipe.stages
+    t_build = time.perf_counter()
+    pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS[args.jitter])
     t_build = time.perf_counter() - t_build
     _log(f"built in {t_build:.1f}s")
     first = stages[0] if stages[0].first else None
@@ -346,12 +340,87 @@ def run_ours(args):
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
+    nominal = {s_: {d: task_us[d][s_] for d in ("F", "B", "W")} for s_ in range(n)}
+    pipe.close()
+    del pipe, stages, first, last
+    if args.compare or (world > 1 and args.compare is None):
+        line["variants"] = compare_variants(cfg, args, world, dist, barrier, nominal)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    pipe.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
+    if world > 1:
+        from paper_2605_18750_b200.distributed import DistPipeline
+        pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay)
+        return pipe, [pipe.stage]
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay)
+    return pipe, pipe.stages
+
+
+def compare_variants(cfg, args, world, dist, barrier, nominal):
+    """Same kernels, same box: fixed-order 1F1B vs RRFP (BF, BFW), without and
+    with injected lognormal compute + comm jitter (sigma = args.sigma, paired
+    draws keyed by task).  Each variant: build, calibrate, K timed steps."""
+    import gc
+    import math
+    import torch
+    from paper_2605_18750_b200.jitter import PRESETS
+    from paper_2605_18750_b200.workload import CommDelay
+    out = {}
+    sigmas = [0.0] + ([args.sigma] if args.sigma > 0 else [])
+    for sigma in sigmas:
+        comm = None
+        if sigma > 0:
+            comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
+                             hi=int(args.comm_us * 50), seed=17)
+        for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
+            if world == 1 and name == "bfw" and cfg.n_layer * args.mb > 8 * 32:
+                continue          # PP=1 BFW keeps every W pending: memory-bound, meaningless
+            pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS["J0"], comm)
+            for _ in range(2):
+                pipe.step()
+            if sigma > 0:
+                if world > 1:
+                    pipe.set_lognormal_jitter(sigma, seed=11)
+                else:
+                    pipe.set_lognormal_jitter(sigma, seed=11)
+                pipe.step()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                pipe.launch()
+                pipe.wait()
+            barrier()
+            ms = (time.perf_counter() - t0) * 1e3 / args.steps
+            if dist:
+                t = torch.tensor([ms], dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = t.item()
+            from paper_2605_18750_b200.runtime import wall_trace
+            ev, t0n = pipe.last_events
+            bub = None
+            if not dist:
+                tr, met = wall_trace(pipe.workload, ev, t0n)
+                bub = round(met.bubble_fraction(), 4)
+            out[f"{name}@sigma{sigma}"] = {"iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
+                                           "bubble_fraction": bub}
+            pipe.close()
+            del pipe, stages
+            gc.collect()
+            torch.cuda.empty_cache()
+            _log(f"variant {name} sigma={sigma}: {ms:.1f} ms")
+        base = out.get(f"1f1b@sigma{sigma}")
+        if base:
+            for name in ("bf", "bfw"):
+                v = out.get(f"{name}@sigma{sigma}")
+                if v:
+                    v["speedup_vs_1f1b"] = round(base["ms"] / v["ms"], 4)
+    return out
 
 
 def cpu_baseline(args, n, task_us):
@@ -392,6 +461,12 @@ def main():
     ap.add_argument("--layers", type=int, default=24)
     ap.add_argument("--jitter", default="J0")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--compare", dest="compare", action="store_true", default=None,
+                    help="also time fixed 1F1B / BF / BFW (default on for N>1)")
+    ap.add_argument("--no-compare", dest="compare", action="store_false")
+    ap.add_argument("--sigma", type=float, default=0.5,
+                    help="lognormal compute+comm jitter sigma of the comparison runs")
+    ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -194,10 +194,13 @@ void rrfp_ipc_free(void* dev_ptr);
 int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst_inboxes, void* const* bwd_dst_inboxes,
                          void* const* tp_peer_inboxes);
 /* Load host tables (per-lane): dur_ns[3*KEYS] (spin length incl. injected
- * delay), comm_ns[2*KEYS] (flag visibility delay of sent messages),
- * skew_ns[2*KEYS*R] (arrival skew per destination rank), fixed order. */
+ * delay; with caller bodies: the additive jitter pad), comm_ns[2*KEYS] (flag
+ * visibility delay of sent messages), skew_ns[2*KEYS*R] (arrival skew per
+ * destination rank), fixed order, min_ns[3*KEYS] (optional task floor:
+ * end >= start + min_ns, the lognormal compute jitter).  May be reloaded
+ * between iterations. */
 int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
-                             const int64_t* skew_ns, const rrfp_task_t* fixed);
+                             const int64_t* skew_ns, const rrfp_task_t* fixed, const int64_t* min_ns);
 /* Register caller-captured compute bodies: graphs[kind * M + mb] is the
  * cudaGraph_t run for task (kind, mb) (kind: 0 = B, 1 = F, 2 = W; NULL = no
  * work), n = 3 * M.  The dispatcher selects the branch with

@@ -67,6 +67,7 @@ struct lane_state {
   const long long* dur_ns;                  // [3][KEYS] spin / jitter pad
   const long long* comm_ns;                 // [2][KEYS]
   const long long* dskew_ns;                // [2][KEYS][R] arrival skew of a sent msg at each dest rank
+  const long long* min_ns;                  // [3][KEYS] task floor: end >= start + min_ns (lognormal jitter)
   const rrfp_task_t* fixed;                 // [per_stage]
   rrfp_event* ring;
   int32_t ring_n, ring_cap;
@@ -429,9 +430,14 @@ __global__ void lane_complete_kernel(lane_state* L) {
   int mb = rrfp_task_mb(t), c = rrfp_task_chunk(t);
   int k = rrfp_key(mb, c, d.MW);
   if (d.compute_kind == 1) {
-    // K11: injected jitter pads real compute (dur table holds the injection only)
+    // K11: injected jitter pads real compute: an additive delay (the J-level
+    // injection table) and a floor start + nominal * X (lognormal compute jitter)
     long long pad = L->dur_ns[(size_t)kind * L->KEYS + k];
-    if (pad > 0) spin_until(gtimer() + (unsigned long long)pad);
+    long long floor_ns = L->min_ns[(size_t)kind * L->KEYS + k];
+    unsigned long long until = gtimer() + (unsigned long long)(pad > 0 ? pad : 0);
+    if (floor_ns > 0 && L->t_start + (unsigned long long)floor_ns > until)
+      until = L->t_start + (unsigned long long)floor_ns;
+    spin_until(until);
   }
   unsigned long long end = gtimer();
   ring_emit(L, 0, L->t_start, end, d.R > 1 ? d.rank : -1, t);
@@ -504,7 +510,7 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   RRFP_CUDA_TRY(cudaMalloc(&rt->L, sizeof(lane_state)));
   RRFP_CUDA_TRY(cudaMalloc(&rt->inbox, sizeof(lane_inbox)));
   RRFP_CUDA_TRY(cudaMemset(rt->inbox, 0, sizeof(lane_inbox)));
-  size_t tbytes = sizeof(long long) * (size_t)rt->KEYS * (3 + 2 + 2 * desc->R);
+  size_t tbytes = sizeof(long long) * (size_t)rt->KEYS * (3 + 2 + 2 * desc->R + 3);
   RRFP_CUDA_TRY(cudaMalloc(&rt->tables, tbytes));
   RRFP_CUDA_TRY(cudaMemset(rt->tables, 0, tbytes));
   RRFP_CUDA_TRY(cudaMalloc(&rt->fixed, sizeof(rrfp_task_t) * (size_t)(desc->per_stage + 1)));
@@ -527,6 +533,7 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   h.dur_ns = rt->tables;
   h.comm_ns = rt->tables + 3 * rt->KEYS;
   h.dskew_ns = rt->tables + 5 * (size_t)rt->KEYS;
+  h.min_ns = rt->tables + (5 + 2 * desc->R) * (size_t)rt->KEYS;
   h.fixed = rt->fixed;
   h.ring = rt->ring;
   h.ring_cap = desc->trace_cap;
@@ -624,7 +631,8 @@ extern "C" int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst, void
 // skew_ns[2*KEYS*R]: arrival skew at each destination rank, indexed by
 // [send direction][destination key][rank].
 extern "C" int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
-                                        const int64_t* skew_ns, const rrfp_task_t* fixed) {
+                                        const int64_t* skew_ns, const rrfp_task_t* fixed,
+                                        const int64_t* min_ns) {
   if (!rt || !dur_ns || !comm_ns || !skew_ns) return rrfp_fail(RRFP_E_INVALID, "null table");
   RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
   size_t K = rt->KEYS, R = rt->d.R;
@@ -632,6 +640,11 @@ extern "C" int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns,
   RRFP_CUDA_TRY(cudaMemcpy(rt->tables + 3 * K, comm_ns, sizeof(long long) * 2 * K, cudaMemcpyHostToDevice));
   RRFP_CUDA_TRY(cudaMemcpy(rt->tables + 5 * K, skew_ns, sizeof(long long) * 2 * K * R,
                            cudaMemcpyHostToDevice));
+  if (min_ns)
+    RRFP_CUDA_TRY(cudaMemcpy(rt->tables + (5 + 2 * R) * K, min_ns, sizeof(long long) * 3 * K,
+                             cudaMemcpyHostToDevice));
+  else
+    RRFP_CUDA_TRY(cudaMemset(rt->tables + (5 + 2 * R) * K, 0, sizeof(long long) * 3 * K));
   if (fixed && rt->d.per_stage > 0)
     RRFP_CUDA_TRY(cudaMemcpy(rt->fixed, fixed, sizeof(rrfp_task_t) * rt->d.per_stage,
                              cudaMemcpyHostToDevice));

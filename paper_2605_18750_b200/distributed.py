@@ -78,7 +78,7 @@ class DistPipeline:
     """This rank's stage of a PP=world pipeline (one stage per GPU)."""
 
     def __init__(self, cfg, n_mb: int, *, hint="bf", buffer_limit=32, mode="free", jitter=None,
-                 seed=0, model_seed=1234, data_seed=0, schedule=None, group=None):
+                 seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None):
         import torch.distributed as dist
         from .arbitration import HintOrder
         from .model import StageCompute
@@ -100,7 +100,12 @@ class DistPipeline:
                                   decompose=decompose, seed=model_seed, data_seed=data_seed,
                                   fwd_in=fwd_in, bwd_in=bwd_in)
         w = nominal_workload(cfg, n, n_mb, decompose)
+        if comm_delay is not None:
+            from .workload import Workload
+            w = Workload(num_stages=n, num_microbatches=n_mb, num_chunks=1, tp_group_size=1,
+                         latency=w.latency, comm_delay=comm_delay, decompose_backward=decompose)
         self.workload = w
+        self.n_mb = n_mb
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
                                placement=[[self.device] for _ in range(n)], local=[(s, 0)],
                                bodies=None, compute_kind=1, schedule=schedule, defer_bodies=True)
@@ -127,6 +132,24 @@ class DistPipeline:
         # every rank instantiates + uploads its lane graph before ANY rank launches
         self.group.prepare()
         dist.barrier(group=group)
+
+    def set_lognormal_jitter(self, sigma: float, seed: int = 0, nominal_us=None, group=None):
+        """Lognormal compute jitter floors for THIS rank's stage; nominal task
+        times are gathered from every rank's last iteration."""
+        import torch.distributed as dist
+        from .pipeline import lognormal_floor_tables
+        if nominal_us is None:
+            ev, _ = self.last_events
+            mine = {}
+            for d, code in (("F", 1), ("B", 0), ("W", 2)):
+                xs = [e.t1 - e.t0 for e in ev if e.kind == 0 and (e.task & 3) == code]
+                mine[d] = (sum(xs) / len(xs) / 1000.0) if xs else 0.0
+            allv = [None] * self.world
+            dist.all_gather_object(allv, mine, group=group)
+            nominal_us = allv
+        self.nominal_us = nominal_us
+        floors = lognormal_floor_tables(self.world, self.n_mb, nominal_us, sigma, seed, stages=[self.rank])
+        self.group.set_floor_us(floors)
 
     def kernel_launches_per_step(self):
         return sum(self.stage.kernel_counts.values()) + 2 * len(self.stage.kernel_counts) + 2

@@ -44,6 +44,43 @@ def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
                     latency=lat, decompose_backward=decompose)
 
 
+def lognormal_floor_tables(n_stages, n_mb, nominal_us, sigma, seed, stages=None):
+    """Per-task duration floors (µs) for injected lognormal compute jitter
+    (SURVEY.md 8d, config 5): X ~ LogNormal(0, sigma) drawn on the host per
+    (stage, mb, direction) from the (seed, "cjitter", ...) stream; the device
+    pads the task until start + nominal * X.  W shares B's draw so a
+    decomposed (BFW) and a fused (1F1B / BF) backward see the same
+    perturbation.  Returns {stage: float64[3, KEYS]} (dir rows B=0, F=1, W=2).
+    """
+    import numpy as np
+    from .rng import substream
+    keys = ((n_mb + 31) // 32) * 32
+    out = {}
+    for s in (stages if stages is not None else range(n_stages)):
+        t = np.zeros((3, keys))
+        if sigma > 0:
+            for mb in range(n_mb):
+                for d, row in (("F", 1), ("B", 0)):
+                    x = float(np.exp(substream(seed, "cjitter", s, mb, d).normal(0.0, sigma)))
+                    t[row, mb] = nominal_us[s][d] * x
+                    if d == "B" and nominal_us[s].get("W"):
+                        t[2, mb] = nominal_us[s]["W"] * x
+        out[s] = t
+    return out
+
+
+def measured_nominal(trace, n_stages):
+    """Mean per-stage task durations (µs) by direction from a wall trace."""
+    out = []
+    for s in range(n_stages):
+        row = {}
+        for d in ("F", "B", "W"):
+            xs = [e.t_end - e.t_start for e in trace.execs() if e.stage == s and e.direction == d]
+            row[d] = sum(xs) / len(xs) if xs else 0.0
+        out.append(row)
+    return out
+
+
 class GpuPipeline:
     def __init__(self, cfg: GPTConfig, n_stages: int, n_mb: int, *, hint="bf", buffer_limit=32,
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
@@ -97,6 +134,16 @@ class GpuPipeline:
         events, t0s = self.group.wait(watchdog_secs)
         self.last_events = (events, min(t0s))
         return events
+
+    def set_lognormal_jitter(self, sigma: float, seed: int = 0, nominal_us=None):
+        """Enable injected lognormal compute jitter; nominal task times default
+        to the last iteration's measured means (call after a clean step)."""
+        if nominal_us is None:
+            tr, _ = self.trace()
+            nominal_us = measured_nominal(tr, self.N)
+        self.nominal_us = nominal_us
+        floors = lognormal_floor_tables(self.N, self.M, nominal_us, sigma, seed)
+        self.group.set_floor_us(floors)
 
     def kernel_launches_per_step(self):
         """Our kernels launched per iteration: every task body (captured counts)

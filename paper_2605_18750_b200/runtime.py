@@ -65,7 +65,8 @@ class LaneGroup:
                  time_scale: float = 1.0, *, seed: int = 0, jitter: JitterConfig | None = None,
                  tp: TpGroup | None = None, mode: str = "free", schedule: FixedSchedule | None = None,
                  placement=None, local=None, bodies=None, compute_kind: int = 0,
-                 trace_cap: int | None = None, pad_table_us=None, defer_bodies: bool = False):
+                 trace_cap: int | None = None, pad_table_us=None, defer_bodies: bool = False,
+                 floor_table_us=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("run_gpu needs a CUDA device (B200)")
@@ -98,6 +99,7 @@ class LaneGroup:
         self.L = _lib.lib()
         self.lanes = {}
         self.streams = {}
+        self._tables = {}
         for (s, k) in self.local:
             d = _lib.LaneDesc()
             d.N, d.M, d.C, d.R, d.MW = n, workload.num_microbatches, workload.num_chunks, r, mw
@@ -140,8 +142,14 @@ class LaneGroup:
             if order is not None:
                 fixed[:] = [_lib.task_code(t.direction, t.stage, t.microbatch, t.chunk)
                             for t in order[s]]
+            floor = None
+            if floor_table_us is not None:
+                floor = np.ascontiguousarray(np.rint(np.asarray(floor_table_us[s], np.float64)
+                                                     * 1000.0 * time_scale).astype(np.int64))
+            self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
-                                                      _ptr(fixed)))
+                                                      _ptr(fixed), _ptr(floor) if floor is not None
+                                                      else None))
             if bodies is not None:
                 arr = bodies[(s, k)]          # 3*M raw cudaGraph_t handles (kind*M + mb)
                 carr = (C.c_void_p * len(arr))(*[C.c_void_p(x or 0) for x in arr])
@@ -150,6 +158,17 @@ class LaneGroup:
         self.epoch = 0
         if len(self.local) == n * r and not defer_bodies:
             self.connect_local()
+
+    def set_floor_us(self, floor_by_stage):
+        """Replace the lognormal-jitter floor tables (µs, [3, KEYS] per stage)
+        between iterations."""
+        for (s, k), h in self.lanes.items():
+            dur, comm, dskew, fixed, _ = self._tables[(s, k)]
+            floor = np.ascontiguousarray(np.rint(np.asarray(floor_by_stage[s], np.float64)
+                                                 * 1000.0 * self.scale).astype(np.int64))
+            self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
+            _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
+                                                      _ptr(fixed), _ptr(floor)))
 
     def set_bodies(self, bodies: dict):
         for lane, arr in bodies.items():
