@@ -103,21 +103,29 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
   const float mean = mean_in[row], rstd = rstd_in[row];
   const __nv_bfloat16* xr = x + (size_t)row * D;
   const __nv_bfloat16* dr = dy + (size_t)row * D;
-  float xh[NV][8], dh[NV][8];
+  // the row stays in registers as packed bf16 (2 x NV x 16 B); all loads issued up front
+  uint4 xq[NV], dq[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 8;
+    xq[i] = *reinterpret_cast<const uint4*>(xr + c);
+    dq[i] = *reinterpret_cast<const uint4*>(dr + c);
+  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = (i * 32 + lane) * 8;
-    float xv[8], dv[8], gv[8];
-    load8(xr + c, xv);
-    load8(dr + c, dv);
+    float gv[8];
     load8(g + c, gv);
+    const __nv_bfloat162* xh2 = reinterpret_cast<const __nv_bfloat162*>(&xq[i]);
+    const __nv_bfloat162* dh2 = reinterpret_cast<const __nv_bfloat162*>(&dq[i]);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      xh[i][j] = (xv[j] - mean) * rstd;
-      dh[i][j] = dv[j] * gv[j];
-      s1 += dh[i][j] * xh[i][j];
-      s2 += dh[i][j];
+    for (int j = 0; j < 4; ++j) {
+      const float2 xv = __bfloat1622float2(xh2[j]), dv = __bfloat1622float2(dh2[j]);
+      const float xa = (xv.x - mean) * rstd, xb = (xv.y - mean) * rstd;
+      const float da = dv.x * gv[2 * j], db = dv.y * gv[2 * j + 1];
+      s1 += da * xa + db * xb;
+      s2 += da + db;
     }
   }
   s1 = warp_sum(s1) * (1.f / D);
@@ -125,10 +133,18 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = (i * 32 + lane) * 8;
-    float o[8], rv[8];
+    float gv[8], o[8], rv[8];
+    load8(g + c, gv);
     if (dres) load8(dres + (size_t)row * D + c, rv);
+    const __nv_bfloat162* xh2 = reinterpret_cast<const __nv_bfloat162*>(&xq[i]);
+    const __nv_bfloat162* dh2 = reinterpret_cast<const __nv_bfloat162*>(&dq[i]);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = rstd * (dh[i][j] - xh[i][j] * s1 - s2) + (dres ? rv[j] : 0.f);
+    for (int j = 0; j < 4; ++j) {
+      const float2 xv = __bfloat1622float2(xh2[j]), dv = __bfloat1622float2(dh2[j]);
+      const float xa = (xv.x - mean) * rstd, xb = (xv.y - mean) * rstd;
+      o[2 * j] = rstd * (dv.x * gv[2 * j] - xa * s1 - s2) + (dres ? rv[2 * j] : 0.f);
+      o[2 * j + 1] = rstd * (dv.y * gv[2 * j + 1] - xb * s1 - s2) + (dres ? rv[2 * j + 1] : 0.f);
+    }
     store8(dx + (size_t)row * D + c, o);
   }
 }
