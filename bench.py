@@ -164,9 +164,9 @@ def workload_config(args, n):
 
 
 # ------------------------------------------------------------------ our arm
-def gemm_roofline(cfg, peak_tf):
-    """Time the dominant kernel (the stage GEMMs) with CUDA events on its own
-    launch stream, shapes and epilogues exactly as one layer's F/B/W issue them."""
+def roofline_gemm_calls(cfg):
+    """One layer's ten F/B/W GEMMs, shapes and epilogues exactly as the stage
+    bodies issue them: [(fn, flops), ...] (also used by tools/prof_gemm.py)."""
     import torch
     from paper_2605_18750_b200 import kernels as K
     S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
@@ -179,7 +179,7 @@ def gemm_roofline(cfg, peak_tf):
     qkv, y, pre, act = (torch.empty(S, 3 * D, device=dev, dtype=bf), torch.empty(S, D, device=dev, dtype=bf),
                         torch.empty(S, Fd, device=dev, dtype=bf), torch.empty(S, Fd, device=dev, dtype=bf))
     gq, g1, g2 = torch.zeros(3 * D, D, device=dev), torch.zeros(Fd, D, device=dev), torch.zeros(D, Fd, device=dev)
-    calls = [
+    return [
         (lambda: K.gemm(x, w_qkv, qkv, bias=bias[:3 * D]), 2 * S * D * 3 * D),
         (lambda: K.gemm(x, w_o, y, epi=K.EPI_RESID, bias=bias[:D], r=x), 2 * S * D * D),
         (lambda: K.gemm(x, w_1, pre, epi=K.EPI_BIAS_GELU, c2=act, bias=bias), 2 * S * D * Fd),
@@ -191,6 +191,13 @@ def gemm_roofline(cfg, peak_tf):
         (lambda: K.gemm(pre, x, g1, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * Fd),
         (lambda: K.gemm(qkv, x, gq, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * 3 * D),
     ]
+
+
+def gemm_roofline(cfg, peak_tf):
+    """Time the dominant kernel (the stage GEMMs) with CUDA events on its own
+    launch stream, shapes and epilogues exactly as one layer's F/B/W issue them."""
+    import torch
+    calls = roofline_gemm_calls(cfg)
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for fn, _ in calls:
