@@ -214,8 +214,15 @@ def gemm_roofline(cfg, peak_tf):
     ms = e0.elapsed_time(e1) / (reps * len(calls))
     flops = sum(f for _, f in calls) / len(calls)
     achieved = flops / (ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f)["traffic_bytes_per_launch_mean"]
+    except Exception:
+        pass
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": round(achieved / peak_tf, 3), "traffic": None,
+            "frac": round(achieved / peak_tf, 3), "traffic": traffic,
+            "traffic_unit": "bytes/launch (dram rd+wr, ncu --set full, profiles/gemm_traffic.json)",
             "kernel": "gemm_bf16_sm100 (tcgen05.mma 128x256x16, TMA 4-stage, TMEM x2)",
             "per_launch": "mean over one layer's 10 F/B/W GEMMs (2048 tokens, d=2048, ffn=8192)",
             "avg_launch_us": round(ms * 1e3, 1)}

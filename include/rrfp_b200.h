@@ -231,6 +231,8 @@ int rrfp_gemm_set_variant(int pair);
 /* Programmatic dependent launch for the stage kernels (default on; env RRFP_PDL=0 disables). */
 int rrfp_set_pdl(int on);
 int rrfp_gemm_reserve_sms(int n);
+/* 1 = smem-staged TMA store / reduce-add epilogue (default), 0 = per-thread global stores. */
+int rrfp_gemm_set_epilogue(int tma_store);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                        int rows, int D, float eps, void* stream);

@@ -57,6 +57,7 @@ struct GemmArgs {
   int accumulate;
   int vec;   // 1 when C/C2/R rows are 16-byte aligned (vector epilogue path allowed)
   int vec_bias;
+  int tma_st;  // 1: pair-kernel epilogue stages tiles in smem and stores / reduce-adds them with TMA
 };
 
 // MUFU.TANH (rel. error ~2^-11, far below the bf16 output rounding)
@@ -92,6 +93,82 @@ __device__ __forceinline__ void epilogue_prefetch(const GemmArgs& g, int row, in
   const char* p = reinterpret_cast<const char*>(g.R + (size_t)row * g.ldr + col0);
   const int bytes = min(ncols, g.N - col0) * 2;
   for (int b = 0; b < bytes; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+}
+
+// Fused epilogue math on one 32-column chunk of a row, in registers: bias,
+// residual add or GELU' (the f32 epilogues and GELU itself are applied by the
+// caller).  Loops have compile-time trip counts with predicated tails.
+template <int EPI>
+__device__ __forceinline__ void epi_apply(const GemmArgs& g, int row, int col0, float (&v)[32]) {
+  if (EPI == EPI_ACC_F32 || EPI == EPI_F32) return;
+  if (row >= g.M || col0 >= g.N) return;
+  const bool full = g.vec && col0 + 32 <= g.N;
+  const int nvalid = g.N - col0;
+  if (g.bias && EPI != EPI_GELU_BWD) {
+    if (full && g.vec_bias) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(g.bias + col0 + j));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float2 f = __bfloat1622float2(h[t]);
+          v[j + 2 * t] += f.x;
+          v[j + 2 * t + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) v[j] += __bfloat162float(g.bias[col0 + j]);
+    }
+  }
+  if (EPI == EPI_RESID || EPI == EPI_GELU_BWD) {
+    const __nv_bfloat16* rp = g.R + (size_t)row * g.ldr + col0;
+    if (full) {
+      uint4 q[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[j] = *reinterpret_cast<const uint4*>(rp + 8 * j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 x = __bfloat1622float2(h[t]);
+          if (EPI == EPI_RESID) {
+            v[8 * j + 2 * t] += x.x;
+            v[8 * j + 2 * t + 1] += x.y;
+          } else {
+            v[8 * j + 2 * t] *= gelu_tanh_grad(x.x);
+            v[8 * j + 2 * t + 1] *= gelu_tanh_grad(x.y);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < nvalid) {
+          const float x = __bfloat162float(rp[j]);
+          if (EPI == EPI_RESID) v[j] += x;
+          else v[j] *= gelu_tanh_grad(x);
+        }
+      }
+    }
+  }
+}
+
+// Write one 128-byte row segment (8 x 16 B) of a SWIZZLE_128B staging box:
+// chunk j of row `lane` lands at chunk position j ^ (lane % 8), so the 32
+// lanes of a warp (32 rows) hit all 32 banks every 8 rows (4 wavefronts / store).
+__device__ __forceinline__ void stage_row_sw128(uint8_t* box, int lane, const uint32_t (&w)[32]) {
+  uint8_t* rowp = box + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t a = sm100::smem_u32(rowp + ((j ^ (lane & 7)) << 4));
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[4 * j]), "r"(w[4 * j + 1]),
+                 "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
+                 : "memory");
+  }
 }
 
 // All loops below have compile-time trip counts (tails are predicated), so the
@@ -346,18 +423,21 @@ __global__ void __launch_bounds__(256, 1)
 constexpr int P_BM = 256, P_BN = 256, P_STAGES = 6;
 constexpr int P_A_BYTES = 128 * BK * 2;      // this CTA's 128 rows of A
 constexpr int P_B_BYTES = 128 * BK * 2;      // this CTA's 128 rows (N/2) of B
-constexpr int P_SMEM_BYTES = P_STAGES * (P_A_BYTES + P_B_BYTES) + 1024 + 256;
+constexpr int P_EPI_BYTES = 4 * 2 * 4096;     // per epilogue warp: two 32-row x 128-byte staging boxes
+constexpr int P_SMEM_BYTES = P_STAGES * (P_A_BYTES + P_B_BYTES) + P_EPI_BYTES + 1024 + 256;
 constexpr int P_TMEM_COLS = 2 * P_BN;
 
 template <int EPI, int A_MN, int B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_sm100_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                          GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_B_BYTES);
+  uint8_t* sEpi = sB + P_STAGES * P_B_BYTES;   // 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + P_EPI_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + P_STAGES;
   uint64_t* tfull = bars + 2 * P_STAGES;
@@ -450,27 +530,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const uint32_t lead_tempty0 = sm100::mapa_shared(sm100::smem_u32(&tempty[0]), 0);
+    uint8_t* wbuf = sEpi + ew * 8192;     // this warp's two staging boxes
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t unit = 0;                    // staging-box round robin
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
-      const int row = mb * P_BM + rank * 128 + ew * 32 + lane;
+      const int row0 = mb * P_BM + rank * 128 + ew * 32;
+      const int row = row0 + lane;
       epilogue_prefetch<EPI>(g, row, nb * P_BN, P_BN);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * P_BN;
+      if (!g.tma_st) {
 #pragma unroll 1
-      for (int c = 0; c < P_BN; c += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld32(t_row + c, r);
-        sm100::tmem_ld_wait();
-        if (nb * P_BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * P_BN + c, r);
+        for (int c = 0; c < P_BN; c += 32) {
+          uint32_t r[32];
+          sm100::tmem_ld32(t_row + c, r);
+          sm100::tmem_ld_wait();
+          if (nb * P_BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * P_BN + c, r);
+        }
+      } else if (EPI == EPI_ACC_F32 || EPI == EPI_F32) {
+        // 32 f32 columns per box: TMA reduce-add (weight-gradient accumulate) or store
+#pragma unroll 1
+        for (int c = 0; c < P_BN; c += 32) {
+          const int col = nb * P_BN + c;
+          if (col >= g.N) break;
+          uint32_t r[32];
+          sm100::tmem_ld32(t_row + c, r);
+          uint8_t* box = wbuf + (unit & 1) * 4096;
+          if (lane == 0) sm100::bulk_wait_read<1>();
+          __syncwarp();
+          sm100::tmem_ld_wait();
+          stage_row_sw128(box, lane, r);
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (EPI == EPI_ACC_F32 && g.accumulate) sm100::tma_reduce_add_2d(&tmC, box, col, row0);
+            else sm100::tma_store_2d(&tmC, box, col, row0);
+            sm100::bulk_commit();
+          }
+          ++unit;
+        }
+      } else {
+        // 64 bf16 columns per box (two TMEM chunks); GELU also stages gelu(C) for C2
+#pragma unroll 1
+        for (int c = 0; c < P_BN; c += 64) {
+          const int col = nb * P_BN + c;
+          if (col >= g.N) break;
+          uint32_t w[32];
+          uint32_t w2[32];   // gelu(C) (EPI_BIAS_GELU only; dead otherwise)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[32];
+            sm100::tmem_ld32(t_row + c + 32 * h, r);
+            sm100::tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            epi_apply<EPI>(g, row, col + 32 * h, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              w[16 * h + j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+              if (EPI == EPI_BIAS_GELU) w2[16 * h + j] = pack_bf16(gelu_tanh(v[2 * j]), gelu_tanh(v[2 * j + 1]));
+            }
+          }
+          uint8_t* box = wbuf + (EPI == EPI_BIAS_GELU ? 0 : (unit & 1) * 4096);
+          if (lane == 0) {
+            if (EPI == EPI_BIAS_GELU) sm100::bulk_wait_read<0>();
+            else sm100::bulk_wait_read<1>();
+          }
+          __syncwarp();
+          stage_row_sw128(box, lane, w);
+          if (EPI == EPI_BIAS_GELU) stage_row_sw128(wbuf + 4096, lane, w2);
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tmC, box, col, row0);
+            if (EPI == EPI_BIAS_GELU) sm100::tma_store_2d(&tmC2, wbuf + 4096, col, row0);
+            sm100::bulk_commit();
+          }
+          ++unit;
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive_cluster(lead_tempty0 + acc * 8);
+      if (lane == 0) sm100::mbar_arrive_remote(lead_tempty0 + acc * 8);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) sm100::bulk_wait<0>();
   }
   sm100::tc_fence_before();
   sm100::cluster_sync();
@@ -501,14 +649,15 @@ encode_fn_t get_encode() {
 // 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading dim ld
 // (elements); box = {box_cols, box_rows}, 128-byte swizzle.
 int make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld,
-             int box_cols, int box_rows) {
+             int box_cols, int box_rows, bool f32 = false) {
   encode_fn_t enc = get_encode();
   if (!enc) return rrfp_fail(RRFP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -521,6 +670,16 @@ int g_num_sms = 0;
 int g_reserve_sms = 0;
 int g_pair = -1;   // 1: use the CTA-pair kernel (env RRFP_GEMM_PAIR, default on)
 
+int g_tma_store = -1;   // 1: TMA-store epilogue (env RRFP_GEMM_TMA_STORE, default on)
+
+bool use_tma_store() {
+  if (g_tma_store < 0) {
+    const char* e = getenv("RRFP_GEMM_TMA_STORE");
+    g_tma_store = e ? atoi(e) : 1;
+  }
+  return g_tma_store != 0;
+}
+
 bool use_pair() {
   if (g_pair < 0) {
     const char* e = getenv("RRFP_GEMM_PAIR");
@@ -530,7 +689,8 @@ bool use_pair() {
 }
 
 template <int EPI, int A_MN, int B_MN>
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs g, cudaStream_t st) {
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                GemmArgs g, cudaStream_t st) {
   auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN>;
   static bool attr = false;
   if (!attr) {
@@ -543,7 +703,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs g, cudaSt
   int pairs = (g_num_sms - g_reserve_sms) / 2;
   if (pairs < 1) pairs = 1;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
-  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, g));
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, g));
   return RRFP_OK;
 }
 
@@ -564,18 +724,18 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
 }
 
 template <int EPI>
-int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
-                    const GemmArgs& g, cudaStream_t st) {
+int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                    const CUtensorMap& tc2, const GemmArgs& g, cudaStream_t st) {
   if (!g_num_sms) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   if (use_pair()) {
-    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0>(ta, tb, g, st);
-    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1>(ta, tb, g, st);
-    if (a_mn && b_mn) return launch_pair<EPI, 1, 1>(ta, tb, g, st);
-    return launch_pair<EPI, 1, 0>(ta, tb, g, st);
+    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0>(ta, tb, tc, tc2, g, st);
+    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1>(ta, tb, tc, tc2, g, st);
+    if (a_mn && b_mn) return launch_pair<EPI, 1, 1>(ta, tb, tc, tc2, g, st);
+    return launch_pair<EPI, 1, 0>(ta, tb, tc, tc2, g, st);
   }
   if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
   if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
@@ -615,14 +775,25 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
           (!C2 || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
           (!R || (((uintptr_t)R % 16 == 0) && (ldr * 2) % 16 == 0));
   g.vec_bias = ((uintptr_t)bias % 16) == 0;
+  // TMA-store epilogue (pair kernel): C (and C2) must be valid TMA globals
+  CUtensorMap tc, tc2;
+  memset(&tc, 0, sizeof(tc));
+  memset(&tc2, 0, sizeof(tc2));
+  g.tma_st = 0;
+  if (use_pair() && use_tma_store() && g.vec) {
+    const bool f32 = (epi == EPI_ACC_F32 || epi == EPI_F32);
+    bool ok = make_map(&tc, C, M, N, ldc, f32 ? 32 : 64, 32, f32) == RRFP_OK;
+    if (ok && epi == EPI_BIAS_GELU) ok = make_map(&tc2, C2, M, N, ldc2, 64, 32) == RRFP_OK;
+    g.tma_st = ok ? 1 : 0;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
-    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, g, st);
-    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, g, st);
-    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, g, st);
-    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, g, st);
-    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, g, st);
-    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, g, st);
+    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
   }
   return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
 }
@@ -630,6 +801,12 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
 // 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel
 extern "C" int rrfp_gemm_set_variant(int pair) {
   g_pair = pair ? 1 : 0;
+  return RRFP_OK;
+}
+
+// 1 = smem-staged TMA store / reduce-add epilogue, 0 = per-thread global stores
+extern "C" int rrfp_gemm_set_epilogue(int tma_store) {
+  g_tma_store = tma_store ? 1 : 0;
   return RRFP_OK;
 }
 

@@ -5,12 +5,16 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[1, 0], ids=["pair", "single"], autouse=True)
+@pytest.fixture(params=[(1, 1), (1, 0), (0, 0)], ids=["pair-tma-store", "pair-st-global", "single"],
+                autouse=True)
 def variant(request):
     from paper_2605_18750_b200 import _lib
-    _lib.lib().rrfp_gemm_set_variant(request.param)
+    pair, tma = request.param
+    _lib.lib().rrfp_gemm_set_variant(pair)
+    _lib.lib().rrfp_gemm_set_epilogue(tma)
     yield request.param
     _lib.lib().rrfp_gemm_set_variant(1)
+    _lib.lib().rrfp_gemm_set_epilogue(1)
 
 
 def _rand(*shape, scale=1.0):
@@ -24,7 +28,8 @@ def _close(got, want, tol=2e-2):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (2048, 6144, 2048),
-                                   (384, 300, 192), (200, 256, 128), (2048, 50304, 2048)])
+                                   (384, 300, 192), (200, 256, 128), (200, 320, 128),
+                                   (2048, 50304, 2048)])
 def test_gemm_forward_kk(M, N, K):
     from paper_2605_18750_b200 import kernels as Kn
     torch.manual_seed(0)
@@ -47,7 +52,7 @@ def test_gemm_dgrad_kmn(M, N, K):
     _close(c, dy.float() @ w.float())
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (6144, 2048, 2048)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (200, 320, 128), (6144, 2048, 2048)])
 def test_gemm_wgrad_mnmn_accumulate(M, N, K):
     from paper_2605_18750_b200 import kernels as Kn
     torch.manual_seed(2)
@@ -80,3 +85,35 @@ def test_gemm_fused_epilogues():
     t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
     g = 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
     _close(gb, (a.float() @ b.float().t()) * g)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (200, 320, 64)])
+def test_gemm_f32_store(M, N, K):
+    """EPI_F32 and EPI_ACC_F32 with accumulate=0 overwrite C (no reduction)."""
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(4)
+    a, b = _rand(M, K), _rand(N, K)
+    want = a.float() @ b.float().t()
+    for epi in (Kn.EPI_F32, Kn.EPI_ACC_F32):
+        c = torch.full((M, N), 7.0, device="cuda")
+        Kn.gemm(a, b, c, epi=epi, accumulate=False)
+        torch.cuda.synchronize()
+        _close(c, want, 1e-2)
+
+
+def test_gemm_fused_epilogues_tails():
+    """Row and column tails (M=200, N=320: a partial 256x256 pair tile) for every bf16 epilogue."""
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(5)
+    M, N, K = 200, 320, 192
+    a, b, bias, res = _rand(M, K), _rand(N, K), _rand(N), _rand(M, N)
+    ref = a.float() @ b.float().t() + bias.float()
+    pre = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    act = torch.zeros_like(pre)
+    Kn.gemm(a, b, pre, epi=Kn.EPI_BIAS_GELU, c2=act, bias=bias)
+    out = torch.zeros_like(pre)
+    Kn.gemm(a, b, out, epi=Kn.EPI_RESID, bias=bias, r=res)
+    torch.cuda.synchronize()
+    _close(pre, ref)
+    _close(act, torch.nn.functional.gelu(ref, approximate="tanh"))
+    _close(out, ref + res.float())

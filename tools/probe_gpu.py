@@ -38,7 +38,8 @@ try:
 except Exception as ex:
     print("flash_attn FAILED", type(ex).__name__, str(ex)[:200], flush=True)
 
-from paper_2605_18750_b200 import kernels as Kn
+from paper_2605_18750_b200 import kernels as Kn, _lib
+_lib.lib().rrfp_gemm_set_epilogue(int(os.environ.get("RRFP_GEMM_TMA_STORE", "1")))
 for (M, N, K, am, bm, name) in [(2048, 6144, 2048, 0, 0, "qkv fwd"), (2048, 8192, 2048, 0, 0, "fc1 fwd"),
                                 (2048, 2048, 8192, 0, 0, "fc2 fwd"), (2048, 2048, 2048, 0, 0, "proj fwd"),
                                 (2048, 2048, 8192, 0, 1, "fc1 dgrad"), (8192, 2048, 2048, 1, 1, "fc1 wgrad"),
