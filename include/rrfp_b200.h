@@ -233,6 +233,8 @@ int rrfp_set_pdl(int on);
 int rrfp_gemm_reserve_sms(int n);
 /* 1 = smem-staged TMA store / reduce-add epilogue (default), 0 = per-thread global stores. */
 int rrfp_gemm_set_epilogue(int tma_store);
+/* 1 = stream-K split of the last partial round of 256x256 tiles over all CTA pairs (default 0). */
+int rrfp_gemm_set_streamk(int on);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                        int rows, int D, float eps, void* stream);

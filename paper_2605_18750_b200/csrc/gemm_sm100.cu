@@ -23,6 +23,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/rrfp_b200.h"
 #include "rrfp_common.h"
 #include "sm100_ptx.cuh"
@@ -58,7 +62,97 @@ struct GemmArgs {
   int vec;   // 1 when C/C2/R rows are 16-byte aligned (vector epilogue path allowed)
   int vec_bias;
   int tma_st;  // 1: pair-kernel epilogue stages tiles in smem and stores / reduce-adds them with TMA
+  // stream-K tail (pair kernel): tiles [0, sk_full) run data-parallel, one per
+  // cluster per round; the sk_W = (tiles - sk_full) * kblocks k-block iterations
+  // of the last, partial round are split evenly over all clusters.  A tile split
+  // between clusters is finished by its "owner" (the cluster holding its last
+  // k-block), which adds the other contributors' fp32 partials from `ws`
+  // (one 256 KB slot per cluster) after they signal `cnt`.  sk_W = 0: plain
+  // data-parallel persistent schedule.
+  int sk_full;
+  int sk_W;
+  float4* ws;
+  int* cnt;
 };
+
+enum Role : int { ROLE_FULL = 0, ROLE_OWNER = 1, ROLE_PARTIAL = 2 };
+
+struct Unit {
+  int tile, k0, k1, role;
+  int tail;        // tail-tile index (counter slot), owner / partial only
+  int first;       // owner: first contributing cluster (partials in slots first .. cluster-1)
+};
+
+__device__ __forceinline__ long long sk_start(const GemmArgs& g, int c, int C) {
+  return (long long)c * g.sk_W / C;
+}
+
+// The i-th work unit of cluster `cid` (of C).  Producer, MMA issuer and
+// epilogue all walk the same sequence.  Tail order: a cluster's range covers
+// at most two tiles (range < one tile); the partial segment of the second tile
+// is done FIRST, the owner segment of the first tile LAST, so a partial writer
+// never waits on anything and an owner waits only for segments other clusters
+// run first.
+__device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int kblocks, int cid, int C,
+                                         int i, bool direct, Unit& u) {
+  if (!g.sk_W) {
+    const int t = cid + i * C;
+    if (t >= num_tiles) return false;
+    u.tile = t; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+    return true;
+  }
+  const int n_dp = g.sk_full / C;
+  if (i < n_dp) {
+    u.tile = cid + i * C; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+    return true;
+  }
+  const int j = i - n_dp;
+  const long long s = sk_start(g, cid, C), e = sk_start(g, cid + 1, C);
+  if (s >= e) return false;
+  const int tA = (int)(s / kblocks);
+  const bool hasB = e > (long long)(tA + 1) * kblocks;
+  int t, k0, k1;
+  if (hasB && j == 0) {
+    t = tA + 1; k0 = 0; k1 = (int)(e - (long long)(tA + 1) * kblocks);
+  } else if (j == (hasB ? 1 : 0)) {
+    t = tA; k0 = (int)(s - (long long)tA * kblocks);
+    k1 = (int)min((long long)kblocks, e - (long long)tA * kblocks);
+  } else {
+    return false;
+  }
+  u.tile = g.sk_full + t; u.k0 = k0; u.k1 = k1; u.tail = t; u.first = cid;
+  if (direct || (k0 == 0 && k1 == kblocks)) {
+    u.role = ROLE_FULL;
+  } else if (k1 == kblocks) {
+    u.role = ROLE_OWNER;
+    const long long x = (long long)t * kblocks;   // the tile's first iteration
+    int c = (int)(x * C / g.sk_W);
+    while (c + 1 < C && sk_start(g, c + 1, C) <= x) ++c;
+    while (c > 0 && sk_start(g, c, C) > x) --c;
+    u.first = c;
+  } else {
+    u.role = ROLE_PARTIAL;
+  }
+  return true;
+}
+
+// fp32 partial accumulators: slot (cluster, cta rank) = 128 rows x 256 cols
+// laid out so that thread (warp ew, lane) of the writer and of the owner touch
+// the same float4s and every warp access is 512 contiguous bytes.
+__device__ __forceinline__ float4* ws_chunk(const GemmArgs& g, int slot, int rank, int c32, int ew, int lane) {
+  return g.ws + (size_t)(slot * 2 + rank) * 8192 + (size_t)((c32 * 4 + ew) * 8) * 32 + lane;
+}
+__device__ __forceinline__ void ws_add(const GemmArgs& g, const Unit& u, int cid, int rank, int c32, int ew,
+                                       int lane, float (&v)[32]) {
+  for (int p = u.first; p < cid; ++p) {
+    const float4* q = ws_chunk(g, p, rank, c32, ew, lane);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 a = __ldcg(q + j * 32);
+      v[4 * j] += a.x; v[4 * j + 1] += a.y; v[4 * j + 2] += a.z; v[4 * j + 3] += a.w;
+    }
+  }
+}
 
 // MUFU.TANH (rel. error ~2^-11, far below the bf16 output rounding)
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -465,16 +559,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int num_tiles = g.tiles_m * g.tiles_n;
   const int kblocks = (g.K + BK - 1) / BK;
   const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  // f32 accumulate: every split segment reduce-adds into C by itself (no fix-up)
+  const bool direct = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
 
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t lead_full0 = sm100::mapa_shared(sm100::smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+      Unit u;
+      for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
+        const int mb = u.tile % g.tiles_m, nb = u.tile / g.tiles_m;
         const int m0 = mb * P_BM + rank * 128, n0 = nb * P_BN + rank * 128;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = u.k0; kb < u.k1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2 * (P_A_BYTES + P_B_BYTES));
           const uint32_t bar = lead_full0 + stage * 8;
@@ -503,11 +600,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      Unit u;
+      for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * P_BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = u.k0; kb < u.k1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
           sm100::tc_fence_after();
           const uint32_t a_base = sm100::smem_u32(sA + stage * P_A_BYTES);
@@ -518,7 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                                : sm100::umma_desc_sw128(a_base + k * 32, 16, 1024);
             uint64_t bd = B_MN ? sm100::umma_desc_sw128(b_base + k * 16 * 128, 64 * BK * 2, 1024)
                                : sm100::umma_desc_sw128(b_base + k * 32, 16, 1024);
-            sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != u.k0) || (k != 0));
           }
           sm100::mma_commit_pair(&empty[stage], 0x3);
           if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
@@ -534,20 +632,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t unit = 0;                    // staging-box round robin
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+    Unit u;
+    for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
+      const int tile = u.tile;
       const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
       const int row0 = mb * P_BM + rank * 128 + ew * 32;
       const int row = row0 + lane;
-      epilogue_prefetch<EPI>(g, row, nb * P_BN, P_BN);
+      int* cnt = g.cnt ? g.cnt + u.tail * 8 + rank * 4 + ew : nullptr;
+      if (u.role != ROLE_PARTIAL) epilogue_prefetch<EPI>(g, row, nb * P_BN, P_BN);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * P_BN;
-      if (!g.tma_st) {
+      if (u.role == ROLE_OWNER) {
+        // wait until every other contributor's warp (same rank, same rows) published its partial
+        if (lane == 0) {
+          const int need = cluster_id - u.first;
+          int got;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(cnt) : "memory");
+          } while (got < need);
+        }
+        __syncwarp();
+      }
+      if (u.role == ROLE_PARTIAL) {
+        // raw fp32 partial -> this cluster's workspace slot (coalesced), then signal
 #pragma unroll 1
         for (int c = 0; c < P_BN; c += 32) {
           uint32_t r[32];
           sm100::tmem_ld32(t_row + c, r);
           sm100::tmem_ld_wait();
+          float4* q = ws_chunk(g, cluster_id, rank, c >> 5, ew, lane);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(q + j * 32, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                           __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
+      } else if (!g.tma_st) {
+#pragma unroll 1
+        for (int c = 0; c < P_BN; c += 32) {
+          uint32_t r[32];
+          sm100::tmem_ld32(t_row + c, r);
+          sm100::tmem_ld_wait();
+          if (u.role == ROLE_OWNER) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            ws_add(g, u, cluster_id, rank, c >> 5, ew, lane, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+          }
           if (nb * P_BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * P_BN + c, r);
         }
       } else if (EPI == EPI_ACC_F32 || EPI == EPI_F32) {
@@ -562,6 +698,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (lane == 0) sm100::bulk_wait_read<1>();
           __syncwarp();
           sm100::tmem_ld_wait();
+          if (u.role == ROLE_OWNER) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            ws_add(g, u, cluster_id, rank, c >> 5, ew, lane, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+          }
           stage_row_sw128(box, lane, r);
           sm100::fence_proxy_async_smem();
           __syncwarp();
@@ -588,6 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            if (u.role == ROLE_OWNER) ws_add(g, u, cluster_id, rank, (c >> 5) + h, ew, lane, v);
             epi_apply<EPI>(g, row, col + 32 * h, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -613,6 +758,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           ++unit;
         }
       }
+      if (u.role == ROLE_OWNER && lane == 0) *cnt = 0;   // ready for the next launch on this stream
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(lead_tempty0 + acc * 8);
@@ -688,6 +834,51 @@ bool use_pair() {
   return g_pair != 0;
 }
 
+// Stream-K workspace, one per (device, stream): kernels on one stream never
+// overlap (PDL dependents wait in griddepcontrol.wait before touching it), and
+// concurrent branches of a graph were captured from different streams.
+struct SkWorkspace {
+  float4* ws = nullptr;
+  int* cnt = nullptr;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_ws;
+// env RRFP_GEMM_STREAMK (default 0).  Measured on B200 (profiles/r01_gemm_ab.txt):
+// the 256x256 pair kernel is bound by L2->SM (TMA) throughput (~11 TB/s of operand
+// traffic at 1.8 GHz), not by wave quantization, so idle SMs in the last round cost
+// little and the fix-up traffic of the split costs more (-10% on one layer).
+int g_streamk = -1;
+
+bool use_streamk() {
+  if (g_streamk < 0) {
+    const char* e = getenv("RRFP_GEMM_STREAMK");
+    g_streamk = e ? atoi(e) : 0;
+  }
+  return g_streamk != 0;
+}
+
+// workspace for `st`, allocated on first (eager) use; never allocates while
+// the stream is being captured (returns null -> no stream-K fix-up then)
+SkWorkspace* sk_workspace(cudaStream_t st, int clusters) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto key = std::make_pair(dev, st);
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) return &it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  SkWorkspace w;
+  const size_t ws_bytes = (size_t)148 * 128 * 256 * 4;   // one 128x256 f32 slot per CTA (>= clusters * 2)
+  const size_t cnt_bytes = (size_t)148 * 8 * sizeof(int);
+  (void)clusters;
+  if (cudaMalloc(&w.ws, ws_bytes) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&w.cnt, cnt_bytes) != cudaSuccess) { cudaFree(w.ws); return nullptr; }
+  if (cudaMemset(w.cnt, 0, cnt_bytes) != cudaSuccess) return nullptr;
+  cudaDeviceSynchronize();
+  return &(g_ws[key] = w);
+}
+
 template <int EPI, int A_MN, int B_MN>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
                 GemmArgs g, cudaStream_t st) {
@@ -702,7 +893,20 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   int tiles = g.tiles_m * g.tiles_n;
   int pairs = (g_num_sms - g_reserve_sms) / 2;
   if (pairs < 1) pairs = 1;
+  const int kblocks = (g.K + BK - 1) / BK;
+  g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int tail = tiles % pairs;
+  if (use_streamk() && tail != 0 && (long long)tail * kblocks >= 2LL * pairs) {
+    const bool direct = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
+    SkWorkspace* w = direct ? nullptr : sk_workspace(st, pairs);
+    if (direct || w) {
+      g.sk_full = tiles - tail;
+      g.sk_W = tail * kblocks;
+      if (w) { g.ws = w->ws; g.cnt = w->cnt; }
+      grid = 2 * pairs;
+    }
+  }
   RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, g));
   return RRFP_OK;
 }
@@ -801,6 +1005,12 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
 // 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel
 extern "C" int rrfp_gemm_set_variant(int pair) {
   g_pair = pair ? 1 : 0;
+  return RRFP_OK;
+}
+
+// 1 = stream-K split of the last partial round of tiles, 0 = data-parallel only (default)
+extern "C" int rrfp_gemm_set_streamk(int on) {
+  g_streamk = on ? 1 : 0;
   return RRFP_OK;
 }
 

@@ -117,3 +117,50 @@ def test_gemm_fused_epilogues_tails():
     _close(pre, ref)
     _close(act, torch.nn.functional.gelu(ref, approximate="tanh"))
     _close(out, ref + res.float())
+
+
+@pytest.mark.parametrize("pairs", [3, 5, 7])
+def test_gemm_streamk_fixup_all_epilogues(pairs, variant):
+    """Few CTA pairs (SMs reserved) so the last partial round is split over
+    clusters with 2-3 contributors per tile: owner fix-up for every epilogue,
+    direct reduce-add for the f32 accumulate."""
+    from paper_2605_18750_b200 import kernels as Kn, _lib
+    if variant[0] == 0:
+        pytest.skip("stream-K is a pair-kernel schedule")
+    L = _lib.lib()
+    n_sms = torch.cuda.get_device_properties(0).multi_processor_count
+    L.rrfp_gemm_reserve_sms(n_sms - 2 * pairs)
+    L.rrfp_gemm_set_streamk(1)
+    try:
+        torch.manual_seed(6 + pairs)
+        M, N, K = 512, 1024, 960          # 8 tiles of 256x256, 15 k-blocks
+        a, b, bias, res = _rand(M, K), _rand(N, K), _rand(N), _rand(M, N)
+        ref = a.float() @ b.float().t()
+        for _ in range(2):                 # second launch reuses the (self-reset) counters
+            c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            Kn.gemm(a, b, c, bias=bias)
+            pre, act = torch.empty_like(c), torch.empty_like(c)
+            Kn.gemm(a, b, pre, epi=Kn.EPI_BIAS_GELU, c2=act, bias=bias)
+            out = torch.empty_like(c)
+            Kn.gemm(a, b, out, epi=Kn.EPI_RESID, bias=bias, r=res)
+            gb = torch.empty_like(c)
+            Kn.gemm(a, b, gb, epi=Kn.EPI_GELU_BWD, r=res)
+            f = torch.full((M, N), 3.0, device="cuda")
+            Kn.gemm(a, b, f, epi=Kn.EPI_F32)
+            acc = torch.randn(M, N, device="cuda")
+            want_acc = acc + ref
+            Kn.gemm(a, b, acc, epi=Kn.EPI_ACC_F32, accumulate=True)
+            torch.cuda.synchronize()
+            _close(c, ref + bias.float())
+            _close(pre, ref + bias.float())
+            _close(act, torch.nn.functional.gelu(ref + bias.float(), approximate="tanh"))
+            _close(out, ref + bias.float() + res.float())
+            x = res.float()
+            t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+            gg = 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+            _close(gb, ref * gg)
+            _close(f, ref, 1e-2)
+            _close(acc, want_acc, 1e-2)
+    finally:
+        L.rrfp_gemm_reserve_sms(0)
+        L.rrfp_gemm_set_streamk(0)

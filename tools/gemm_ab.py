@@ -13,7 +13,9 @@ names = ["qkv fwd", "proj fwd+R", "fc1 fwd gelu", "fc2 fwd+R", "fc2 dgrad gelu'"
          "fc2 wgrad f32+=", "fc1 wgrad f32+=", "qkv wgrad f32+="]
 calls = bench.roofline_gemm_calls(GPTConfig())
 L = _lib.lib()
-variants = [("tma-store", lambda: L.rrfp_gemm_set_epilogue(1)), ("st.global", lambda: L.rrfp_gemm_set_epilogue(0))]
+def setv(tma, sk):
+    return lambda: (L.rrfp_gemm_set_epilogue(tma), L.rrfp_gemm_set_streamk(sk))
+variants = [("tma+streamK", setv(1, 1)), ("tma, DP only", setv(1, 0)), ("st.global+streamK", setv(0, 1))]
 res = {}
 for vname, setv in variants:
     setv()
