@@ -306,7 +306,8 @@ class StageCompute:
         dec = self.decompose
         fused_w = not dec
         nl = len(self.layers)
-        main, side = torch.cuda.current_stream(), self.side
+        main = torch.cuda.current_stream()
+        side = self.side or main          # side=None: the whole task on one stream
         side_done = {}
 
         def ev():
@@ -315,6 +316,9 @@ class StageCompute:
             return e
 
         def on_side(after, fn):
+            if side == main:
+                fn()
+                return
             with torch.cuda.stream(side):
                 side.wait_event(after)
                 fn()
@@ -437,7 +441,8 @@ class StageCompute:
             return
         cfg = self.cfg
         S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
-        main, side = torch.cuda.current_stream(), self.side
+        main = torch.cuda.current_stream()
+        side = self.side or main
         fork = torch.cuda.Event()
         fork.record(main)
         side.wait_event(fork)
