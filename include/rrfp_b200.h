@@ -188,6 +188,26 @@ int rrfp_ipc_open(const void* handle64, void** dev_ptr);
 int rrfp_ipc_alloc(size_t bytes, void** dev_ptr);
 int rrfp_ipc_handle(void* dev_ptr, void* handle64);
 void rrfp_ipc_free(void* dev_ptr);
+
+/* ---- tensor-parallel group of one pipeline stage (csrc/tp.cu; BASELINE config 3) ----
+ * Replaces the reference's TP collective step that follows tp_coordinate
+ * (arbitration.py:323-334; live.py:246-277 resolves the group, the collective
+ * itself is the Megatron all-reduce the paper times).
+ * Each rank owns a partial buffer (row-parallel GEMM output) and a flag board;
+ * rrfp_tp_allreduce sums the R partials in rank order over peer memory, fuses
+ * bias + residual, and writes up to 4 destinations; replayable in CUDA graphs. */
+typedef struct rrfp_tp rrfp_tp;
+int rrfp_tp_create(int rank, int R, size_t part_bytes, rrfp_tp** out);
+/* own partial buffer and flag board (cudaMalloc'd: export with rrfp_ipc_handle) */
+int rrfp_tp_buffers(rrfp_tp* t, void** part, void** board);
+/* every rank's partial and board, indexed by TP rank (own included; peer pointers ok) */
+int rrfp_tp_connect(rrfp_tp* t, void* const* parts, void* const* boards);
+/* local_only: no rendezvous (out = own partial + bias + resid) -- eager warm-up */
+int rrfp_tp_allreduce(rrfp_tp* t, int rows, int cols, const void* bias, const void* resid,
+                      long long ld_resid, void* const* outs, int n_out, int local_only, void* stream);
+/* *err = 1 if a peer wait timed out (20 s) since creation */
+int rrfp_tp_error(rrfp_tp* t, int* err);
+void rrfp_tp_destroy(rrfp_tp* t);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */

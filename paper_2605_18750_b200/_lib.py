@@ -84,6 +84,8 @@ EXPORTS = [
     "rrfp_spin", "rrfp_last_error", "rrfp_abi_version", "rrfp_gemm_bf16", "rrfp_gemm_set_variant", "rrfp_set_pdl",
     "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_embedding_fwd",
     "rrfp_embedding_bwd", "rrfp_bias_grad", "rrfp_copy_rows", "rrfp_xent_fwd", "rrfp_xent_bwd",
+    "rrfp_tp_create", "rrfp_tp_buffers", "rrfp_tp_connect", "rrfp_tp_allreduce", "rrfp_tp_error",
+    "rrfp_tp_destroy",
 ]
 
 _lib = None
@@ -107,6 +109,7 @@ def lib():
         L.rrfp_replay_event_capacity.restype = C.c_int32
         L.rrfp_runtime_destroy.restype = None
         L.rrfp_ipc_free.restype = None
+        L.rrfp_tp_destroy.restype = None
         _lib = L
     return _lib
 

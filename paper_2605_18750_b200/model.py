@@ -96,6 +96,27 @@ def init_layer_params(cfg: GPTConfig, layer: int, device, seed: int):
     }
 
 
+def shard_layer_params(cfg: GPTConfig, p: dict, rank: int, size: int) -> dict:
+    """Megatron split of one layer over a TP group of `size` ranks: QKV and FC1
+    column-parallel (heads / FFN columns rank*1/size..), out-proj and FC2
+    row-parallel (their input features); LayerNorms and the row-parallel biases
+    b_o, b_2 replicated (added once, inside the all-reduce)."""
+    if size == 1:
+        return p
+    D, Fd = cfg.d_model, cfg.d_ff
+    dl, fl = D // size, Fd // size
+    q = slice(rank * dl, (rank + 1) * dl)
+    f = slice(rank * fl, (rank + 1) * fl)
+    out = dict(p)
+    out["w_qkv"] = torch.cat([p["w_qkv"][i * D:(i + 1) * D][q] for i in range(3)]).contiguous()
+    out["b_qkv"] = torch.cat([p["b_qkv"][i * D:(i + 1) * D][q] for i in range(3)]).contiguous()
+    out["w_o"] = p["w_o"][:, q].contiguous()
+    out["w_1"] = p["w_1"][f].contiguous()
+    out["b_1"] = p["b_1"][f].contiguous()
+    out["w_2"] = p["w_2"][:, f].contiguous()
+    return out
+
+
 def init_embed_params(cfg: GPTConfig, device, seed: int):
     g = _gen(device, seed * 100003 + 77777)
     bf = torch.bfloat16
@@ -135,6 +156,14 @@ def _ln_bwd(dy, x, mean, rstd, g, dres, dx, dg, db):
                                     x.shape[1], K._stream()))
 
 
+def _copy_rows(dst, src, rows, cols):
+    """bf16 [rows, cols] copy (e.g. into a peer stage's mailbox slot)."""
+    K.note()
+    _lib.check(_lib.lib().rrfp_copy_rows(
+        C.c_void_p(dst.data_ptr()), C.c_longlong(dst.stride(0) * 2), C.c_void_p(src.data_ptr()),
+        C.c_longlong(src.stride(0) * 2), rows, C.c_longlong(cols * 2), K._stream()))
+
+
 def _bias_grad(dy, db):
     K.note()
     _lib.check(_lib.lib().rrfp_bias_grad(K._p(dy), C.c_longlong(dy.stride(0)), K._p(db),
@@ -157,16 +186,26 @@ class RawBuffer:
 class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
                  decompose: bool = False, seed: int = 1234, data_seed: int = 0,
-                 fwd_in=None, bwd_in=None):
+                 fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
         self.first, self.last = stage == 0, stage == n_stages - 1
         self.decompose = decompose
         self.layers = split_layers(cfg.n_layer, n_stages, stage)
         S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
+        if cfg.n_head % tp_size or Fd % tp_size:
+            raise ValueError(f"TP size {tp_size} must divide n_head and d_ff")
+        if tp_size > 1 and tp is None:
+            raise ValueError("tp_size > 1 needs a TpComm (paper_2605_18750_b200.tp)")
+        # tensor parallelism (config 3): this rank's heads / FFN columns
+        self.tp_rank, self.R, self.tp = tp_rank, tp_size, tp
+        self.model_seed = seed
+        self.Hl, self.Dl, self.Fl = cfg.n_head // tp_size, D // tp_size, Fd // tp_size
+        Dl, Fl = self.Dl, self.Fl
         dev, bf = self.device, torch.bfloat16
         with torch.no_grad():
-            self.p = [init_layer_params(cfg, l, dev, seed) for l in self.layers]
+            self.p = [shard_layer_params(cfg, init_layer_params(cfg, l, dev, seed), tp_rank, tp_size)
+                      for l in self.layers]
             self.emb = init_embed_params(cfg, dev, seed) if self.first else None
             self.head = init_head_params(cfg, dev, seed) if self.last else None
         self.g = [{k: torch.zeros(v.shape, device=dev) for k, v in p.items()} for p in self.p]
@@ -190,9 +229,9 @@ class StageCompute:
         e = lambda *s: torch.empty(*s, device=dev, dtype=bf)
         f32 = lambda *s: torch.empty(*s, device=dev, dtype=torch.float32)
         self.x0 = e(n_mb, S, D) if self.first else None
-        self.h1, self.qkv, self.x2 = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D), e(n_mb, nl, S, D)
+        self.h1, self.qkv, self.x2 = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl), e(n_mb, nl, S, D)
         # (the attention output lives in cuDNN's BSHD output buffer, see _attn_fwd)
-        self.h2, self.pre, self.act, self.y = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd), e(n_mb, nl, S, Fd), e(n_mb, nl, S, D)
+        self.h2, self.pre, self.act, self.y = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl), e(n_mb, nl, S, Fl), e(n_mb, nl, S, D)
         self.m1, self.r1, self.m2, self.r2 = f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S)
         self.attn_aux = [[None] * nl for _ in range(n_mb)]
         self.o_view = [[None] * nl for _ in range(n_mb)]   # attention output as [S, D]
@@ -207,13 +246,14 @@ class StageCompute:
         # input-gradient chain proceeds on the main stream
         self.sd_a = [e(S, D), e(S, D)]
         self.sd_b = [e(S, D), e(S, D)]
-        self.sd_big = [e(S, Fd), e(S, Fd)]
-        self.sd_qkv = [e(S, 3 * D), e(S, 3 * D)]
+        self.sd_big = [e(S, Fl), e(S, Fl)]
+        self.sd_qkv = [e(S, 3 * Dl), e(S, 3 * Dl)]
         self.d_head = e(S, D)
+        self.d_o = e(S, Dl) if tp_size > 1 else None   # attention-output gradient (this rank's heads)
         self.side = torch.cuda.Stream(dev)
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
-            self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fd)
-            self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * D)
+            self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl)
+            self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl)
             if self.first:
                 self.gx0 = e(n_mb, S, D)
         self.graphs = {}
@@ -222,15 +262,19 @@ class StageCompute:
     # ------------------------------------------------------------ wiring
     def connect_outputs(self, fwd_out=None, bwd_out=None):
         """fwd_out / bwd_out: per-mb destination (tensor or RawBuffer) in the
-        next / previous stage's mailbox."""
-        self.fwd_out, self.bwd_out = fwd_out, bwd_out
+        next / previous stage's mailbox, or per-mb LISTS of destinations (one per
+        TP rank of the neighbour stage: every sender rank writes every receiver
+        rank's slot -- identical bytes -- before raising its flags)."""
+        as_list = lambda v: v if isinstance(v, (list, tuple)) else [v]
+        self.fwd_out = [as_list(v) for v in fwd_out] if fwd_out is not None else None
+        self.bwd_out = [as_list(v) for v in bwd_out] if bwd_out is not None else None
 
     def param_bytes(self):
         return sum(t.numel() * 2 for p in self.p for t in p.values())
 
     # ------------------------------------------------------------ forward
     def _attn_fwd(self, qkv, mb, li):
-        S, H, Dh, D = self.cfg.seq, self.cfg.n_head, self.cfg.d_head, self.cfg.d_model
+        S, H, Dh, D = self.cfg.seq, self.Hl, self.cfg.d_head, self.Dl
         q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
         k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
         v = qkv[:, 2 * D:].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
@@ -262,15 +306,23 @@ class StageCompute:
             _ln_fwd(x, p["ln1_g"], p["ln1_b"], self.h1[mb, li], self.m1[mb, li], self.r1[mb, li], cfg.eps)
             K.gemm(self.h1[mb, li], p["w_qkv"], self.qkv[mb, li], bias=p["b_qkv"])
             self._attn_fwd(self.qkv[mb, li], mb, li)
-            K.gemm(self.o_view[mb][li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
+            if self.R == 1:
+                K.gemm(self.o_view[mb][li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
+            else:   # row-parallel: partial sum, then all-reduce (+ b_o + residual) over the TP group
+                K.gemm(self.o_view[mb][li], p["w_o"], self.tp.partial, m=S, n=D, k=self.Dl)
+                self.tp.allreduce([self.x2[mb, li]], bias=p["b_o"], resid=x)
             _ln_fwd(self.x2[mb, li], p["ln2_g"], p["ln2_b"], self.h2[mb, li], self.m2[mb, li],
                     self.r2[mb, li], cfg.eps)
             K.gemm(self.h2[mb, li], p["w_1"], self.pre[mb, li], epi=K.EPI_BIAS_GELU,
                    c2=self.act[mb, li], bias=p["b_1"])
-            out = self._layer_output(mb, li)    # last layer: the next stage's mailbox slot
-            K.gemm(self.act[mb, li], p["w_2"], out, epi=K.EPI_RESID, bias=p["b_2"], r=self.x2[mb, li],
-                   m=S, n=D, k=cfg.d_ff)
-            x = out
+            outs = self._layer_output(mb, li)   # last layer: the next stage's mailbox slot(s)
+            if self.R == 1:
+                K.gemm(self.act[mb, li], p["w_2"], outs[0], epi=K.EPI_RESID, bias=p["b_2"],
+                       r=self.x2[mb, li], m=S, n=D, k=self.Fl)
+            else:
+                K.gemm(self.act[mb, li], p["w_2"], self.tp.partial, m=S, n=D, k=self.Fl)
+                self.tp.allreduce(outs, bias=p["b_2"], resid=self.x2[mb, li])
+            x = outs[0]
         if self.last:
             h = self.head
             _ln_fwd(x, h["lnf_g"], h["lnf_b"], self.hf[mb], self.mf[mb], self.rf[mb], cfg.eps)
@@ -286,9 +338,14 @@ class StageCompute:
         return self.x0[mb] if self.first else self.fwd_in[mb]
 
     def _layer_output(self, mb, li):
+        """Destination list of layer li's output (the next stage's mailbox slot of
+        every receiving TP rank for the last layer; first entry is read back)."""
         if li == len(self.layers) - 1 and not self.last and self.fwd_out is not None:
-            return self.fwd_out[mb]
-        return self.y[mb, li]
+            outs = list(self.fwd_out[mb])
+            if len(outs) > 1 and self.R == 1:
+                raise ValueError("a TP=1 stage feeds a TP>1 stage: not supported")
+            return outs
+        return [self.y[mb, li]]
 
     # ----------------------------------------------------------- backward
     def backward_input(self, mb: int):
@@ -345,6 +402,7 @@ class StageCompute:
             if dec:
                 self.gy[mb, nl - 1].copy_(dy)
                 dy = self.gy[mb, nl - 1]
+        S_, Dl, Fl = S, self.Dl, self.Fl
         for li in reversed(range(nl)):
             p, g = self.p[li], self.g[li]
             x = self._layer_input(mb, li)
@@ -357,49 +415,56 @@ class StageCompute:
             if fused_w:
                 dyy = dy
                 on_side(ev(), lambda: (K.gemm(dyy, self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fd, k=S),
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=S_),
                                        _bias_grad(dyy, g["b_2"])))
-            # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)
+            # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
             K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=self.pre[mb, li],
-                   m=S, n=Fd, k=D)
+                   m=S_, n=Fl, k=D)
             if fused_w:
                 on_side(ev(), lambda: (K.gemm(d_pre, self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=Fd, n=D, k=S),
+                                              a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=S_),
                                        _bias_grad(d_pre, g["b_1"])))
-            # FC1 dgrad -> LN2 backward (+ residual grad dy)
-            K.gemm(d_pre, p["w_1"], self.d_head, b_mn=True, m=S, n=D, k=Fd)
+            # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy)
+            self._dgrad_reduce(d_pre, p["w_1"], Fl)
             _ln_bwd(self.d_head, self.x2[mb, li], self.m2[mb, li], self.r2[mb, li], p["ln2_g"], dy,
                     d_x2, g["ln2_g"], g["ln2_b"])
             if fused_w:
                 on_side(ev(), lambda: (K.gemm(d_x2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=D, k=S),
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=S_),
                                        _bias_grad(d_x2, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
-            K.gemm(d_x2, p["w_o"], self.d_head, b_mn=True, m=S, n=D, k=D)
-            self._attn_bwd(mb, li, self.d_head, d_qkv)
+            d_o = self.d_head if self.R == 1 else self.d_o
+            K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=S_, n=Dl, k=D)
+            self._attn_bwd(mb, li, d_o, d_qkv)
             if fused_w:
                 def qkv_w(d_qkv=d_qkv, li=li, g=g):
                     K.gemm(d_qkv, self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                           b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
+                           b_mn=True, accumulate=True, m=3 * Dl, n=D, k=S_)
                     _bias_grad(d_qkv, g["b_qkv"])
                 on_side(ev(), qkv_w)
                 done = torch.cuda.Event()
                 done.record(side)
                 side_done[li] = done
-            K.gemm(d_qkv, p["w_qkv"], self.d_head, b_mn=True, m=S, n=D, k=3 * D)
+            self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
+            extra = []
             if li > 0:
                 dx = dy_buf(li - 1)
                 if fused_w and li + 1 in side_done:   # layer li+1's side work read this buffer
                     main.wait_event(side_done[li + 1])
             elif not self.first:
-                dx = self.bwd_out[mb] if self.bwd_out is not None else self.sd_a[1]
+                if self.bwd_out is not None:
+                    dx, extra = self.bwd_out[mb][0], self.bwd_out[mb][1:]
+                else:
+                    dx = self.sd_a[1]
             else:
                 dx = self.gx0[mb] if dec else self.sd_a[1]
                 if fused_w and 1 in side_done:
                     main.wait_event(side_done[1])
             _ln_bwd(self.d_head, x, self.m1[mb, li], self.r1[mb, li], p["ln1_g"], d_x2, dx,
                     g["ln1_g"], g["ln1_b"])
+            for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
+                _copy_rows(dst, dx, S, D)
             dy = dx
         if self.first and fused_w:
             dyy = dy
@@ -411,9 +476,19 @@ class StageCompute:
             join.record(side)
             main.wait_event(join)
 
+    def _dgrad_reduce(self, d_col, w, k):
+        """Input gradient of a column-parallel layer into self.d_head: d_col . W
+        (K = this rank's columns); under TP a partial sum all-reduced over the group."""
+        S, D = self.cfg.seq, self.cfg.d_model
+        if self.R == 1:
+            K.gemm(d_col, w, self.d_head, b_mn=True, m=S, n=D, k=k)
+        else:
+            K.gemm(d_col, w, self.tp.partial, b_mn=True, m=S, n=D, k=k)
+            self.tp.allreduce([self.d_head])
+
     def _attn_bwd(self, mb, li, d_o, d_qkv):
         cfg = self.cfg
-        S, H, Dh, D = cfg.seq, cfg.n_head, cfg.d_head, cfg.d_model
+        S, H, Dh, D = cfg.seq, self.Hl, cfg.d_head, self.Dl
         qkv = self.qkv[mb, li]
         q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
         k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
@@ -440,7 +515,7 @@ class StageCompute:
         if not self.decompose:
             return
         cfg = self.cfg
-        S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
+        S, D, Fd, Dl = cfg.seq, cfg.d_model, self.Fl, self.Dl
         main = torch.cuda.current_stream()
         side = self.side or main
         fork = torch.cuda.Event()
@@ -456,10 +531,10 @@ class StageCompute:
                        b_mn=True, accumulate=True, m=Fd, n=D, k=S)
                 _bias_grad(self.gpre[mb, li], g["b_1"])
                 K.gemm(self.gx2[mb, li], self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=D, n=D, k=S)
+                       b_mn=True, accumulate=True, m=D, n=Dl, k=S)
                 _bias_grad(self.gx2[mb, li], g["b_o"])
                 K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=3 * D, n=D, k=S)
+                       b_mn=True, accumulate=True, m=3 * Dl, n=D, k=S)
                 _bias_grad(self.gqkv[mb, li], g["b_qkv"])
         with torch.cuda.stream(side):
             if self.last:
@@ -490,19 +565,27 @@ class StageCompute:
         else:
             self.backward_weight(mb)
 
-    def capture_bodies(self, stream=None):
-        """One CUDA graph per (kind, mb); returns 3*M raw cudaGraph_t handles
-        indexed kind*M + mb with kind B=0, F=1, W=2 (None where no work)."""
-        # F is captured before B/W: the B graph must bind the attention outputs
-        # (o, lse) that the CAPTURED F graph writes, not the warm-up's.
-        kinds = ["F", "B", "W"] if self.decompose else ["F", "B"]
+    def warmup(self, stream=None):
+        """Run every body once eagerly (cuDNN plan selection, module loads,
+        GEMM workspaces) on the capture stream; no host synchronisation, so
+        the ranks of a TP group can warm up concurrently (their all-reduces
+        wait for each other on the device).  Returns the stream."""
         stream = stream or torch.cuda.Stream(self.device)
-        # warm-up: run every body once eagerly (cuDNN plan selection, module loads)
         with torch.cuda.stream(stream):
             for mb in range(self.M):
                 for kind in ("F", "B", "W") if self.decompose else ("F", "B"):
                     self.run_task(kind, mb)
-        stream.synchronize()
+        self._cap_stream = stream
+        return stream
+
+    def capture(self):
+        """One CUDA graph per (kind, mb) (after warmup() and a synchronize);
+        returns 3*M raw cudaGraph_t handles indexed kind*M + mb with kind
+        B=0, F=1, W=2 (None where no work)."""
+        # F is captured before B/W: the B graph must bind the attention outputs
+        # (o, lse) that the CAPTURED F graph writes, not the warm-up's.
+        kinds = ["F", "B", "W"] if self.decompose else ["F", "B"]
+        stream = self._cap_stream
         self.zero_grads()
         raw = [None] * (3 * self.M)
         for kind in kinds:
@@ -518,3 +601,8 @@ class StageCompute:
         torch.cuda.synchronize(self.device)
         return raw
 
+    def capture_bodies(self, stream=None):
+        """warmup() + synchronize + capture() for a stage without TP peers."""
+        stream = self.warmup(stream)
+        stream.synchronize()
+        return self.capture()

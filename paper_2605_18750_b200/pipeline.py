@@ -26,7 +26,7 @@ from .workload import BACKWARD, FORWARD, WEIGHT, TaskId, Workload
 
 
 def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
-                     f_us=None, b_us=None, w_us=None) -> Workload:
+                     f_us=None, b_us=None, w_us=None, tp_size: int = 1) -> Workload:
     """A Workload describing the GPT iteration (latencies = nominal per-task µs).
 
     Only the structure matters to the free-running lanes (real kernels set
@@ -40,7 +40,7 @@ def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
             lat[TaskId(s, mb, 0, BACKWARD)] = int(b_us[s] if b_us else 2000)
             if decompose:
                 lat[TaskId(s, mb, 0, WEIGHT)] = int(w_us[s] if w_us else 1000)
-    return Workload(num_stages=n_stages, num_microbatches=n_mb, num_chunks=1, tp_group_size=1,
+    return Workload(num_stages=n_stages, num_microbatches=n_mb, num_chunks=1, tp_group_size=tp_size,
                     latency=lat, decompose_backward=decompose)
 
 
@@ -82,42 +82,80 @@ def measured_nominal(trace, n_stages):
 
 
 class GpuPipeline:
+    """All stages (and, with ``tp_size`` > 1, all TP ranks of every stage) in
+    this process; ``stages[s]`` is TP rank 0 of stage s, ``grid[s][r]`` every
+    rank.  TP ranks of a stage share its device; each is its own lane."""
+
     def __init__(self, cfg: GPTConfig, n_stages: int, n_mb: int, *, hint="bf", buffer_limit=32,
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
-                 schedule=None, comm_delay=None):
+                 schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None):
         if isinstance(hint, str):
             hint = HintOrder.parse(hint)
         if decompose is None:
             decompose = hint.kind == "bfw"
-        self.cfg, self.N, self.M, self.hint = cfg, n_stages, n_mb, hint
+        R = tp_size
+        self.cfg, self.N, self.M, self.hint, self.R = cfg, n_stages, n_mb, hint, R
         devices = devices or [0] * n_stages
         f_us, b_us, w_us = stage_latency_us or (None, None, None)
-        w = nominal_workload(cfg, n_stages, n_mb, decompose, f_us, b_us, w_us)
+        w = nominal_workload(cfg, n_stages, n_mb, decompose, f_us, b_us, w_us, tp_size=R)
         if comm_delay is not None:
             w = Workload(num_stages=w.num_stages, num_microbatches=w.num_microbatches,
-                         num_chunks=1, tp_group_size=1, latency=w.latency, comm_delay=comm_delay,
+                         num_chunks=1, tp_group_size=R, latency=w.latency, comm_delay=comm_delay,
                          decompose_backward=decompose)
         self.workload = w
-        self.stages = [StageCompute(cfg, s, n_stages, n_mb, torch.device("cuda", devices[s]),
-                                    decompose=decompose, seed=model_seed, data_seed=data_seed)
-                       for s in range(n_stages)]
-        for s, st in enumerate(self.stages):
-            nxt = self.stages[s + 1] if s + 1 < n_stages else None
-            prv = self.stages[s - 1] if s > 0 else None
-            st.connect_outputs(fwd_out=[nxt.fwd_in[mb] for mb in range(n_mb)] if nxt else None,
-                               bwd_out=[prv.bwd_in[mb] for mb in range(n_mb)] if prv else None)
-        bodies = {(s, 0): st.capture_bodies() for s, st in enumerate(self.stages)}
+        self.comms = {}
+        if R > 1:
+            from .tp import TpComm
+            for s in range(n_stages):
+                self.comms[s] = [TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", devices[s]))
+                                 for r in range(R)]
+                TpComm.connect_local(self.comms[s])
+        self.grid = [[StageCompute(cfg, s, n_stages, n_mb, torch.device("cuda", devices[s]),
+                                   decompose=decompose, seed=model_seed, data_seed=data_seed,
+                                   tp_rank=r, tp_size=R, tp=self.comms[s][r] if R > 1 else None)
+                      for r in range(R)] for s in range(n_stages)]
+        self.stages = [row[0] for row in self.grid]
+        for s in range(n_stages):
+            for r in range(R):
+                nxt = self.grid[s + 1] if s + 1 < n_stages else None
+                prv = self.grid[s - 1] if s > 0 else None
+                self.grid[s][r].connect_outputs(
+                    fwd_out=[[q.fwd_in[mb] for q in nxt] for mb in range(n_mb)] if nxt else None,
+                    bwd_out=[[q.bwd_in[mb] for q in prv] for mb in range(n_mb)] if prv else None)
+        # warm-up: every body once with rank-local all-reduces (every kernel
+        # module loaded before any rank spins on a peer), then capture
+        kinds = ("F", "B", "W") if decompose else ("F", "B")
+        for comms in self.comms.values():
+            for c in comms:
+                c.local_only = True
+        streams = {(s, r): torch.cuda.Stream(torch.device("cuda", devices[s]))
+                   for s in range(n_stages) for r in range(R)}
+        for mb in range(n_mb):
+            for kind in kinds:
+                for (s, r), stream in streams.items():
+                    st = self.grid[s][r]
+                    st._cap_stream = stream
+                    with torch.cuda.stream(stream):
+                        st.run_task(kind, mb)
+        for stream in streams.values():
+            stream.synchronize()
+        for comms in self.comms.values():
+            for c in comms:
+                c.local_only = False
+        bodies = {(s, r): self.grid[s][r].capture() for s in range(n_stages) for r in range(R)}
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
-                               placement=[[d] for d in devices], bodies=bodies, compute_kind=1,
+                               tp=tp or (TpGroup(group_size=R) if R > 1 else None),
+                               placement=[[d] * R for d in devices], bodies=bodies, compute_kind=1,
                                schedule=schedule)
         self.last_events = None
 
     def step(self, watchdog_secs: float = 120.0, zero_grads: bool = True):
         """One iteration; returns (loss tensor on device, raw events, t0)."""
         if zero_grads:
-            for st in self.stages:
-                st.zero_grads()
+            for row in self.grid:
+                for st in row:
+                    st.zero_grads()
         events, t0s = self.group.run_iteration(watchdog_secs)
         self.last_events = (events, min(t0s))
         last = self.stages[-1]
@@ -126,8 +164,9 @@ class GpuPipeline:
     def launch(self, zero_grads: bool = True):
         """Asynchronous step (for timing loops): enqueue, do not wait."""
         if zero_grads:
-            for st in self.stages:
-                st.zero_grads()
+            for row in self.grid:
+                for st in row:
+                    st.zero_grads()
         self.group.launch()
 
     def wait(self, watchdog_secs: float = 120.0):
@@ -149,9 +188,10 @@ class GpuPipeline:
         """Our kernels launched per iteration: every task body (captured counts)
         plus the lane's dispatch + complete kernels per task and init/final."""
         n = 0
-        for st in self.stages:
-            n += sum(st.kernel_counts.values())
-            n += 2 * len(st.kernel_counts) + 2
+        for row in self.grid:
+            for st in row:
+                n += sum(st.kernel_counts.values())
+                n += 2 * len(st.kernel_counts) + 2
         return n
 
     def trace(self):
@@ -160,3 +200,7 @@ class GpuPipeline:
 
     def close(self):
         self.group.close()
+        for comms in self.comms.values():
+            for c in comms:
+                c.close()
+        self.comms = {}

@@ -12,10 +12,13 @@ def ln(x, g, b, eps):
 
 def reference_loss_and_grads(cfg, stages):
     """stages: list of StageCompute (any PP split).  Returns (loss, {name: grad})."""
+    from paper_2605_18750_b200.model import init_layer_params
     params = {}
     for st in stages:
         for li, lid in enumerate(st.layers):
-            for k, v in st.p[li].items():
+            # TP stages hold shards: rebuild the full layer from its deterministic init
+            full = st.p[li] if st.R == 1 else init_layer_params(cfg, lid, st.device, st.model_seed)
+            for k, v in full.items():
                 params[f"L{lid}.{k}"] = v.float().clone().requires_grad_(True)
         if st.first:
             for k, v in st.emb.items():
@@ -59,6 +62,38 @@ def device_grads(stages):
             out.update(st.g_emb)
         if st.last:
             out.update(st.g_head)
+    return out
+
+
+def device_grads_tp(grid, cfg):
+    """Full gradients from the TP shards of every stage (grid[s][r]): QKV / FC1
+    rows and out-proj / FC2 columns concatenated in rank order; replicated
+    parameters (LayerNorms, b_o, b_2, embedding, head) must agree across ranks
+    (to fp32 atomic-order noise: their column reductions use atomics)."""
+    out = {}
+    D, R = cfg.d_model, len(grid[0])
+    dl = D // R
+    for row in grid:
+        st0 = row[0]
+        for li, lid in enumerate(st0.layers):
+            gs = [st.g[li] for st in row]
+            for k in gs[0]:
+                if k in ("w_qkv", "b_qkv"):
+                    parts = [torch.cat([g[k][i * dl:(i + 1) * dl] for g in gs]) for i in range(3)]
+                    out[f"L{lid}.{k}"] = torch.cat(parts)
+                elif k in ("w_1", "b_1"):
+                    out[f"L{lid}.{k}"] = torch.cat([g[k] for g in gs])
+                elif k in ("w_o", "w_2"):
+                    out[f"L{lid}.{k}"] = torch.cat([g[k] for g in gs], dim=1)
+                else:
+                    for g in gs[1:]:
+                        assert torch.allclose(g[k], gs[0][k], rtol=1e-3, atol=1e-6), \
+                            f"replicated grad {k} differs across TP ranks"
+                    out[f"L{lid}.{k}"] = gs[0][k]
+        if st0.first:
+            out.update(st0.g_emb)
+        if st0.last:
+            out.update(st0.g_head)
     return out
 
 

@@ -52,3 +52,29 @@ def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode):
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("n_stages,tp,hint,mode", [(1, 2, "bf", "free"), (2, 2, "bf", "free"),
+                                                   (2, 2, "bfw", "free"), (2, 2, "bf", "fixed")])
+def test_tp_pipeline_matches_fp32_reference(n_stages, tp, hint, mode):
+    """Config 3 on one GPU: TP=2 lanes per stage, column/row-parallel GEMMs and
+    the peer-memory all-reduce kernel; loss and (unsharded) gradients against
+    the non-parallel fp32 reference; replicated gradients bit-identical across ranks."""
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from ref_gpt import device_grads_tp
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, tp_size=tp)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        for row in pipe.grid:
+            for st in row:
+                assert st.tp.error() == 0
+        assert torch.equal(pipe.grid[-1][0].loss, pipe.grid[-1][1].loss)   # ranks agree bit-exactly
+        tr, met = pipe.trace()
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads_tp(pipe.grid, cfg))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
