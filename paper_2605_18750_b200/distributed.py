@@ -23,6 +23,14 @@ import torch
 from . import _lib
 
 
+def stage_coords(global_rank: int, world: int, tp_size: int = 1):
+    """torchrun rank -> (pipeline stage, TP rank, n_stages): the TP ranks of a
+    stage are adjacent process ranks (adjacent GPUs of the box)."""
+    if tp_size < 1 or world % tp_size:
+        raise ValueError(f"world size {world} is not a multiple of the TP size {tp_size}")
+    return global_rank // tp_size, global_rank % tp_size, world // tp_size
+
+
 def plan_peers(stage: int, n_stages: int, n_ranks: int = 1):
     """Who a lane sends to: F output -> next stage (chunk wrap to stage 0),
     B output -> previous stage (wrap to N-1); all R ranks of the receiver."""
@@ -75,20 +83,28 @@ def open_handle(handle: bytes) -> int:
 
 
 class DistPipeline:
-    """This rank's stage of a PP=world pipeline (one stage per GPU)."""
+    """This rank's lane of a PP x TP pipeline: one (stage, TP rank) per GPU.
+
+    world = n_stages * tp_size; stage_coords() maps the process rank.  Every
+    sender rank writes its output into the mailbox of EVERY TP rank of the
+    neighbour stage (identical bytes), then raises its flags (runtime lane_send);
+    TP partial sums are all-reduced over peer memory (tp.py / csrc/tp.cu)."""
 
     def __init__(self, cfg, n_mb: int, *, hint="bf", buffer_limit=32, mode="free", jitter=None,
-                 seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None):
+                 seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None,
+                 tp_size: int = 1, tp=None):
         import torch.distributed as dist
-        from .arbitration import HintOrder
+        from .arbitration import HintOrder, TpGroup
         from .model import StageCompute
         from .pipeline import nominal_workload
         from .runtime import LaneGroup
         if isinstance(hint, str):
             hint = HintOrder.parse(hint)
-        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.grank, self.gworld = dist.get_rank(group), dist.get_world_size(group)
+        s, r, n = stage_coords(self.grank, self.gworld, tp_size)
+        R = tp_size
+        self.rank, self.world, self.tp_rank, self.R = s, n, r, R
         self.device = torch.cuda.current_device()
-        n, s = self.world, self.rank
         decompose = hint.kind == "bfw"
         S, D = cfg.seq, cfg.d_model
         slot_bytes = n_mb * S * D * 2
@@ -96,37 +112,52 @@ class DistPipeline:
                      "bwd": IpcBuffer(slot_bytes, self.device) if s < n - 1 else None}
         fwd_in = wrap_bf16(self.bufs["fwd"].ptr.value, (n_mb, S, D), self.device) if s > 0 else None
         bwd_in = wrap_bf16(self.bufs["bwd"].ptr.value, (n_mb, S, D), self.device) if s < n - 1 else None
+        self.comm = None
+        if R > 1:
+            from .tp import TpComm
+            self.comm = TpComm(r, R, (S, D), torch.device("cuda", self.device))
         self.stage = StageCompute(cfg, s, n, n_mb, torch.device("cuda", self.device),
                                   decompose=decompose, seed=model_seed, data_seed=data_seed,
-                                  fwd_in=fwd_in, bwd_in=bwd_in)
-        w = nominal_workload(cfg, n, n_mb, decompose)
+                                  fwd_in=fwd_in, bwd_in=bwd_in, tp_rank=r, tp_size=R, tp=self.comm)
+        w = nominal_workload(cfg, n, n_mb, decompose, tp_size=R)
         if comm_delay is not None:
             from .workload import Workload
-            w = Workload(num_stages=n, num_microbatches=n_mb, num_chunks=1, tp_group_size=1,
+            w = Workload(num_stages=n, num_microbatches=n_mb, num_chunks=1, tp_group_size=R,
                          latency=w.latency, comm_delay=comm_delay, decompose_backward=decompose)
         self.workload = w
         self.n_mb = n_mb
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
-                               placement=[[self.device] for _ in range(n)], local=[(s, 0)],
+                               tp=tp or (TpGroup(group_size=R) if R > 1 else None),
+                               placement=[[self.device] * R for _ in range(n)], local=[(s, r)],
                                bodies=None, compute_kind=1, schedule=schedule, defer_bodies=True)
-        mine = {"stage": s, "fwd": self.bufs["fwd"].handle() if self.bufs["fwd"] else None,
+        mine = {"stage": s, "tp_rank": r,
+                "fwd": self.bufs["fwd"].handle() if self.bufs["fwd"] else None,
                 "bwd": self.bufs["bwd"].handle() if self.bufs["bwd"] else None,
-                "lane": self.group.ipc_handles()[(s, 0)]}
-        allh = [None] * n
+                "lane": self.group.ipc_handles()[(s, r)],
+                "tp": self.comm.ipc_handles() if self.comm else None}
+        allh = [None] * self.gworld
         dist.all_gather_object(allh, mine, group=group)
-        peers = plan_peers(s, n)
+        by = {(h["stage"], h["tp_rank"]): h for h in allh}
+        if self.comm:
+            self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
+        peers = plan_peers(s, n, R)
         fwd_out = bwd_out = None
         if peers["writes_fwd_mailbox"]:
-            base = open_handle(allh[s + 1]["fwd"])
-            fwd_out = wrap_bf16(base, (n_mb, S, D), self.device)
+            dst = [wrap_bf16(open_handle(by[(s + 1, q)]["fwd"]), (n_mb, S, D), self.device) for q in range(R)]
+            fwd_out = [[d[mb] for d in dst] for mb in range(n_mb)]
         if peers["writes_bwd_mailbox"]:
-            base = open_handle(allh[s - 1]["bwd"])
-            bwd_out = wrap_bf16(base, (n_mb, S, D), self.device)
-        self.stage.connect_outputs(fwd_out=[fwd_out[mb] for mb in range(n_mb)] if fwd_out is not None else None,
-                                   bwd_out=[bwd_out[mb] for mb in range(n_mb)] if bwd_out is not None else None)
-        raw = self.stage.capture_bodies()
-        self.group.set_bodies({(s, 0): raw})
-        self.group.connect_ipc({(h["stage"], 0): h["lane"] for h in allh})
+            dst = [wrap_bf16(open_handle(by[(s - 1, q)]["bwd"]), (n_mb, S, D), self.device) for q in range(R)]
+            bwd_out = [[d[mb] for d in dst] for mb in range(n_mb)]
+        self.stage.connect_outputs(fwd_out=fwd_out, bwd_out=bwd_out)
+        # eager warm-up with rank-local all-reduces (module loading never races a spinning peer)
+        if self.comm:
+            self.comm.local_only = True
+        self.stage.warmup().synchronize()
+        if self.comm:
+            self.comm.local_only = False
+        raw = self.stage.capture()
+        self.group.set_bodies({(s, r): raw})
+        self.group.connect_ipc({(h["stage"], h["tp_rank"]): h["lane"] for h in allh})
         torch.cuda.synchronize()
         dist.barrier(group=group)
         # every rank instantiates + uploads its lane graph before ANY rank launches
@@ -144,9 +175,9 @@ class DistPipeline:
             for d, code in (("F", 1), ("B", 0), ("W", 2)):
                 xs = [e.t1 - e.t0 for e in ev if e.kind == 0 and (e.task & 3) == code]
                 mine[d] = (sum(xs) / len(xs) / 1000.0) if xs else 0.0
-            allv = [None] * self.world
+            allv = [None] * self.gworld
             dist.all_gather_object(allv, mine, group=group)
-            nominal_us = allv
+            nominal_us = allv[::self.R]      # TP rank 0 of every stage
         self.nominal_us = nominal_us
         floors = lognormal_floor_tables(self.world, self.n_mb, nominal_us, sigma, seed, stages=[self.rank])
         self.group.set_floor_us(floors)
@@ -173,3 +204,6 @@ class DistPipeline:
 
     def close(self):
         self.group.close()
+        if self.comm:
+            self.comm.close()
+            self.comm = None

@@ -69,3 +69,12 @@ def test_plan_wraps_for_interleaved_chunks():
     p = plan_peers(3, 4, 2)
     assert p["fwd"] == [(0, 0), (0, 1)] and p["bwd"] == [(2, 0), (2, 1)]
     assert not p["writes_fwd_mailbox"] and p["writes_bwd_mailbox"]
+
+
+def test_stage_coords_tp_groups():
+    """torchrun rank -> (stage, TP rank): TP ranks of a stage are adjacent (config 3: TP2 x PP4)."""
+    from paper_2605_18750_b200.distributed import stage_coords
+    assert [stage_coords(g, 8, 2) for g in range(8)] == [(s, r, 4) for s in range(4) for r in range(2)]
+    assert [stage_coords(g, 4, 1)[:2] for g in range(4)] == [(g, 0) for g in range(4)]
+    with pytest.raises(ValueError):
+        stage_coords(0, 6, 4)

@@ -23,7 +23,8 @@ def main():
     from paper_2605_18750_b200.distributed import DistPipeline
     cfg = GPTConfig(n_layer=4, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=256)
     hint = sys.argv[1] if len(sys.argv) > 1 else "bf"
-    pipe = DistPipeline(cfg, 4, hint=hint)
+    tp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp)
     losses = []
     for _ in range(2):
         loss = pipe.step(watchdog_secs=60)
@@ -32,7 +33,8 @@ def main():
     ev, t0 = pipe.last_events
     n_exec = sum(1 for e in ev if e.kind == 0)
     out = [None] * world
-    dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec})
+    tp_err = pipe.comm.error() if pipe.comm else 0
+    dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec, "tp_err": tp_err})
     pipe.close()
     if rank == 0:
         from paper_2605_18750_b200.pipeline import GpuPipeline
