@@ -98,8 +98,8 @@ def run_reference(args):
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import rrfp_oracle as O
-    n = max(1, args.gpus)
-    times = default_task_times(n, args.layers)
+    n = max(1, args.gpus // args.tp)
+    times = default_task_times(n, model_config(args).n_layer)
     lat = {}
     dec = args.hint == "bfw"
     for s in range(n):
@@ -155,11 +155,21 @@ def default_task_times(n_stages, n_layer=24):
     return {"F": f, "B": [2.1 * x for x in f], "Bin": [1.15 * x for x in f], "W": [0.95 * x for x in f]}
 
 
+def model_config(args):
+    """GPT-1.3B (BASELINE config 2) or GPT-7B (config 3, run with --tp 2)."""
+    from paper_2605_18750_b200.model import GPTConfig
+    if args.model == "7b":
+        return GPTConfig(n_layer=args.layers or 32, d_model=4096, n_head=32, d_ff=16384)
+    return GPTConfig(n_layer=args.layers or 24)
+
+
 def workload_config(args, n):
-    return {"workload": f"GPT-1.3B synthetic (L={args.layers}, d=2048, h=16, ffn=8192, V=50304, "
-                        f"s=2048, mbs=1), PP={n}, M={args.mb}",
-            "model": "gpt-1.3b-synthetic", "global_batch": args.mb, "seq_len": 2048,
-            "parallelism": f"pp{n}", "hint": args.hint, "jitter": args.jitter,
+    c = model_config(args)
+    par = f"pp{n}" + (f"xtp{args.tp}" if args.tp > 1 else "")
+    return {"workload": f"GPT-{args.model.upper()} synthetic (L={c.n_layer}, d={c.d_model}, h={c.n_head}, "
+                        f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, M={args.mb}",
+            "model": f"gpt-{args.model}-synthetic", "global_batch": args.mb, "seq_len": c.seq,
+            "parallelism": par, "hint": args.hint, "jitter": args.jitter,
             "buffer_limit": 32, "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
 
 
@@ -239,10 +249,11 @@ def run_ours(args):
     if os.environ.get("RRFP_SAME_DEVICE") == "1":     # 1-GPU test of the multi-process path
         local = 0
     torch.cuda.set_device(local)
-    from paper_2605_18750_b200.model import GPTConfig
     from paper_2605_18750_b200.jitter import PRESETS
-    cfg = GPTConfig(n_layer=args.layers)
-    n = world
+    cfg = model_config(args)
+    if world % args.tp:
+        raise SystemExit(f"--tp {args.tp} must divide the number of processes {world}")
+    n = world // args.tp if world > 1 else 1      # pipeline stages
     hint = "bf" if args.hint == "1f1b" else args.hint
     mode = "fixed" if args.hint == "1f1b" else "free"
     dist = None
@@ -328,8 +339,13 @@ def run_ours(args):
     roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
     fF, fB, fW = cfg.flops_per_layer()
     it_flops = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
-    p2p = 2 * args.mb * cfg.seq * cfg.d_model * 2 if n > 1 else 0
-    t_roof = it_flops / (n * peak_sus * 1e12) + p2p / 770e9
+    n_dev = max(1, world)
+    act = cfg.seq * cfg.d_model * 2
+    # per GPU: mailbox writes (F out + B out, one copy per receiving TP rank) and
+    # TP all-reduce peer reads (4 per layer per microbatch, R-1 partials each)
+    p2p = (2 * args.mb * act * args.tp if n > 1 else 0) + \
+        4 * (cfg.n_layer // n) * args.mb * act * (args.tp - 1)
+    t_roof = it_flops / (n_dev * peak_sus * 1e12) + p2p / 770e9
     launches = pipe.kernel_launches_per_step() if hasattr(pipe, "kernel_launches_per_step") else 0
     if dist:
         lt = torch.tensor([launches], dtype=torch.int64)
@@ -343,8 +359,8 @@ def run_ours(args):
             "tokens_per_s": round(it_s * tok, 1), "bubble_fraction": round(bubble, 4),
             "iteration_roofline": {"t_roof_ms": round(t_roof * 1e3, 2),
                                    "frac": round(t_roof * 1e3 / ms, 3),
-                                   "definition": "sum stage FLOPs / (N * sustained bf16 peak) "
-                                                 "+ per-GPU P2P bytes / 770 GB/s"},
+                                   "definition": "sum stage FLOPs / (N_gpu * sustained bf16 peak) "
+                                                 "+ per-GPU P2P + TP all-reduce bytes / 770 GB/s"},
             "roofline": roof,
             "task_us": task_us,
             "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
@@ -369,10 +385,12 @@ def run_ours(args):
 def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
-        pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay)
+        pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
+                            tp_size=args.tp)
         return pipe, [pipe.stage]
     from paper_2605_18750_b200.pipeline import GpuPipeline
-    pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay)
+    pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
+                       tp_size=args.tp)
     return pipe, pipe.stages
 
 
@@ -472,7 +490,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--hint", default="bf", choices=["bf", "bfw", "fb", "bprio", "fprio", "1f1b"])
     ap.add_argument("--mb", type=int, default=32)
-    ap.add_argument("--layers", type=int, default=24)
+    ap.add_argument("--layers", type=int, default=None, help="default: 24 (1.3b) / 32 (7b)")
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"])
+    ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size per stage (config 3: 2)")
     ap.add_argument("--jitter", default="J0")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--compare", dest="compare", action="store_true", default=None,
