@@ -221,9 +221,9 @@ int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst_inboxes, void* c
  * between iterations. */
 int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns, const int64_t* comm_ns,
                              const int64_t* skew_ns, const rrfp_task_t* fixed, const int64_t* min_ns);
-/* Register caller-captured compute bodies: graphs[kind * M + mb] is the
- * cudaGraph_t run for task (kind, mb) (kind: 0 = B, 1 = F, 2 = W; NULL = no
- * work), n = 3 * M.  The dispatcher selects the branch with
+/* Register caller-captured compute bodies: graphs[kind * M*C + chunk * M + mb]
+ * is the cudaGraph_t run for task (kind, mb, chunk) (kind: 0 = B, 1 = F, 2 = W;
+ * NULL = no work), n = 3 * M * C.  The dispatcher selects the branch with
  * cudaGraphSetConditional.  Must be called before the first launch. */
 int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* const* graphs, int32_t n);
 int rrfp_runtime_task_ptr(rrfp_runtime* rt, void** dev_ptr);

@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
         L->mon[1] = (int32_t)L->cur_task;
         L->t_start = gtimer();
         unsigned branch = (unsigned)s_kind;
-        if (d.compute_kind == 1) branch = (unsigned)(s_kind * d.M + rrfp_task_mb(L->cur_task));
+        if (d.compute_kind == 1)   // body (kind, chunk, mb): kind * M*C + chunk * M + mb
+          branch = (unsigned)(s_kind * d.M * d.C + rrfp_task_chunk(L->cur_task) * d.M + rrfp_task_mb(L->cur_task));
         cudaGraphSetConditional(L->h_switch, branch);
       }
     }
@@ -654,7 +655,8 @@ extern "C" int rrfp_runtime_load_tables(rrfp_runtime* rt, const int64_t* dur_ns,
 extern "C" int rrfp_runtime_set_bodies(rrfp_runtime* rt, void* const* graphs, int32_t n) {
   if (!rt || !graphs) return rrfp_fail(RRFP_E_INVALID, "null argument");
   if (rt->built) return rrfp_fail(RRFP_E_INVALID, "bodies must be set before the first launch");
-  if (n != 3 * rt->d.M) return rrfp_fail(RRFP_E_INVALID, "need 3*M body graphs, got %d", n);
+  if (n != 3 * rt->d.M * rt->d.C)
+    return rrfp_fail(RRFP_E_INVALID, "need 3*M*C body graphs, got %d", n);
   rt->bodies.assign(n, nullptr);
   for (int i = 0; i < n; ++i) rt->bodies[i] = (cudaGraph_t)graphs[i];
   return RRFP_OK;
@@ -701,7 +703,7 @@ static int build_graph(rrfp_runtime* rt) {
   sp.conditional.handle = hs;
   sp.conditional.type = cudaGraphCondTypeSwitch;
   const bool per_mb = rt->d.compute_kind == 1;
-  const int nb = per_mb ? 3 * rt->d.M : 3;
+  const int nb = per_mb ? 3 * rt->d.M * rt->d.C : 3;
   sp.conditional.size = nb;
   RRFP_CUDA_TRY(cudaGraphAddNode(&n_sw, loop, &n_dec, 1, &sp));
   for (int k = 0; k < nb; ++k) {

@@ -26,7 +26,7 @@ from .workload import BACKWARD, FORWARD, WEIGHT, TaskId, Workload
 
 
 def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
-                     f_us=None, b_us=None, w_us=None, tp_size: int = 1) -> Workload:
+                     f_us=None, b_us=None, w_us=None, tp_size: int = 1, n_chunks: int = 1) -> Workload:
     """A Workload describing the GPT iteration (latencies = nominal per-task µs).
 
     Only the structure matters to the free-running lanes (real kernels set
@@ -35,12 +35,13 @@ def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
     """
     lat = {}
     for s in range(n_stages):
-        for mb in range(n_mb):
-            lat[TaskId(s, mb, 0, FORWARD)] = int(f_us[s] if f_us else 1000)
-            lat[TaskId(s, mb, 0, BACKWARD)] = int(b_us[s] if b_us else 2000)
-            if decompose:
-                lat[TaskId(s, mb, 0, WEIGHT)] = int(w_us[s] if w_us else 1000)
-    return Workload(num_stages=n_stages, num_microbatches=n_mb, num_chunks=1, tp_group_size=tp_size,
+        for c in range(n_chunks):
+            for mb in range(n_mb):
+                lat[TaskId(s, mb, c, FORWARD)] = int(f_us[s] if f_us else 1000)
+                lat[TaskId(s, mb, c, BACKWARD)] = int(b_us[s] if b_us else 2000)
+                if decompose:
+                    lat[TaskId(s, mb, c, WEIGHT)] = int(w_us[s] if w_us else 1000)
+    return Workload(num_stages=n_stages, num_microbatches=n_mb, num_chunks=n_chunks, tp_group_size=tp_size,
                     latency=lat, decompose_backward=decompose)
 
 
@@ -83,44 +84,50 @@ def measured_nominal(trace, n_stages):
 
 class GpuPipeline:
     """All stages (and, with ``tp_size`` > 1, all TP ranks of every stage) in
-    this process; ``stages[s]`` is TP rank 0 of stage s, ``grid[s][r]`` every
-    rank.  TP ranks of a stage share its device; each is its own lane."""
+    this process.  With ``n_chunks`` = C > 1 (interleaved virtual stages,
+    workload.py:251-256) the model is split over V = N*C virtual stages and
+    virtual stage v = c*N + s is chunk c of lane s: its F output feeds v+1,
+    i.e. (s+1, c) or, from the last stage, the wrap edge (0, c+1).
+    ``grid[v][r]`` is virtual stage v, TP rank r; ``stages[v]`` its rank 0.
+    TP ranks of a stage share its device; each is its own lane."""
 
     def __init__(self, cfg: GPTConfig, n_stages: int, n_mb: int, *, hint="bf", buffer_limit=32,
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
-                 schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None):
+                 schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
+                 n_chunks: int = 1):
         if isinstance(hint, str):
             hint = HintOrder.parse(hint)
         if decompose is None:
             decompose = hint.kind == "bfw"
-        R = tp_size
-        self.cfg, self.N, self.M, self.hint, self.R = cfg, n_stages, n_mb, hint, R
-        devices = devices or [0] * n_stages
+        R, C, N = tp_size, n_chunks, n_stages
+        V = N * C
+        self.cfg, self.N, self.M, self.hint, self.R, self.C = cfg, N, n_mb, hint, R, C
+        devices = devices or [0] * N
         f_us, b_us, w_us = stage_latency_us or (None, None, None)
-        w = nominal_workload(cfg, n_stages, n_mb, decompose, f_us, b_us, w_us, tp_size=R)
+        w = nominal_workload(cfg, N, n_mb, decompose, f_us, b_us, w_us, tp_size=R, n_chunks=C)
         if comm_delay is not None:
             w = Workload(num_stages=w.num_stages, num_microbatches=w.num_microbatches,
-                         num_chunks=1, tp_group_size=R, latency=w.latency, comm_delay=comm_delay,
+                         num_chunks=C, tp_group_size=R, latency=w.latency, comm_delay=comm_delay,
                          decompose_backward=decompose)
         self.workload = w
         self.comms = {}
-        if R > 1:
+        if R > 1:   # one TP group per lane (its virtual stages run one task at a time)
             from .tp import TpComm
-            for s in range(n_stages):
+            for s in range(N):
                 self.comms[s] = [TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", devices[s]))
                                  for r in range(R)]
                 TpComm.connect_local(self.comms[s])
-        self.grid = [[StageCompute(cfg, s, n_stages, n_mb, torch.device("cuda", devices[s]),
+        self.grid = [[StageCompute(cfg, v, V, n_mb, torch.device("cuda", devices[v % N]),
                                    decompose=decompose, seed=model_seed, data_seed=data_seed,
-                                   tp_rank=r, tp_size=R, tp=self.comms[s][r] if R > 1 else None)
-                      for r in range(R)] for s in range(n_stages)]
+                                   tp_rank=r, tp_size=R, tp=self.comms[v % N][r] if R > 1 else None)
+                      for r in range(R)] for v in range(V)]
         self.stages = [row[0] for row in self.grid]
-        for s in range(n_stages):
+        for v in range(V):
             for r in range(R):
-                nxt = self.grid[s + 1] if s + 1 < n_stages else None
-                prv = self.grid[s - 1] if s > 0 else None
-                self.grid[s][r].connect_outputs(
+                nxt = self.grid[v + 1] if v + 1 < V else None
+                prv = self.grid[v - 1] if v > 0 else None
+                self.grid[v][r].connect_outputs(
                     fwd_out=[[q.fwd_in[mb] for q in nxt] for mb in range(n_mb)] if nxt else None,
                     bwd_out=[[q.bwd_in[mb] for q in prv] for mb in range(n_mb)] if prv else None)
         # warm-up: every body once with rank-local all-reduces (every kernel
@@ -129,12 +136,12 @@ class GpuPipeline:
         for comms in self.comms.values():
             for c in comms:
                 c.local_only = True
-        streams = {(s, r): torch.cuda.Stream(torch.device("cuda", devices[s]))
-                   for s in range(n_stages) for r in range(R)}
+        streams = {(v, r): torch.cuda.Stream(torch.device("cuda", devices[v % N]))
+                   for v in range(V) for r in range(R)}
         for mb in range(n_mb):
             for kind in kinds:
-                for (s, r), stream in streams.items():
-                    st = self.grid[s][r]
+                for (v, r), stream in streams.items():
+                    st = self.grid[v][r]
                     st._cap_stream = stream
                     with torch.cuda.stream(stream):
                         st.run_task(kind, mb)
@@ -143,7 +150,17 @@ class GpuPipeline:
         for comms in self.comms.values():
             for c in comms:
                 c.local_only = False
-        bodies = {(s, r): self.grid[s][r].capture() for s in range(n_stages) for r in range(R)}
+        raw_v = {(v, r): self.grid[v][r].capture() for v in range(V) for r in range(R)}
+        bodies = {}
+        for s in range(N):
+            for r in range(R):
+                arr = [None] * (3 * n_mb * C)
+                for c in range(C):
+                    raw = raw_v[(c * N + s, r)]
+                    for ki in range(3):
+                        for mb in range(n_mb):
+                            arr[ki * n_mb * C + c * n_mb + mb] = raw[ki * n_mb + mb]
+                bodies[(s, r)] = arr
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
                                tp=tp or (TpGroup(group_size=R) if R > 1 else None),
                                placement=[[d] * R for d in devices], bodies=bodies, compute_kind=1,

@@ -151,7 +151,7 @@ class LaneGroup:
                                                       _ptr(fixed), _ptr(floor) if floor is not None
                                                       else None))
             if bodies is not None:
-                arr = bodies[(s, k)]          # 3*M raw cudaGraph_t handles (kind*M + mb)
+                arr = bodies[(s, k)]          # 3*M*C raw cudaGraph_t handles (kind*M*C + chunk*M + mb)
                 carr = (C.c_void_p * len(arr))(*[C.c_void_p(x or 0) for x in arr])
                 _lib.check(self.L.rrfp_runtime_set_bodies(h, carr, len(arr)))
         self.cap = cap

@@ -78,3 +78,27 @@ def test_tp_pipeline_matches_fp32_reference(n_stages, tp, hint, mode):
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("n_stages,chunks,hint,mode,tp", [(2, 2, "bf", "free", 1), (2, 2, "bfw", "free", 1),
+                                                          (2, 2, "bf", "replay", 1), (2, 2, "bf", "free", 2)])
+def test_interleaved_chunks_match_fp32_reference(n_stages, chunks, hint, mode, tp):
+    """C=2 virtual stages per lane (chunk-wrap edge N-1 -> 0),
+    GPT bodies selected per (kind, chunk, mb) by the device dispatcher."""
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from ref_gpt import device_grads_tp
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, n_chunks=chunks, tp_size=tp)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        tr, met = pipe.trace()
+        assert len(tr.execs()) == pipe.workload.task_count() * tp
+        assert {e.chunk for e in tr.execs()} == set(range(chunks))
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        got = device_grads_tp(pipe.grid, cfg) if tp > 1 else device_grads(pipe.stages)
+        bad = compare(ref_grads, got)
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
