@@ -165,9 +165,9 @@ def model_config(args):
 
 def workload_config(args, n):
     c = model_config(args)
-    par = f"pp{n}" + (f"xtp{args.tp}" if args.tp > 1 else "")
+    par = f"pp{n}" + (f"xtp{args.tp}" if args.tp > 1 else "") + (f"xc{args.chunks}" if args.chunks > 1 else "")
     return {"workload": f"GPT-{args.model.upper()} synthetic (L={c.n_layer}, d={c.d_model}, h={c.n_head}, "
-                        f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, M={args.mb}",
+                        f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, C={args.chunks}, M={args.mb}",
             "model": f"gpt-{args.model}-synthetic", "global_batch": args.mb, "seq_len": c.seq,
             "parallelism": par, "hint": args.hint, "jitter": args.jitter,
             "buffer_limit": 32, "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
@@ -386,11 +386,11 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                            tp_size=args.tp)
-        return pipe, [pipe.stage]
+                            tp_size=args.tp, n_chunks=args.chunks)
+        return pipe, pipe.vstages
     from paper_2605_18750_b200.pipeline import GpuPipeline
     pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                       tp_size=args.tp)
+                       tp_size=args.tp, n_chunks=args.chunks)
     return pipe, pipe.stages
 
 
@@ -411,6 +411,8 @@ def compare_variants(cfg, args, world, dist, barrier, nominal):
             comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
                              hi=int(args.comm_us * 50), seed=17)
         for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
+            if name == "1f1b" and args.chunks > 1:
+                continue          # 1F1B is undefined for interleaved chunks (baselines.py:72-75)
             if world == 1 and name == "bfw" and cfg.n_layer * args.mb > 8 * 32:
                 continue          # PP=1 BFW keeps every W pending: memory-bound, meaningless
             pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS["J0"], comm)
@@ -493,6 +495,7 @@ def main():
     ap.add_argument("--layers", type=int, default=None, help="default: 24 (1.3b) / 32 (7b)")
     ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"])
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size per stage (config 3: 2)")
+    ap.add_argument("--chunks", type=int, default=1, help="interleaved virtual stages per GPU (C)")
     ap.add_argument("--jitter", default="J0")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--compare", dest="compare", action="store_true", default=None,

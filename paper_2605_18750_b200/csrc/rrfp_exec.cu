@@ -41,8 +41,12 @@ struct lane_inbox {
   uint32_t bflag[RRFP_MAX_KEYS];
   unsigned long long fvis[RRFP_MAX_KEYS];
   unsigned long long bvis[RRFP_MAX_KEYS];
-  unsigned long long tp_prop[RRFP_MAX_RANKS];  // (round << 32) | decision code
-  uint32_t tp_cnt[RRFP_MAX_RANKS];             // proposer's view count at proposal
+  // proposals double-buffered by round parity: a rank can run at most ONE round
+  // ahead of a peer still gathering (it needs the peer's proposal of the
+  // current round to finish it), so slot (round & 1) is never overwritten
+  // before every peer has read it.
+  unsigned long long tp_prop[2][RRFP_MAX_RANKS];  // (round << 32) | decision code
+  uint32_t tp_cnt[2][RRFP_MAX_RANKS];             // proposer's view count at proposal
   uint32_t view_count;                          // monotone count of visible arrivals
   uint32_t done_epoch;                          // iteration barrier
   uint32_t pad[2];
@@ -290,22 +294,23 @@ __global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
         unsigned long long round = ++L->tp_round;
         unsigned long long word = (round << 32) | dec_code(dec);
         uint32_t mycnt = L->inbox->view_count;
+        const int par = (int)(round & 1);
         for (int r = 0; r < R; ++r) {
-          L->tp_peer[r]->tp_cnt[d.rank] = mycnt;
+          L->tp_peer[r]->tp_cnt[par][d.rank] = mycnt;
           __threadfence_system();
-          st_release_sys64(&L->tp_peer[r]->tp_prop[d.rank], word);
+          st_release_sys64(&L->tp_peer[r]->tp_prop[par][d.rank], word);
         }
         rrfp_decision ds[RRFP_MAX_RANKS];
         uint32_t snap = 0;
         for (int r = 0; r < R; ++r) {
           unsigned long long w;
-          while (((w = ld_acquire_sys64(&L->inbox->tp_prop[r])) >> 32) < round) {
+          while (((w = ld_acquire_sys64(&L->inbox->tp_prop[par][r])) >> 32) != round) {
             if (*L->abort_flag) break;
             __nanosleep(32);
           }
           uint32_t code = (uint32_t)w;
           ds[r].kind = code & 3; ds[r].mb = (code >> 2) & 1023; ds[r].chunk = (code >> 12) & 15;
-          snap += L->inbox->tp_cnt[r];
+          snap += L->inbox->tp_cnt[par][r];
         }
         bool all_wait = true, all_w = true;
         for (int r = 0; r < R; ++r) {

@@ -92,7 +92,7 @@ class DistPipeline:
 
     def __init__(self, cfg, n_mb: int, *, hint="bf", buffer_limit=32, mode="free", jitter=None,
                  seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None,
-                 tp_size: int = 1, tp=None):
+                 tp_size: int = 1, tp=None, n_chunks: int = 1):
         import torch.distributed as dist
         from .arbitration import HintOrder, TpGroup
         from .model import StageCompute
@@ -102,27 +102,38 @@ class DistPipeline:
             hint = HintOrder.parse(hint)
         self.grank, self.gworld = dist.get_rank(group), dist.get_world_size(group)
         s, r, n = stage_coords(self.grank, self.gworld, tp_size)
-        R = tp_size
-        self.rank, self.world, self.tp_rank, self.R = s, n, r, R
+        R, C = tp_size, n_chunks
+        V = n * C
+        self.rank, self.world, self.tp_rank, self.R, self.C = s, n, r, R, C
         self.device = torch.cuda.current_device()
         decompose = hint.kind == "bfw"
         S, D = cfg.seq, cfg.d_model
         slot_bytes = n_mb * S * D * 2
-        self.bufs = {"fwd": IpcBuffer(slot_bytes, self.device) if s > 0 else None,
-                     "bwd": IpcBuffer(slot_bytes, self.device) if s < n - 1 else None}
-        fwd_in = wrap_bf16(self.bufs["fwd"].ptr.value, (n_mb, S, D), self.device) if s > 0 else None
-        bwd_in = wrap_bf16(self.bufs["bwd"].ptr.value, (n_mb, S, D), self.device) if s < n - 1 else None
+        # this lane hosts virtual stages v = c*N + s (chunk c), each with its own mailboxes
+        self.vids = [c * n + s for c in range(C)]
+        self.bufs = {}
+        for v in self.vids:
+            self.bufs[(v, "fwd")] = IpcBuffer(slot_bytes, self.device) if v > 0 else None
+            self.bufs[(v, "bwd")] = IpcBuffer(slot_bytes, self.device) if v < V - 1 else None
         self.comm = None
         if R > 1:
             from .tp import TpComm
             self.comm = TpComm(r, R, (S, D), torch.device("cuda", self.device))
-        self.stage = StageCompute(cfg, s, n, n_mb, torch.device("cuda", self.device),
-                                  decompose=decompose, seed=model_seed, data_seed=data_seed,
-                                  fwd_in=fwd_in, bwd_in=bwd_in, tp_rank=r, tp_size=R, tp=self.comm)
-        w = nominal_workload(cfg, n, n_mb, decompose, tp_size=R)
+        self.vstages = []
+        for v in self.vids:
+            fb, bb = self.bufs[(v, "fwd")], self.bufs[(v, "bwd")]
+            self.vstages.append(StageCompute(
+                cfg, v, V, n_mb, torch.device("cuda", self.device), decompose=decompose, seed=model_seed,
+                data_seed=data_seed,
+                fwd_in=wrap_bf16(fb.ptr.value, (n_mb, S, D), self.device) if fb else None,
+                bwd_in=wrap_bf16(bb.ptr.value, (n_mb, S, D), self.device) if bb else None,
+                tp_rank=r, tp_size=R, tp=self.comm))
+        # the lane's first / last virtual stages (loss lives on virtual stage V-1)
+        self.stage = self.vstages[-1] if self.vstages[-1].last else self.vstages[0]
+        w = nominal_workload(cfg, n, n_mb, decompose, tp_size=R, n_chunks=C)
         if comm_delay is not None:
             from .workload import Workload
-            w = Workload(num_stages=n, num_microbatches=n_mb, num_chunks=1, tp_group_size=R,
+            w = Workload(num_stages=n, num_microbatches=n_mb, num_chunks=C, tp_group_size=R,
                          latency=w.latency, comm_delay=comm_delay, decompose_backward=decompose)
         self.workload = w
         self.n_mb = n_mb
@@ -130,9 +141,9 @@ class DistPipeline:
                                tp=tp or (TpGroup(group_size=R) if R > 1 else None),
                                placement=[[self.device] * R for _ in range(n)], local=[(s, r)],
                                bodies=None, compute_kind=1, schedule=schedule, defer_bodies=True)
+        hd = lambda b: b.handle() if b else None
         mine = {"stage": s, "tp_rank": r,
-                "fwd": self.bufs["fwd"].handle() if self.bufs["fwd"] else None,
-                "bwd": self.bufs["bwd"].handle() if self.bufs["bwd"] else None,
+                "mbox": {v: (hd(self.bufs[(v, "fwd")]), hd(self.bufs[(v, "bwd")])) for v in self.vids},
                 "lane": self.group.ipc_handles()[(s, r)],
                 "tp": self.comm.ipc_handles() if self.comm else None}
         allh = [None] * self.gworld
@@ -140,23 +151,29 @@ class DistPipeline:
         by = {(h["stage"], h["tp_rank"]): h for h in allh}
         if self.comm:
             self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
-        peers = plan_peers(s, n, R)
-        fwd_out = bwd_out = None
-        if peers["writes_fwd_mailbox"]:
-            dst = [wrap_bf16(open_handle(by[(s + 1, q)]["fwd"]), (n_mb, S, D), self.device) for q in range(R)]
-            fwd_out = [[d[mb] for d in dst] for mb in range(n_mb)]
-        if peers["writes_bwd_mailbox"]:
-            dst = [wrap_bf16(open_handle(by[(s - 1, q)]["bwd"]), (n_mb, S, D), self.device) for q in range(R)]
-            bwd_out = [[d[mb] for d in dst] for mb in range(n_mb)]
-        self.stage.connect_outputs(fwd_out=fwd_out, bwd_out=bwd_out)
+
+        def mailboxes(v, which):   # virtual stage v's F (0) / B (1) mailbox on every TP rank
+            dst = [wrap_bf16(open_handle(by[(v % n, q)]["mbox"][v][which]), (n_mb, S, D), self.device)
+                   for q in range(R)]
+            return [[d[mb] for d in dst] for mb in range(n_mb)]
+
+        for st, v in zip(self.vstages, self.vids):
+            st.connect_outputs(fwd_out=mailboxes(v + 1, 0) if v + 1 < V else None,
+                               bwd_out=mailboxes(v - 1, 1) if v > 0 else None)
         # eager warm-up with rank-local all-reduces (module loading never races a spinning peer)
         if self.comm:
             self.comm.local_only = True
-        self.stage.warmup().synchronize()
+        for st in self.vstages:
+            st.warmup().synchronize()
         if self.comm:
             self.comm.local_only = False
-        raw = self.stage.capture()
-        self.group.set_bodies({(s, r): raw})
+        arr = [None] * (3 * n_mb * C)
+        for c, st in enumerate(self.vstages):
+            raw = st.capture()
+            for ki in range(3):
+                for mb in range(n_mb):
+                    arr[ki * n_mb * C + c * n_mb + mb] = raw[ki * n_mb + mb]
+        self.group.set_bodies({(s, r): arr})
         self.group.connect_ipc({(h["stage"], h["tp_rank"]): h["lane"] for h in allh})
         torch.cuda.synchronize()
         dist.barrier(group=group)
@@ -183,10 +200,11 @@ class DistPipeline:
         self.group.set_floor_us(floors)
 
     def kernel_launches_per_step(self):
-        return sum(self.stage.kernel_counts.values()) + 2 * len(self.stage.kernel_counts) + 2
+        return sum(sum(st.kernel_counts.values()) + 2 * len(st.kernel_counts) for st in self.vstages) + 2
 
     def step(self, watchdog_secs=120.0):
-        self.stage.zero_grads()
+        for st in self.vstages:
+            st.zero_grads()
         events, t0s = self.group.run_iteration(watchdog_secs)
         self.last_events = (events, min(t0s))
         if self.stage.last:
@@ -194,7 +212,8 @@ class DistPipeline:
         return None
 
     def launch(self):
-        self.stage.zero_grads()
+        for st in self.vstages:
+            st.zero_grads()
         self.group.launch()
 
     def wait(self, watchdog_secs=120.0):

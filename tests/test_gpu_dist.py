@@ -14,14 +14,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("hint,tp,nproc", [("bf", 1, 2), ("bfw", 1, 2), ("bf", 2, 2), ("bfw", 2, 4)])
-def test_multi_process_pipeline_matches_single_process(hint, tp, nproc):
-    """PP=2 (tp=1), TP=2 x PP=1 and TP=2 x PP=2: IPC mailboxes written by every
-    sender TP rank, peer-memory all-reduce between processes."""
+@pytest.mark.parametrize("hint,tp,nproc,chunks", [("bf", 1, 2, 1), ("bfw", 1, 2, 1), ("bf", 2, 2, 1),
+                                                  ("bfw", 2, 4, 1), ("bf", 1, 2, 2)])
+def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks):
+    """PP=2 (tp=1), TP=2 x PP=1, TP=2 x PP=2 and PP=2 x C=2 (chunk wrap across
+    processes): IPC mailboxes written by every sender TP rank, peer-memory
+    all-reduce between processes."""
     env = dict(os.environ, RRFP_SAME_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tools", "dist_check.py"),
-           hint, str(tp)]
+           hint, str(tp), str(chunks)]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     line = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]
@@ -32,5 +34,5 @@ def test_multi_process_pipeline_matches_single_process(hint, tp, nproc):
     for r in last:
         for l in r["losses"]:
             assert abs(l - ref) / ref < 1e-2, (l, ref)
-    per_stage = 4 * (3 if hint == "bfw" else 2)
+    per_stage = 4 * chunks * (3 if hint == "bfw" else 2)
     assert all(r["n_exec"] == per_stage and r["tp_err"] == 0 for r in res["ranks"])

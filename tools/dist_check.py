@@ -24,10 +24,15 @@ def main():
     cfg = GPTConfig(n_layer=4, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=256)
     hint = sys.argv[1] if len(sys.argv) > 1 else "bf"
     tp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp)
+    chunks = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks)
     losses = []
+    import time
+    wd = float(os.environ.get("RRFP_WATCHDOG", "60"))
     for _ in range(2):
-        loss = pipe.step(watchdog_secs=60)
+        t0 = time.time()
+        loss = pipe.step(watchdog_secs=wd)
+        print(f"[rank {rank}] step {time.time() - t0:.2f}s", file=sys.stderr, flush=True)
         dist.barrier()
         losses.append(None if loss is None else loss.item())
     ev, t0 = pipe.last_events
