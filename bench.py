@@ -308,21 +308,8 @@ def run_ours(args):
         t = torch.tensor([ms, e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_s = t[0].item(), t[1].item()
-    from paper_2605_18750_b200.runtime import wall_trace
-    ev, t0n = pipe.last_events
-    if dist:
-        allev = [None] * world
-        dist.all_gather_object(allev, ([(e.t0, e.t1, e.kind, e.stage, e.rank, e.task) for e in ev], t0n))
-        from paper_2605_18750_b200 import _lib
-        ev = []
-        for lst, _ in allev:
-            for t in lst:
-                x = _lib.Event()
-                x.t0, x.t1, x.kind, x.stage, x.rank, x.task = t
-                ev.append(x)
-        t0n = min(t for _, t in allev)
     _log("timed region done")
-    tr, met = wall_trace(pipe.workload, ev, t0n)
+    tr, met = gather_trace(pipe, dist, world)
     bubble = met.bubble_fraction()
     it_s = 1000.0 / ms
     tok = args.mb * cfg.seq
@@ -370,11 +357,10 @@ def run_ours(args):
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
-    nominal = {s_: {d: task_us[d][s_] for d in ("F", "B", "W")} for s_ in range(n)}
     pipe.close()
     del pipe, stages, first, last
     if args.compare or (world > 1 and args.compare is None):
-        line["variants"] = compare_variants(cfg, args, world, dist, barrier, nominal)
+        line["variants"] = compare_variants(cfg, args, world, dist, barrier)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -394,64 +380,91 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     return pipe, pipe.stages
 
 
-def compare_variants(cfg, args, world, dist, barrier, nominal):
-    """Same kernels, same box: fixed-order 1F1B vs RRFP (BF, BFW), without and
-    with injected lognormal compute + comm jitter (sigma = args.sigma, paired
-    draws keyed by task).  Each variant: build, calibrate, K timed steps."""
+def gather_trace(pipe, dist, world):
+    """Wall trace + metrics of the last iteration over every rank's device events."""
+    from paper_2605_18750_b200 import _lib
+    from paper_2605_18750_b200.runtime import wall_trace
+    ev, t0n = pipe.last_events
+    if dist:
+        allev = [None] * world
+        dist.all_gather_object(allev, ([(e.t0, e.t1, e.kind, e.stage, e.rank, e.task) for e in ev], t0n))
+        ev = []
+        for lst, _ in allev:
+            for t in lst:
+                x = _lib.Event()
+                x.t0, x.t1, x.kind, x.stage, x.rank, x.task = t
+                ev.append(x)
+        t0n = min(t for _, t in allev)
+    return wall_trace(pipe.workload, ev, t0n)
+
+
+def timed_steps(pipe, steps, dist, barrier):
+    """K iterations between CUDA events on the lane stream; max over ranks (ms/step)."""
+    import torch
+    lane_stream = pipe.group.streams[next(iter(pipe.group.streams))]
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(lane_stream)
+    for _ in range(steps):
+        pipe.launch()
+        pipe.wait()
+    e1.record(lane_stream)
+    barrier()
+    ms = e0.elapsed_time(e1) / steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    return ms
+
+
+def compare_variants(cfg, args, world, dist, barrier):
+    """Same kernels, same box: fixed-order 1F1B vs RRFP (BF, BFW) under the
+    J-preset jitter table (--compare-jitter) and injected lognormal compute +
+    comm jitter for every sigma of --sigmas (config 5's sweep; draws keyed by
+    task / edge, so every variant sees identical perturbations).  One build per
+    variant; per sigma: new floor + comm tables, one warm step, K device-timed
+    steps.  Nominal task times = the variant's own clean (sigma 0) iteration."""
     import gc
     import math
     import torch
     from paper_2605_18750_b200.jitter import PRESETS
     from paper_2605_18750_b200.workload import CommDelay
     out = {}
-    sigmas = [0.0] + ([args.sigma] if args.sigma > 0 else [])
-    for sigma in sigmas:
-        comm = None
-        if sigma > 0:
-            comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
-                             hi=int(args.comm_us * 50), seed=17)
-        for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
-            if name == "1f1b" and args.chunks > 1:
-                continue          # 1F1B is undefined for interleaved chunks (baselines.py:72-75)
-            if world == 1 and name == "bfw" and cfg.n_layer * args.mb > 8 * 32:
-                continue          # PP=1 BFW keeps every W pending: memory-bound, meaningless
-            pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS["J0"], comm)
-            for _ in range(2):
-                pipe.step()
+    sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
+    jit = PRESETS[args.compare_jitter]
+    for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
+        if name == "1f1b" and args.chunks > 1:
+            continue          # 1F1B is undefined for interleaved chunks (baselines.py:72-75)
+        if world == 1 and name == "bfw" and cfg.n_layer * args.mb > 8 * 32:
+            continue          # PP=1 BFW keeps every W pending: memory-bound, meaningless
+        pipe, stages = build_pipe(cfg, args, hint, mode, world, jit)
+        for _ in range(2):
+            pipe.step()
+        nominal = pipe.nominal_us()
+        for sigma in sigmas:
+            comm = CommDelay()
             if sigma > 0:
-                if world > 1:
-                    pipe.set_lognormal_jitter(sigma, seed=11)
-                else:
-                    pipe.set_lognormal_jitter(sigma, seed=11)
-                pipe.step()
-            barrier()
-            t0 = time.perf_counter()
-            for _ in range(args.steps):
-                pipe.launch()
-                pipe.wait()
-            barrier()
-            ms = (time.perf_counter() - t0) * 1e3 / args.steps
-            if dist:
-                t = torch.tensor([ms], dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = t.item()
-            from paper_2605_18750_b200.runtime import wall_trace
-            ev, t0n = pipe.last_events
-            bub = None
-            if not dist:
-                tr, met = wall_trace(pipe.workload, ev, t0n)
-                bub = round(met.bubble_fraction(), 4)
-            out[f"{name}@sigma{sigma}"] = {"iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
-                                           "bubble_fraction": bub}
-            pipe.close()
-            del pipe, stages
-            gc.collect()
-            torch.cuda.empty_cache()
-            _log(f"variant {name} sigma={sigma}: {ms:.1f} ms")
-        base = out.get(f"1f1b@sigma{sigma}")
+                comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
+                                 hi=int(args.comm_us * 50), seed=17)
+            pipe.group.set_comm_delay(comm)
+            pipe.set_lognormal_jitter(sigma, seed=11, nominal_us=nominal)
+            pipe.step()
+            ms = timed_steps(pipe, args.steps, dist, barrier)
+            tr, met = gather_trace(pipe, dist, world)
+            out[f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
+                "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
+                "bubble_fraction": round(met.bubble_fraction(), 4)}
+            _log(f"variant {name} {args.compare_jitter} sigma={sigma}: {ms:.1f} ms")
+        pipe.close()
+        del pipe, stages
+        gc.collect()
+        torch.cuda.empty_cache()
+    for sigma in sigmas:
+        base = out.get(f"1f1b@{args.compare_jitter}+sigma{sigma}")
         if base:
             for name in ("bf", "bfw"):
-                v = out.get(f"{name}@sigma{sigma}")
+                v = out.get(f"{name}@{args.compare_jitter}+sigma{sigma}")
                 if v:
                     v["speedup_vs_1f1b"] = round(base["ms"] / v["ms"], 4)
     return out
@@ -501,8 +514,11 @@ def main():
     ap.add_argument("--compare", dest="compare", action="store_true", default=None,
                     help="also time fixed 1F1B / BF / BFW (default on for N>1)")
     ap.add_argument("--no-compare", dest="compare", action="store_false")
-    ap.add_argument("--sigma", type=float, default=0.5,
-                    help="lognormal compute+comm jitter sigma of the comparison runs")
+    ap.add_argument("--sigmas", default="0.5",
+                    help="comma list of lognormal compute+comm jitter sigmas of the comparison runs "
+                         "(config 5 sweep: 0,0.1,0.2,0.3,0.4,0.5); sigma 0 is always included")
+    ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0",
+                    help="J-preset jitter table (jitter.py PRESETS) applied to every comparison variant")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     args = ap.parse_args()
     if args.impl == "reference":

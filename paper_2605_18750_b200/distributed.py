@@ -181,6 +181,19 @@ class DistPipeline:
         self.group.prepare()
         dist.barrier(group=group)
 
+    def nominal_us(self, group=None):
+        """Per-stage mean F/B/W durations (µs) of the last iteration, gathered
+        from TP rank 0 of every stage (collective: call on every rank)."""
+        import torch.distributed as dist
+        ev, _ = self.last_events
+        mine = {}
+        for d, code in (("F", 1), ("B", 0), ("W", 2)):
+            xs = [e.t1 - e.t0 for e in ev if e.kind == 0 and (e.task & 3) == code]
+            mine[d] = (sum(xs) / len(xs) / 1000.0) if xs else 0.0
+        allv = [None] * self.gworld
+        dist.all_gather_object(allv, mine, group=group)
+        return allv[::self.R]
+
     def set_lognormal_jitter(self, sigma: float, seed: int = 0, nominal_us=None, group=None):
         """Lognormal compute jitter floors for THIS rank's stage; nominal task
         times are gathered from every rank's last iteration."""

@@ -191,6 +191,11 @@ class GpuPipeline:
         self.last_events = (events, min(t0s))
         return events
 
+    def nominal_us(self):
+        """Per-stage mean F/B/W durations (µs) of the last iteration."""
+        tr, _ = self.trace()
+        return measured_nominal(tr, self.N)
+
     def set_lognormal_jitter(self, sigma: float, seed: int = 0, nominal_us=None):
         """Enable injected lognormal compute jitter; nominal task times default
         to the last iteration's measured means (call after a clean step)."""

@@ -88,6 +88,7 @@ class LaneGroup:
             order = replay_order(workload, hint, buffer_limit, seed, jitter, tp)
         tb = lower(workload, hint, buffer_limit, seed, jitter, tp)
         self.tables = tb
+        self._seed, self._jitter, self._tp = seed, jitter, tp
         self.injected = tb.injected
         placement = placement or [[0] * r for _ in range(n)]
         self.local = local or [(s, k) for s in range(n) for k in range(r)]
@@ -169,6 +170,21 @@ class LaneGroup:
             self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
                                                       _ptr(fixed), _ptr(floor)))
+
+    def set_comm_delay(self, comm_delay):
+        """Replace the per-edge communication delays (e.g. a lognormal CommDelay
+        of another sigma, config 5) between iterations: the edge table is
+        re-lowered exactly as at construction (workload.py:109-117 draws)."""
+        from dataclasses import replace
+        w = replace(self.w, comm_delay=comm_delay)
+        tb = lower(w, self.hint, self.tables.desc.buffer_limit, self._seed, self._jitter, self._tp)
+        for (s, k), h in self.lanes.items():
+            dur, _, dskew, fixed, floor = self._tables[(s, k)]
+            comm = np.ascontiguousarray(np.rint(tb.comm[s] * 1000.0 * self.scale).astype(np.int64))
+            self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
+            _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew), _ptr(fixed),
+                                                      _ptr(floor) if floor is not None else None))
+        self.w = w
 
     def set_bodies(self, bodies: dict):
         for lane, arr in bodies.items():
