@@ -349,10 +349,14 @@ __global__ void copy_rows_kernel(char* __restrict__ dst, long long ldd, const ch
 }  // namespace
 
 #define LAUNCH_NV(KERNEL, D, ...)                                                          \
+  if ((D) % 256) return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d not a multiple of 256", (int)(D)); \
   switch ((D) / 256) {                                                                     \
     case 1: RRFP_CUDA_TRY(rrfp_launch(KERNEL<1>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     case 2: RRFP_CUDA_TRY(rrfp_launch(KERNEL<2>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 3: RRFP_CUDA_TRY(rrfp_launch(KERNEL<3>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     case 4: RRFP_CUDA_TRY(rrfp_launch(KERNEL<4>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 5: RRFP_CUDA_TRY(rrfp_launch(KERNEL<5>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
+    case 6: RRFP_CUDA_TRY(rrfp_launch(KERNEL<6>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     case 8: RRFP_CUDA_TRY(rrfp_launch(KERNEL<8>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     case 16: RRFP_CUDA_TRY(rrfp_launch(KERNEL<16>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
     default: return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported", (int)(D)); \

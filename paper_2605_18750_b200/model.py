@@ -41,6 +41,7 @@ class GPTConfig:
     seq: int = 2048
     eps: float = 1e-5
     init_std: float = 0.02
+    causal: bool = True          # False: bidirectional attention (the ViT encoder of config 4)
 
     @property
     def d_head(self):
@@ -59,6 +60,53 @@ class GPTConfig:
 
 GPT_1P3B = GPTConfig()
 GPT_7B = GPTConfig(n_layer=32, d_model=4096, n_head=32, d_ff=16384)
+VIT_H14 = GPTConfig(n_layer=32, d_model=1280, n_head=16, d_ff=5120, vocab=0, seq=2048, causal=False)
+
+
+@dataclass(frozen=True)
+class MultimodalSpec:
+    """BASELINE config 4: a ViT encoder on the leading ``vit_stages`` pipeline
+    stages feeding a GPT LLM.  Microbatch mb carries n_img(mb) ~ U{1..max_images}
+    images (seeded, rng.substream(image_seed, "images", mb)), i.e. T_v(mb) =
+    patch_tokens * n_img(mb) visual tokens: the ViT stages' work and their
+    messages are input-dependent.  The LLM sequence is [projected visual
+    tokens (T_v rows), text tokens (seq - T_v rows)]; loss over all positions.
+    Patches are synthetic bf16 features [T_v, d_patch] (no pixels / network)."""
+    vit: GPTConfig = VIT_H14
+    llm: GPTConfig = GPT_7B
+    vit_stages: int = 1
+    patch_tokens: int = 256
+    d_patch: int = 768
+    max_images: int = 8
+    image_seed: int = 0
+
+    def images(self, n_mb: int):
+        from .rng import substream
+        return [int(substream(self.image_seed, "images", mb).integers(1, self.max_images + 1))
+                for mb in range(n_mb)]
+
+    def visual_tokens(self, n_mb: int):
+        out = [self.patch_tokens * n for n in self.images(n_mb)]
+        if max(out) > self.llm.seq or self.patch_tokens * self.max_images > self.vit.seq:
+            raise ValueError("visual tokens exceed the sequence length")
+        return out
+
+
+def init_mm_params(spec: MultimodalSpec, device, seed: int, which: str):
+    """Patch embedding ('pe': [d_vit, d_patch]) or projector ('proj': [d_llm, d_vit])."""
+    g = _gen(device, seed * 100003 + (55551 if which == "pe" else 55553))
+    bf = torch.bfloat16
+    dv, dl = spec.vit.d_model, spec.llm.d_model
+    if which == "pe":
+        return {"w_pe": (torch.randn(dv, spec.d_patch, generator=g, device=device) * 0.02).to(bf),
+                "b_pe": (torch.randn(dv, generator=g, device=device) * 0.02).to(bf)}
+    return {"w_proj": (torch.randn(dl, dv, generator=g, device=device) * 0.02).to(bf),
+            "b_proj": (torch.randn(dl, generator=g, device=device) * 0.02).to(bf)}
+
+
+def synthetic_patches(spec: MultimodalSpec, n_mb: int, seed: int, device):
+    g = _gen(device, seed * 7919 + 3)
+    return (torch.randn(n_mb, spec.vit.seq, spec.d_patch, generator=g, device=device)).to(torch.bfloat16)
 
 
 def split_layers(n_layer: int, n_stages: int, stage: int):
@@ -186,13 +234,35 @@ class RawBuffer:
 class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
                  decompose: bool = False, seed: int = 1234, data_seed: int = 0,
-                 fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None):
+                 fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None,
+                 mm: MultimodalSpec | None = None):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
-        self.first, self.last = stage == 0, stage == n_stages - 1
         self.decompose = decompose
-        self.layers = split_layers(cfg.n_layer, n_stages, stage)
+        self.mm = mm
+        # which part of the model this stage holds (config 4: ViT stages, then LLM stages)
+        if mm is not None:
+            nv = mm.vit_stages
+            part, idx, cnt = ("vit", stage, nv) if stage < nv else ("llm", stage - nv, n_stages - nv)
+            if cfg != (mm.vit if part == "vit" else mm.llm):
+                raise ValueError(f"stage {stage} ({part}) needs cfg = mm.{part}")
+            if tp_size > 1:
+                raise ValueError("the multimodal path has no TP split")
+        else:
+            part, idx, cnt = "gpt", stage, n_stages
+        self.part = part
+        self.layers = split_layers(cfg.n_layer, cnt, idx)
+        # prologue: token embedding (GPT stage 0), patch embedding (ViT stage 0), or
+        # merge (first LLM stage: projected visual rows arrive in the mailbox, text
+        # rows are embedded here); epilogue: LM head + loss, or the ViT projector
+        self.prologue = {"gpt": "tokens", "vit": "patches", "llm": "merge"}[part] if idx == 0 else None
+        self.epilogue = ("projector" if part == "vit" else "head") if idx == cnt - 1 else None
+        self.first = self.prologue in ("tokens", "patches")
+        self.last = self.epilogue == "head"
         S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
+        self.T_v = mm.visual_tokens(n_mb) if mm is not None else None
+        # rows each microbatch occupies in this stage's layers (ViT: its visual tokens)
+        self.rows = list(self.T_v) if part == "vit" else [S] * n_mb
         if cfg.n_head % tp_size or Fd % tp_size:
             raise ValueError(f"TP size {tp_size} must divide n_head and d_ff")
         if tp_size > 1 and tp is None:
@@ -203,24 +273,35 @@ class StageCompute:
         self.Hl, self.Dl, self.Fl = cfg.n_head // tp_size, D // tp_size, Fd // tp_size
         Dl, Fl = self.Dl, self.Fl
         dev, bf = self.device, torch.bfloat16
+        lseed = seed + 17 if part == "vit" else seed      # ViT layers: their own init stream
+        self.layer_seed = lseed
         with torch.no_grad():
-            self.p = [shard_layer_params(cfg, init_layer_params(cfg, l, dev, seed), tp_rank, tp_size)
+            self.p = [shard_layer_params(cfg, init_layer_params(cfg, l, dev, lseed), tp_rank, tp_size)
                       for l in self.layers]
-            self.emb = init_embed_params(cfg, dev, seed) if self.first else None
+            self.emb = init_embed_params(cfg, dev, seed) if self.prologue in ("tokens", "merge") else None
             self.head = init_head_params(cfg, dev, seed) if self.last else None
-        self.g = [{k: torch.zeros(v.shape, device=dev) for k, v in p.items()} for p in self.p]
-        self.g_emb = {k: torch.zeros(v.shape, device=dev) for k, v in self.emb.items()} if self.first else None
-        self.g_head = {k: torch.zeros(v.shape, device=dev) for k, v in self.head.items()} if self.last else None
-        # synthetic data (stage 0 reads tokens, last stage reads targets)
-        toks, tgts = synthetic_batch(cfg, n_mb, data_seed, dev)
-        self.tokens = toks if self.first else None
-        self.targets = tgts if self.last else None
+            self.pe = init_mm_params(mm, dev, seed, "pe") if self.prologue == "patches" else None
+            self.proj = init_mm_params(mm, dev, seed, "proj") if self.epilogue == "projector" else None
+        zeros = lambda d: {k: torch.zeros(v.shape, device=dev) for k, v in d.items()} if d else None
+        self.g = [zeros(p) for p in self.p]
+        self.g_emb, self.g_head = zeros(self.emb), zeros(self.head)
+        self.g_pe, self.g_proj = zeros(self.pe), zeros(self.proj)
+        # synthetic data (tokens where the sequence starts, targets at the loss, patches for the ViT)
+        if part != "vit":
+            toks, tgts = synthetic_batch(cfg, n_mb, data_seed, dev)
+            self.tokens = toks if self.prologue in ("tokens", "merge") else None
+            self.targets = tgts if self.last else None
+        else:
+            self.tokens = self.targets = None
+        self.patches = synthetic_patches(mm, n_mb, data_seed, dev) if self.prologue == "patches" else None
         # mailboxes written by neighbours: F input (stage > 0), B input (stage < N-1)
-        # (the caller may pass IPC-exportable buffers, distributed.py)
+        # (the caller may pass IPC-exportable buffers, distributed.py); the ViT
+        # projector stage receives the gradient of its [T_v, d_llm] output
         if fwd_in is None and not self.first:
             fwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf)
         if bwd_in is None and not self.last:
-            bwd_in = torch.empty(n_mb, S, D, device=dev, dtype=bf)
+            bw = mm.llm.d_model if self.epilogue == "projector" else D
+            bwd_in = torch.empty(n_mb, S, bw, device=dev, dtype=bf)
         self.fwd_in, self.bwd_in = fwd_in, bwd_in
         self.fwd_out = None   # per-mb destination buffers (set by connect_outputs)
         self.bwd_out = None
@@ -253,9 +334,8 @@ class StageCompute:
         self.side = torch.cuda.Stream(dev)
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
             self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl)
+            self.gx0 = e(n_mb, S, D) if self.prologue else None
             self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl)
-            if self.first:
-                self.gx0 = e(n_mb, S, D)
         self.graphs = {}
         self.kernel_counts = {}   # (kind, mb) -> our kernel launches in that body
 
@@ -274,54 +354,66 @@ class StageCompute:
 
     # ------------------------------------------------------------ forward
     def _attn_fwd(self, qkv, mb, li):
-        S, H, Dh, D = self.cfg.seq, self.Hl, self.cfg.d_head, self.Dl
-        q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
-        k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
-        v = qkv[:, 2 * D:].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        T, H, Dh, D = qkv.shape[0], self.Hl, self.cfg.d_head, self.Dl
+        q = qkv[:, :D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
+        k = qkv[:, D:2 * D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
+        v = qkv[:, 2 * D:].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         out = torch.ops.aten._scaled_dot_product_cudnn_attention(
-            q, k, v, None, True, 0.0, True, False, scale=1.0 / math.sqrt(Dh))
+            q, k, v, None, True, 0.0, self.cfg.causal, False, scale=1.0 / math.sqrt(Dh))
         o4, lse = out[0], out[1]
         self.attn_aux[mb][li] = (o4, lse, out[2], out[3], out[4], out[5], out[6], out[7])
         o_sd = o4[0].transpose(0, 1)
-        if o_sd.is_contiguous():          # cuDNN writes BSHD: use it in place as [S, D]
-            self.o_view[mb][li] = o_sd.reshape(S, D)
+        if o_sd.is_contiguous():          # cuDNN writes BSHD: use it in place as [T, D]
+            self.o_view[mb][li] = o_sd.reshape(T, D)
         else:
-            o = torch.empty(S, D, device=self.device, dtype=torch.bfloat16)
-            o.view(S, H, Dh).copy_(o_sd)
+            o = torch.empty(T, D, device=self.device, dtype=torch.bfloat16)
+            o.view(T, H, Dh).copy_(o_sd)
             self.o_view[mb][li] = o
+
+    def _text_rows(self, mb):
+        """First text row of microbatch mb in the LLM sequence (after its visual tokens)."""
+        return self.T_v[mb] if self.prologue == "merge" else 0
 
     def forward(self, mb: int):
         cfg = self.cfg
         S, D = cfg.seq, cfg.d_model
-        if self.first:
+        T = self.rows[mb]
+        if self.prologue == "tokens":
             K.note()
             _lib.check(_lib.lib().rrfp_embedding_fwd(
                 K._p(self.tokens[mb]), K._p(self.emb["wte"]), K._p(self.emb["wpe"]),
                 K._p(self.x0[mb]), S, D, K._stream()))
             x = self.x0[mb]
+        elif self.prologue == "patches":   # ViT patch embedding of this microbatch's images
+            x = self.x0[mb, :T]
+            K.gemm(self.patches[mb, :T], self.pe["w_pe"], x, bias=self.pe["b_pe"])
         else:
-            x = self.fwd_in[mb]
-        nl = len(self.layers)
+            x = self.fwd_in[mb][:T]
+            t0 = self._text_rows(mb)
+            if self.prologue == "merge" and t0 < S:   # text rows after the projected visual rows
+                K.note()
+                _lib.check(_lib.lib().rrfp_embedding_fwd(
+                    K._p(self.tokens[mb, t0:]), K._p(self.emb["wte"]), K._p(self.emb["wpe"][t0:]),
+                    K._p(x[t0:]), S - t0, D, K._stream()))
         for li, p in enumerate(self.p):
-            _ln_fwd(x, p["ln1_g"], p["ln1_b"], self.h1[mb, li], self.m1[mb, li], self.r1[mb, li], cfg.eps)
-            K.gemm(self.h1[mb, li], p["w_qkv"], self.qkv[mb, li], bias=p["b_qkv"])
-            self._attn_fwd(self.qkv[mb, li], mb, li)
+            h1, qkv, x2 = self.h1[mb, li, :T], self.qkv[mb, li, :T], self.x2[mb, li, :T]
+            h2, pre, act = self.h2[mb, li, :T], self.pre[mb, li, :T], self.act[mb, li, :T]
+            _ln_fwd(x, p["ln1_g"], p["ln1_b"], h1, self.m1[mb, li, :T], self.r1[mb, li, :T], cfg.eps)
+            K.gemm(h1, p["w_qkv"], qkv, bias=p["b_qkv"])
+            self._attn_fwd(qkv, mb, li)
             if self.R == 1:
-                K.gemm(self.o_view[mb][li], p["w_o"], self.x2[mb, li], epi=K.EPI_RESID, bias=p["b_o"], r=x)
+                K.gemm(self.o_view[mb][li], p["w_o"], x2, epi=K.EPI_RESID, bias=p["b_o"], r=x)
             else:   # row-parallel: partial sum, then all-reduce (+ b_o + residual) over the TP group
                 K.gemm(self.o_view[mb][li], p["w_o"], self.tp.partial, m=S, n=D, k=self.Dl)
-                self.tp.allreduce([self.x2[mb, li]], bias=p["b_o"], resid=x)
-            _ln_fwd(self.x2[mb, li], p["ln2_g"], p["ln2_b"], self.h2[mb, li], self.m2[mb, li],
-                    self.r2[mb, li], cfg.eps)
-            K.gemm(self.h2[mb, li], p["w_1"], self.pre[mb, li], epi=K.EPI_BIAS_GELU,
-                   c2=self.act[mb, li], bias=p["b_1"])
-            outs = self._layer_output(mb, li)   # last layer: the next stage's mailbox slot(s)
+                self.tp.allreduce([x2], bias=p["b_o"], resid=x)
+            _ln_fwd(x2, p["ln2_g"], p["ln2_b"], h2, self.m2[mb, li, :T], self.r2[mb, li, :T], cfg.eps)
+            K.gemm(h2, p["w_1"], pre, epi=K.EPI_BIAS_GELU, c2=act, bias=p["b_1"])
+            outs = [o[:T] for o in self._layer_output(mb, li)]   # last layer: next stage's mailbox
             if self.R == 1:
-                K.gemm(self.act[mb, li], p["w_2"], outs[0], epi=K.EPI_RESID, bias=p["b_2"],
-                       r=self.x2[mb, li], m=S, n=D, k=self.Fl)
+                K.gemm(act, p["w_2"], outs[0], epi=K.EPI_RESID, bias=p["b_2"], r=x2, m=T, n=D, k=self.Fl)
             else:
-                K.gemm(self.act[mb, li], p["w_2"], self.tp.partial, m=S, n=D, k=self.Fl)
-                self.tp.allreduce(outs, bias=p["b_2"], resid=self.x2[mb, li])
+                K.gemm(act, p["w_2"], self.tp.partial, m=S, n=D, k=self.Fl)
+                self.tp.allreduce(outs, bias=p["b_2"], resid=x2)
             x = outs[0]
         if self.last:
             h = self.head
@@ -331,16 +423,21 @@ class StageCompute:
             _lib.check(_lib.lib().rrfp_xent_fwd(
                 K._p(self.logits[mb]), C.c_longlong(cfg.vocab), K._p(self.targets[mb]), S,
                 cfg.vocab, K._p(self.loss[mb]), K._p(self.lse[mb]), K._stream()))
+        elif self.epilogue == "projector":   # [T_v, d_vit] -> [T_v, d_llm] rows of the LLM mailbox
+            for dst in self.fwd_out[mb]:
+                K.gemm(x, self.proj["w_proj"], dst[:T], bias=self.proj["b_proj"])
 
     def _layer_input(self, mb, li):
+        T = self.rows[mb]
         if li > 0:
-            return self.y[mb, li - 1]
-        return self.x0[mb] if self.first else self.fwd_in[mb]
+            return self.y[mb, li - 1, :T]
+        return self.x0[mb, :T] if self.first else self.fwd_in[mb][:T]
 
     def _layer_output(self, mb, li):
         """Destination list of layer li's output (the next stage's mailbox slot of
         every receiving TP rank for the last layer; first entry is read back)."""
-        if li == len(self.layers) - 1 and not self.last and self.fwd_out is not None:
+        if (li == len(self.layers) - 1 and not self.last and self.epilogue != "projector"
+                and self.fwd_out is not None):
             outs = list(self.fwd_out[mb])
             if len(outs) > 1 and self.R == 1:
                 raise ValueError("a TP=1 stage feeds a TP>1 stage: not supported")
@@ -360,6 +457,7 @@ class StageCompute:
         """
         cfg = self.cfg
         S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
+        T = self.rows[mb]
         dec = self.decompose
         fused_w = not dec
         nl = len(self.layers)
@@ -381,7 +479,7 @@ class StageCompute:
                 fn()
 
         def dy_buf(li):           # where layer li reads its output gradient
-            return self.gy[mb, li] if dec else self.sd_a[li % 2]
+            return (self.gy[mb, li] if dec else self.sd_a[li % 2])[:T]
 
         if self.last:
             h, gh = self.head, self.g_head
@@ -397,116 +495,150 @@ class StageCompute:
             dy = dy_buf(nl - 1)
             _ln_bwd(self.d_head, self.y[mb, nl - 1], self.mf[mb], self.rf[mb], h["lnf_g"], None, dy,
                     gh["lnf_g"], gh["lnf_b"])
+        elif self.epilogue == "projector":
+            # gradient of the projected visual rows -> ViT output gradient (+ projector grads)
+            dyp, pj, gp = self.bwd_in[mb][:T], self.proj, self.g_proj
+            if fused_w:
+                yl = self.y[mb, nl - 1, :T]
+                on_side(ev(), lambda: (K.gemm(dyp, yl, gp["w_proj"], epi=K.EPI_ACC_F32, a_mn=True,
+                                              b_mn=True, accumulate=True, m=dyp.shape[1], n=D, k=T),
+                                       _bias_grad(dyp, gp["b_proj"])))
+            dy = dy_buf(nl - 1)
+            K.gemm(dyp, pj["w_proj"], dy, b_mn=True, m=T, n=D, k=dyp.shape[1])
         else:
-            dy = self.bwd_in[mb]
+            dy = self.bwd_in[mb][:T]
             if dec:
-                self.gy[mb, nl - 1].copy_(dy)
-                dy = self.gy[mb, nl - 1]
-        S_, Dl, Fl = S, self.Dl, self.Fl
+                self.gy[mb, nl - 1, :T].copy_(dy)
+                dy = self.gy[mb, nl - 1, :T]
+        Dl, Fl = self.Dl, self.Fl
+        d_head = self.d_head[:T]
         for li in reversed(range(nl)):
             p, g = self.p[li], self.g[li]
             x = self._layer_input(mb, li)
+            h1, x2, h2 = self.h1[mb, li, :T], self.x2[mb, li, :T], self.h2[mb, li, :T]
+            pre, act = self.pre[mb, li, :T], self.act[mb, li, :T]
             q = li % 2
             if li + 2 in side_done:          # set q was last read by layer li+2's side work
                 main.wait_event(side_done[li + 2])
-            d_pre = self.gpre[mb, li] if dec else self.sd_big[q]
-            d_x2 = self.gx2[mb, li] if dec else self.sd_b[q]
-            d_qkv = self.gqkv[mb, li] if dec else self.sd_qkv[q]
+            d_pre = (self.gpre[mb, li] if dec else self.sd_big[q])[:T]
+            d_x2 = (self.gx2[mb, li] if dec else self.sd_b[q])[:T]
+            d_qkv = (self.gqkv[mb, li] if dec else self.sd_qkv[q])[:T]
             if fused_w:
                 dyy = dy
-                on_side(ev(), lambda: (K.gemm(dyy, self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=S_),
+                on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=T),
                                        _bias_grad(dyy, g["b_2"])))
             # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
-            K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=self.pre[mb, li],
-                   m=S_, n=Fl, k=D)
+            K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D)
             if fused_w:
-                on_side(ev(), lambda: (K.gemm(d_pre, self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=S_),
+                on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
                                        _bias_grad(d_pre, g["b_1"])))
             # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy)
-            self._dgrad_reduce(d_pre, p["w_1"], Fl)
-            _ln_bwd(self.d_head, self.x2[mb, li], self.m2[mb, li], self.r2[mb, li], p["ln2_g"], dy,
+            self._dgrad_reduce(d_pre, p["w_1"], Fl, T)
+            _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
                     d_x2, g["ln2_g"], g["ln2_b"])
             if fused_w:
-                on_side(ev(), lambda: (K.gemm(d_x2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=S_),
+                ov = self.o_view[mb][li]
+                on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
                                        _bias_grad(d_x2, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
-            d_o = self.d_head if self.R == 1 else self.d_o
-            K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=S_, n=Dl, k=D)
+            d_o = d_head if self.R == 1 else self.d_o
+            K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=T, n=Dl, k=D)
             self._attn_bwd(mb, li, d_o, d_qkv)
             if fused_w:
-                def qkv_w(d_qkv=d_qkv, li=li, g=g):
-                    K.gemm(d_qkv, self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                           b_mn=True, accumulate=True, m=3 * Dl, n=D, k=S_)
+                def qkv_w(d_qkv=d_qkv, h1=h1, g=g):
+                    K.gemm(d_qkv, h1, g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
                     _bias_grad(d_qkv, g["b_qkv"])
                 on_side(ev(), qkv_w)
                 done = torch.cuda.Event()
                 done.record(side)
                 side_done[li] = done
-            self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl)
+            self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             extra = []
             if li > 0:
                 dx = dy_buf(li - 1)
                 if fused_w and li + 1 in side_done:   # layer li+1's side work read this buffer
                     main.wait_event(side_done[li + 1])
-            elif not self.first:
+            elif self.prologue is None:
                 if self.bwd_out is not None:
-                    dx, extra = self.bwd_out[mb][0], self.bwd_out[mb][1:]
+                    dx, extra = self.bwd_out[mb][0][:T], [o[:T] for o in self.bwd_out[mb][1:]]
                 else:
-                    dx = self.sd_a[1]
-            else:
-                dx = self.gx0[mb] if dec else self.sd_a[1]
+                    dx = self.sd_a[1][:T]
+            else:   # prologue stages keep the input gradient for the embedding backward
+                dx = (self.gx0[mb] if dec else self.sd_a[1])[:T]
                 if fused_w and 1 in side_done:
                     main.wait_event(side_done[1])
-            _ln_bwd(self.d_head, x, self.m1[mb, li], self.r1[mb, li], p["ln1_g"], d_x2, dx,
+            _ln_bwd(d_head, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
                     g["ln1_g"], g["ln1_b"])
             for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
-                _copy_rows(dst, dx, S, D)
+                _copy_rows(dst, dx, T, D)
             dy = dx
-        if self.first and fused_w:
+        if self.prologue == "merge":   # visual rows' gradient -> the ViT projector stage
+            t0 = self._text_rows(mb)
+            if self.bwd_out is not None:
+                for dst in self.bwd_out[mb]:
+                    _copy_rows(dst[:t0], dy[:t0], t0, D)
+        if self.prologue and fused_w:
             dyy = dy
-            on_side(ev(), lambda: (K.note(), _lib.check(_lib.lib().rrfp_embedding_bwd(
-                K._p(self.tokens[mb]), K._p(dyy), K._p(self.g_emb["wte"]), K._p(self.g_emb["wpe"]),
-                S, D, K._stream()))))
+            on_side(ev(), lambda: self._prologue_wgrad(mb, dyy))
         if fused_w:
             join = torch.cuda.Event()
             join.record(side)
             main.wait_event(join)
 
-    def _dgrad_reduce(self, d_col, w, k):
+    def _prologue_wgrad(self, mb, dx):
+        """Parameter gradients of the stage prologue from the input gradient dx."""
+        S, D = self.cfg.seq, self.cfg.d_model
+        T = self.rows[mb]
+        if self.prologue == "patches":
+            K.gemm(dx, self.patches[mb, :T], self.g_pe["w_pe"], epi=K.EPI_ACC_F32, a_mn=True, b_mn=True,
+                   accumulate=True, m=D, n=self.mm.d_patch, k=T)
+            _bias_grad(dx, self.g_pe["b_pe"])
+            return
+        t0 = self._text_rows(mb)
+        if t0 >= S:
+            return
+        K.note()
+        _lib.check(_lib.lib().rrfp_embedding_bwd(
+            K._p(self.tokens[mb, t0:]), K._p(dx[t0:]), K._p(self.g_emb["wte"]),
+            K._p(self.g_emb["wpe"][t0:]), S - t0, D, K._stream()))
+
+    def _dgrad_reduce(self, d_col, w, k, T=None):
         """Input gradient of a column-parallel layer into self.d_head: d_col . W
         (K = this rank's columns); under TP a partial sum all-reduced over the group."""
         S, D = self.cfg.seq, self.cfg.d_model
+        T = S if T is None else T
         if self.R == 1:
-            K.gemm(d_col, w, self.d_head, b_mn=True, m=S, n=D, k=k)
+            K.gemm(d_col, w, self.d_head[:T], b_mn=True, m=T, n=D, k=k)
         else:
             K.gemm(d_col, w, self.tp.partial, b_mn=True, m=S, n=D, k=k)
             self.tp.allreduce([self.d_head])
 
     def _attn_bwd(self, mb, li, d_o, d_qkv):
         cfg = self.cfg
-        S, H, Dh, D = cfg.seq, self.Hl, cfg.d_head, self.Dl
-        qkv = self.qkv[mb, li]
-        q = qkv[:, :D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
-        k = qkv[:, D:2 * D].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
-        v = qkv[:, 2 * D:].view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        T, H, Dh, D = d_qkv.shape[0], self.Hl, cfg.d_head, self.Dl
+        qkv = self.qkv[mb, li, :T]
+        q = qkv[:, :D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
+        k = qkv[:, D:2 * D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
+        v = qkv[:, 2 * D:].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         o4, lse, cq, ck, mq, mk, ps, po = self.attn_aux[mb][li]
-        go = d_o.view(S, H, Dh).transpose(0, 1).unsqueeze(0)
+        go = d_o.view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
             go, q, k, v, o4, lse, ps, po, None, cq, ck, mq, mk, 0.0,
-            True, scale=1.0 / math.sqrt(Dh))
+            cfg.causal, scale=1.0 / math.sqrt(Dh))
         for i, t in enumerate((dq, dk, dv)):
             t_sd = t[0].transpose(0, 1)
-            if t_sd.is_contiguous():       # cuDNN returns BSHD: a row-major [S, D] matrix
+            if t_sd.is_contiguous():       # cuDNN returns BSHD: a row-major [T, D] matrix
                 K.note()
                 _lib.check(_lib.lib().rrfp_copy_rows(
                     C.c_void_p(d_qkv.data_ptr() + i * D * 2), C.c_longlong(d_qkv.stride(0) * 2),
-                    C.c_void_p(t.data_ptr()), C.c_longlong(D * 2), S, C.c_longlong(D * 2), K._stream()))
+                    C.c_void_p(t.data_ptr()), C.c_longlong(D * 2), T, C.c_longlong(D * 2), K._stream()))
             else:
-                d_qkv[:, i * D:(i + 1) * D].view(S, H, Dh).copy_(t_sd)
+                d_qkv[:, i * D:(i + 1) * D].view(T, H, Dh).copy_(t_sd)
 
     def backward_weight(self, mb: int):
         """W task (decomposed backward): weight gradients from saved inputs/grads.
@@ -516,6 +648,7 @@ class StageCompute:
             return
         cfg = self.cfg
         S, D, Fd, Dl = cfg.seq, cfg.d_model, self.Fl, self.Dl
+        T = self.rows[mb]
         main = torch.cuda.current_stream()
         side = self.side or main
         fork = torch.cuda.Event()
@@ -523,34 +656,39 @@ class StageCompute:
         side.wait_event(fork)
         for li in reversed(range(len(self.layers))):
             g = self.g[li]
+            gy, gpre, gx2, gqkv = (self.gy[mb, li, :T], self.gpre[mb, li, :T], self.gx2[mb, li, :T],
+                                   self.gqkv[mb, li, :T])
             with torch.cuda.stream(side if li % 2 else main):
-                K.gemm(self.gy[mb, li], self.act[mb, li], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=D, n=Fd, k=S)
-                _bias_grad(self.gy[mb, li], g["b_2"])
-                K.gemm(self.gpre[mb, li], self.h2[mb, li], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=Fd, n=D, k=S)
-                _bias_grad(self.gpre[mb, li], g["b_1"])
-                K.gemm(self.gx2[mb, li], self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=D, n=Dl, k=S)
-                _bias_grad(self.gx2[mb, li], g["b_o"])
-                K.gemm(self.gqkv[mb, li], self.h1[mb, li], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=3 * Dl, n=D, k=S)
-                _bias_grad(self.gqkv[mb, li], g["b_qkv"])
+                K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=D, n=Fd, k=T)
+                _bias_grad(gy, g["b_2"])
+                K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=Fd, n=D, k=T)
+                _bias_grad(gpre, g["b_1"])
+                K.gemm(gx2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=D, n=Dl, k=T)
+                _bias_grad(gx2, g["b_o"])
+                K.gemm(gqkv, self.h1[mb, li, :T], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
+                _bias_grad(gqkv, g["b_qkv"])
         with torch.cuda.stream(side):
             if self.last:
                 K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,
                        b_mn=True, accumulate=True, m=cfg.vocab, n=D, k=S)
-            if self.first:
-                K.note()
-                _lib.check(_lib.lib().rrfp_embedding_bwd(
-                    K._p(self.tokens[mb]), K._p(self.gx0[mb]), K._p(self.g_emb["wte"]),
-                    K._p(self.g_emb["wpe"]), S, D, K._stream()))
+            if self.epilogue == "projector":
+                dyp = self.bwd_in[mb][:T]
+                K.gemm(dyp, self.y[mb, len(self.layers) - 1, :T], self.g_proj["w_proj"], epi=K.EPI_ACC_F32,
+                       a_mn=True, b_mn=True, accumulate=True, m=dyp.shape[1], n=D, k=T)
+                _bias_grad(dyp, self.g_proj["b_proj"])
+            if self.prologue:
+                self._prologue_wgrad(mb, self.gx0[mb, :T])
         join = torch.cuda.Event()
         join.record(side)
         main.wait_event(join)
 
     def zero_grads(self):
-        for gd in self.g + ([self.g_emb] if self.g_emb else []) + ([self.g_head] if self.g_head else []):
+        extra = [d for d in (self.g_emb, self.g_head, self.g_pe, self.g_proj) if d]
+        for gd in self.g + extra:
             for t in gd.values():
                 t.zero_()
         if self.last:

@@ -95,7 +95,9 @@ class GpuPipeline:
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
                  schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
-                 n_chunks: int = 1):
+                 n_chunks: int = 1, mm=None):
+        if mm is not None and (tp_size > 1 or n_chunks > 1):
+            raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
         if isinstance(hint, str):
             hint = HintOrder.parse(hint)
         if decompose is None:
@@ -118,9 +120,12 @@ class GpuPipeline:
                 self.comms[s] = [TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", devices[s]))
                                  for r in range(R)]
                 TpComm.connect_local(self.comms[s])
-        self.grid = [[StageCompute(cfg, v, V, n_mb, torch.device("cuda", devices[v % N]),
+        self.mm = mm
+        stage_cfg = (lambda v: mm.vit if v < mm.vit_stages else mm.llm) if mm else (lambda v: cfg)
+        self.grid = [[StageCompute(stage_cfg(v), v, V, n_mb, torch.device("cuda", devices[v % N]),
                                    decompose=decompose, seed=model_seed, data_seed=data_seed,
-                                   tp_rank=r, tp_size=R, tp=self.comms[v % N][r] if R > 1 else None)
+                                   tp_rank=r, tp_size=R, tp=self.comms[v % N][r] if R > 1 else None,
+                                   mm=mm)
                       for r in range(R)] for v in range(V)]
         self.stages = [row[0] for row in self.grid]
         for v in range(V):
@@ -176,7 +181,7 @@ class GpuPipeline:
         events, t0s = self.group.run_iteration(watchdog_secs)
         self.last_events = (events, min(t0s))
         last = self.stages[-1]
-        return last.loss.sum() / (self.cfg.seq * self.M)
+        return last.loss.sum() / (last.cfg.seq * self.M)
 
     def launch(self, zero_grads: bool = True):
         """Asynchronous step (for timing loops): enqueue, do not wait."""

@@ -106,3 +106,72 @@ def compare(ref, got, cos_min=0.99, rel_max=0.05):
         if cos < cos_min or rel > rel_max:
             bad.append((k, round(cos, 4), round(rel, 4)))
     return bad
+
+
+def _block(x, p, cfg, causal):
+    T, D, H = x.shape[0], cfg.d_model, cfg.n_head
+    Dh = D // H
+    h = ln(x, p["ln1_g"], p["ln1_b"], cfg.eps)
+    qkv = h @ p["w_qkv"].t() + p["b_qkv"]
+    q, k, v = (qkv[:, i * D:(i + 1) * D].view(T, H, Dh).transpose(0, 1) for i in range(3))
+    o = F.scaled_dot_product_attention(q, k, v, is_causal=causal, scale=1 / math.sqrt(Dh))
+    o = o.transpose(0, 1).reshape(T, D)
+    x2 = x + o @ p["w_o"].t() + p["b_o"]
+    h2 = ln(x2, p["ln2_g"], p["ln2_b"], cfg.eps)
+    a = F.gelu(h2 @ p["w_1"].t() + p["b_1"], approximate="tanh")
+    return x2 + a @ p["w_2"].t() + p["b_2"]
+
+
+def _prefix(st):
+    return "V" if st.part == "vit" else "L"
+
+
+def reference_mm_loss_and_grads(spec, stages):
+    """Config 4 reference: ViT on each microbatch's T_v patch rows -> projector ->
+    [visual rows, text embeddings] -> causal GPT -> loss over all positions."""
+    params = {}
+    for st in stages:
+        for li, lid in enumerate(st.layers):
+            for k, v in st.p[li].items():
+                params[f"{_prefix(st)}{lid}.{k}"] = v.float().clone().requires_grad_(True)
+        for d in (st.emb, st.head, st.pe, st.proj):
+            if d:
+                for k, v in d.items():
+                    params[k] = v.float().clone().requires_grad_(True)
+    vit0 = [st for st in stages if st.prologue == "patches"][0]
+    llm0 = [st for st in stages if st.prologue == "merge"][0]
+    last = stages[-1]
+    vc, lc = spec.vit, spec.llm
+    M, S = vit0.M, lc.seq
+    total = 0.0
+    for mb in range(M):
+        T = vit0.rows[mb]
+        x = vit0.patches[mb, :T].float() @ params["w_pe"].t() + params["b_pe"]
+        for lid in range(vc.n_layer):
+            p = {k.split(".", 1)[1]: v for k, v in params.items() if k.startswith(f"V{lid}.")}
+            x = _block(x, p, vc, False)
+        vis = x @ params["w_proj"].t() + params["b_proj"]
+        tok = llm0.tokens[mb, T:].long()
+        text = params["wte"][tok] + params["wpe"][T:S]
+        x = torch.cat([vis, text])
+        for lid in range(lc.n_layer):
+            p = {k.split(".", 1)[1]: v for k, v in params.items() if k.startswith(f"L{lid}.")}
+            x = _block(x, p, lc, True)
+        hf = ln(x, params["lnf_g"], params["lnf_b"], lc.eps)
+        logits = hf @ params["w_lm"].t()
+        total = total + F.cross_entropy(logits, last.targets[mb].long(), reduction="sum")
+    loss = total / (M * S)
+    loss.backward()
+    return loss.item(), {k: v.grad for k, v in params.items()}
+
+
+def device_grads_mm(stages):
+    out = {}
+    for st in stages:
+        for li, lid in enumerate(st.layers):
+            for k, v in st.g[li].items():
+                out[f"{_prefix(st)}{lid}.{k}"] = v
+        for d in (st.g_emb, st.g_head, st.g_pe, st.g_proj):
+            if d:
+                out.update(d)
+    return out

@@ -102,3 +102,30 @@ def test_interleaved_chunks_match_fp32_reference(n_stages, chunks, hint, mode, t
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("n_stages,vit_stages,hint,mode", [(2, 1, "bf", "free"), (3, 2, "bfw", "free"),
+                                                           (2, 1, "bf", "fixed")])
+def test_multimodal_vit_llm_matches_fp32_reference(n_stages, vit_stages, hint, mode):
+    """Config 4: ViT stages with per-microbatch visual-token counts (variable
+    message rows, non-causal attention) -> projector -> LLM stages."""
+    from paper_2605_18750_b200.model import GPTConfig, MultimodalSpec
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from ref_gpt import device_grads_mm, reference_mm_loss_and_grads
+    vit = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=512, vocab=0, seq=512, causal=False)
+    llm = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=512)
+    spec = MultimodalSpec(vit=vit, llm=llm, vit_stages=vit_stages, patch_tokens=128, d_patch=128,
+                          max_images=4, image_seed=3)
+    assert len(set(spec.visual_tokens(4))) > 1          # the microbatches really differ
+    pipe = GpuPipeline(None, n_stages, 4, hint=hint, mode=mode, mm=spec)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        tr, met = pipe.trace()
+        assert len(tr.execs()) == pipe.workload.task_count()
+        ref_loss, ref_grads = reference_mm_loss_and_grads(spec, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads_mm(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
