@@ -156,15 +156,43 @@ def default_task_times(n_stages, n_layer=24):
 
 
 def model_config(args):
-    """GPT-1.3B (BASELINE config 2) or GPT-7B (config 3, run with --tp 2)."""
+    """GPT-1.3B (BASELINE config 2), GPT-7B (config 3, run with --tp 2) or, for
+    --model mm, the LLM part (7B) of config 4."""
     from paper_2605_18750_b200.model import GPTConfig
-    if args.model == "7b":
+    if args.model in ("7b", "mm"):
         return GPTConfig(n_layer=args.layers or 32, d_model=4096, n_head=32, d_ff=16384)
     return GPTConfig(n_layer=args.layers or 24)
 
 
+def mm_spec(args):
+    """Config 4: ViT-H/14 (32 layers, d=1280, 256 tokens/image, 1..8 images per
+    microbatch, seeded) on stage 0 + the 7B LLM on the remaining stages."""
+    if args.model != "mm":
+        return None
+    from paper_2605_18750_b200.model import VIT_H14, MultimodalSpec
+    return MultimodalSpec(vit=VIT_H14, llm=model_config(args), vit_stages=1)
+
+
+def iteration_flops(args, cfg):
+    """Useful matmul FLOPs of one iteration (F + B-input + W of every layer and the LM head)."""
+    fF, fB, fW = cfg.flops_per_layer()
+    total = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
+    spec = mm_spec(args)
+    if spec is not None:
+        for t in spec.visual_tokens(args.mb):
+            vF, vB, vW = spec.vit.flops_per_layer(t)
+            total += spec.vit.n_layer * (vF + vB + vW) + 3 * 2 * t * spec.vit.d_model * (spec.d_patch + spec.llm.d_model)
+    return total
+
+
 def workload_config(args, n):
     c = model_config(args)
+    if args.model == "mm":
+        return {"workload": f"config 4: ViT-H/14 (32 L, d=1280, 256 tok/image, 1..8 images/mb seeded) on stage 0 "
+                            f"+ GPT-7B (L={c.n_layer}) on stages 1..{n - 1}, s={c.seq}, M={args.mb}",
+                "model": "vit-h14+gpt-7b-synthetic", "global_batch": args.mb, "seq_len": c.seq,
+                "parallelism": f"pp{n}", "hint": args.hint, "jitter": args.jitter, "buffer_limit": 32,
+                "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
     par = f"pp{n}" + (f"xtp{args.tp}" if args.tp > 1 else "") + (f"xc{args.chunks}" if args.chunks > 1 else "")
     return {"workload": f"GPT-{args.model.upper()} synthetic (L={c.n_layer}, d={c.d_model}, h={c.n_head}, "
                         f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, C={args.chunks}, M={args.mb}",
@@ -265,10 +293,15 @@ def run_ours(args):
     pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS[args.jitter])
     t_build = time.perf_counter() - t_build
     _log(f"built in {t_build:.1f}s")
-    first = stages[0] if stages[0].first else None
-    last = stages[-1] if stages[-1].last else None
-    tok_h = first.tokens.cpu().pin_memory() if first else None
-    tgt_h = last.targets.cpu().pin_memory() if last else None
+    # the step's input data held by this rank's stages (tokens / image patches /
+    # targets): copied from pinned host memory every step of the e2e loop
+    inputs = []
+    for st in stages:
+        for name in ("tokens", "patches", "targets"):
+            t = getattr(st, name, None)
+            if t is not None:
+                inputs.append((t, t.cpu().pin_memory()))
+    h2d = sum(h.numel() * h.element_size() for _, h in inputs)
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
 
     def barrier():
@@ -295,19 +328,21 @@ def run_ours(args):
         # end-to-end through the public API with host buffers
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            if first is not None:
-                first.tokens.copy_(tok_h, non_blocking=True)
-            if last is not None:
-                last.targets.copy_(tgt_h, non_blocking=True)
+            for dev_t, host_t in inputs:
+                dev_t.copy_(host_t, non_blocking=True)
             loss = pipe.step()
             if loss is not None:
                 loss_h.copy_(loss.reshape(1), non_blocking=False)
         barrier()
         e2e_s = (time.perf_counter() - t0) / args.steps
+    h2d_all = h2d
     if dist:
         t = torch.tensor([ms, e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_s = t[0].item(), t[1].item()
+        hb = torch.tensor([h2d], dtype=torch.int64)
+        dist.all_reduce(hb)
+        h2d_all = int(hb.item())
     _log("timed region done")
     tr, met = gather_trace(pipe, dist, world)
     bubble = met.bubble_fraction()
@@ -324,8 +359,7 @@ def run_ours(args):
     roof = gemm_roofline(cfg, peak_sus)
     _log("roofline done")
     roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
-    fF, fB, fW = cfg.flops_per_layer()
-    it_flops = args.mb * (cfg.n_layer * (fF + fB + fW) + 3 * cfg.flops_head())
+    it_flops = iteration_flops(args, cfg)
     n_dev = max(1, world)
     act = cfg.seq * cfg.d_model * 2
     # per GPU: mailbox writes (F out + B out, one copy per receiving TP rank) and
@@ -351,14 +385,14 @@ def run_ours(args):
             "roofline": roof,
             "task_us": task_us,
             "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
-                    "h2d_bytes_per_step": int(2 * args.mb * cfg.seq * 4), "d2h_bytes_per_step": 4},
+                    "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": 4},
             "gpu_launches": int(launches),
             "build_s": round(t_build, 1),
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
     pipe.close()
-    del pipe, stages, first, last
+    del pipe, stages, inputs
     if args.compare or (world > 1 and args.compare is None):
         line["variants"] = compare_variants(cfg, args, world, dist, barrier)
     if rank == 0:
@@ -372,8 +406,10 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                            tp_size=args.tp, n_chunks=args.chunks)
+                            tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args))
         return pipe, pipe.vstages
+    if args.model == "mm":
+        raise SystemExit("--model mm (config 4) needs a pipeline of >= 2 GPUs")
     from paper_2605_18750_b200.pipeline import GpuPipeline
     pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
                        tp_size=args.tp, n_chunks=args.chunks)
@@ -506,7 +542,8 @@ def main():
     ap.add_argument("--hint", default="bf", choices=["bf", "bfw", "fb", "bprio", "fprio", "1f1b"])
     ap.add_argument("--mb", type=int, default=32)
     ap.add_argument("--layers", type=int, default=None, help="default: 24 (1.3b) / 32 (7b)")
-    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b"])
+    ap.add_argument("--model", default="1.3b", choices=["1.3b", "7b", "mm"],
+                    help="1.3b (config 2), 7b (config 3 with --tp 2), mm = ViT-H + 7B (config 4)")
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size per stage (config 3: 2)")
     ap.add_argument("--chunks", type=int, default=1, help="interleaved virtual stages per GPU (C)")
     ap.add_argument("--jitter", default="J0")

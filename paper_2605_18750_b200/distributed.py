@@ -92,7 +92,7 @@ class DistPipeline:
 
     def __init__(self, cfg, n_mb: int, *, hint="bf", buffer_limit=32, mode="free", jitter=None,
                  seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None,
-                 tp_size: int = 1, tp=None, n_chunks: int = 1):
+                 tp_size: int = 1, tp=None, n_chunks: int = 1, mm=None):
         import torch.distributed as dist
         from .arbitration import HintOrder, TpGroup
         from .model import StageCompute
@@ -104,30 +104,36 @@ class DistPipeline:
         s, r, n = stage_coords(self.grank, self.gworld, tp_size)
         R, C = tp_size, n_chunks
         V = n * C
+        if mm is not None and (R > 1 or C > 1):
+            raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
+        stage_cfg = (lambda v: mm.vit if v < mm.vit_stages else mm.llm) if mm else (lambda v: cfg)
         self.rank, self.world, self.tp_rank, self.R, self.C = s, n, r, R, C
         self.device = torch.cuda.current_device()
         decompose = hint.kind == "bfw"
-        S, D = cfg.seq, cfg.d_model
-        slot_bytes = n_mb * S * D * 2
-        # this lane hosts virtual stages v = c*N + s (chunk c), each with its own mailboxes
+        # this lane hosts virtual stages v = c*N + s (chunk c), each with its own mailboxes:
+        # F input [M, S, D] of the stage's own width; B input [M, S, D_out] (the ViT
+        # projector stage receives the gradient of its d_llm-wide output)
         self.vids = [c * n + s for c in range(C)]
-        self.bufs = {}
+        self.bufs, shapes = {}, {}
         for v in self.vids:
-            self.bufs[(v, "fwd")] = IpcBuffer(slot_bytes, self.device) if v > 0 else None
-            self.bufs[(v, "bwd")] = IpcBuffer(slot_bytes, self.device) if v < V - 1 else None
+            vc = stage_cfg(v)
+            d_out = mm.llm.d_model if (mm and v == mm.vit_stages - 1) else vc.d_model
+            shapes[v] = ((n_mb, vc.seq, vc.d_model), (n_mb, vc.seq, d_out))
+            self.bufs[(v, "fwd")] = IpcBuffer(2 * n_mb * vc.seq * vc.d_model, self.device) if v > 0 else None
+            self.bufs[(v, "bwd")] = IpcBuffer(2 * n_mb * vc.seq * d_out, self.device) if v < V - 1 else None
         self.comm = None
         if R > 1:
             from .tp import TpComm
-            self.comm = TpComm(r, R, (S, D), torch.device("cuda", self.device))
+            self.comm = TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", self.device))
         self.vstages = []
         for v in self.vids:
             fb, bb = self.bufs[(v, "fwd")], self.bufs[(v, "bwd")]
             self.vstages.append(StageCompute(
-                cfg, v, V, n_mb, torch.device("cuda", self.device), decompose=decompose, seed=model_seed,
-                data_seed=data_seed,
-                fwd_in=wrap_bf16(fb.ptr.value, (n_mb, S, D), self.device) if fb else None,
-                bwd_in=wrap_bf16(bb.ptr.value, (n_mb, S, D), self.device) if bb else None,
-                tp_rank=r, tp_size=R, tp=self.comm))
+                stage_cfg(v), v, V, n_mb, torch.device("cuda", self.device), decompose=decompose,
+                seed=model_seed, data_seed=data_seed,
+                fwd_in=wrap_bf16(fb.ptr.value, shapes[v][0], self.device) if fb else None,
+                bwd_in=wrap_bf16(bb.ptr.value, shapes[v][1], self.device) if bb else None,
+                tp_rank=r, tp_size=R, tp=self.comm, mm=mm))
         # the lane's first / last virtual stages (loss lives on virtual stage V-1)
         self.stage = self.vstages[-1] if self.vstages[-1].last else self.vstages[0]
         w = nominal_workload(cfg, n, n_mb, decompose, tp_size=R, n_chunks=C)
@@ -143,7 +149,7 @@ class DistPipeline:
                                bodies=None, compute_kind=1, schedule=schedule, defer_bodies=True)
         hd = lambda b: b.handle() if b else None
         mine = {"stage": s, "tp_rank": r,
-                "mbox": {v: (hd(self.bufs[(v, "fwd")]), hd(self.bufs[(v, "bwd")])) for v in self.vids},
+                "mbox": {v: (hd(self.bufs[(v, "fwd")]), hd(self.bufs[(v, "bwd")]), shapes[v]) for v in self.vids},
                 "lane": self.group.ipc_handles()[(s, r)],
                 "tp": self.comm.ipc_handles() if self.comm else None}
         allh = [None] * self.gworld
@@ -153,8 +159,8 @@ class DistPipeline:
             self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
 
         def mailboxes(v, which):   # virtual stage v's F (0) / B (1) mailbox on every TP rank
-            dst = [wrap_bf16(open_handle(by[(v % n, q)]["mbox"][v][which]), (n_mb, S, D), self.device)
-                   for q in range(R)]
+            dst = [wrap_bf16(open_handle(by[(v % n, q)]["mbox"][v][which]), by[(v % n, q)]["mbox"][v][2][which],
+                             self.device) for q in range(R)]
             return [[d[mb] for d in dst] for mb in range(n_mb)]
 
         for st, v in zip(self.vstages, self.vids):
@@ -208,7 +214,7 @@ class DistPipeline:
             allv = [None] * self.gworld
             dist.all_gather_object(allv, mine, group=group)
             nominal_us = allv[::self.R]      # TP rank 0 of every stage
-        self.nominal_us = nominal_us
+        self.nominal_table = nominal_us
         floors = lognormal_floor_tables(self.world, self.n_mb, nominal_us, sigma, seed, stages=[self.rank])
         self.group.set_floor_us(floors)
 

@@ -47,11 +47,11 @@ class GPTConfig:
     def d_head(self):
         return self.d_model // self.n_head
 
-    def flops_per_layer(self):
-        """(F, B-input, W) matmul FLOPs of one layer for one microbatch."""
-        s, d, f = self.seq, self.d_model, self.d_ff
+    def flops_per_layer(self, rows: int | None = None):
+        """(F, B-input, W) matmul FLOPs of one layer for one microbatch of `rows` tokens."""
+        s, d, f = rows or self.seq, self.d_model, self.d_ff
         gemm = 2 * s * d * (3 * d + d + 2 * f)
-        attn = 2 * 2 * s * s * d / 2           # QK^T and PV, causal half
+        attn = 2 * 2 * s * s * d / (2 if self.causal else 1)   # QK^T and PV (causal: half)
         return gemm + attn, gemm + 2 * attn, gemm
 
     def flops_head(self):

@@ -207,7 +207,7 @@ class GpuPipeline:
         if nominal_us is None:
             tr, _ = self.trace()
             nominal_us = measured_nominal(tr, self.N)
-        self.nominal_us = nominal_us
+        self.nominal_table = nominal_us
         floors = lognormal_floor_tables(self.N, self.M, nominal_us, sigma, seed)
         self.group.set_floor_us(floors)
 

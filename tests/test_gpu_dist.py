@@ -14,16 +14,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("hint,tp,nproc,chunks", [("bf", 1, 2, 1), ("bfw", 1, 2, 1), ("bf", 2, 2, 1),
-                                                  ("bfw", 2, 4, 1), ("bf", 1, 2, 2)])
-def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks):
+@pytest.mark.parametrize("hint,tp,nproc,chunks,model", [("bf", 1, 2, 1, "gpt"), ("bfw", 1, 2, 1, "gpt"),
+                                                        ("bf", 2, 2, 1, "gpt"), ("bfw", 2, 4, 1, "gpt"),
+                                                        ("bf", 1, 2, 2, "gpt"), ("bfw", 1, 2, 1, "mm")])
+def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks, model):
     """PP=2 (tp=1), TP=2 x PP=1, TP=2 x PP=2 and PP=2 x C=2 (chunk wrap across
-    processes): IPC mailboxes written by every sender TP rank, peer-memory
-    all-reduce between processes."""
+    processes), and config 4 (ViT process -> LLM process, variable-row
+    messages): IPC mailboxes written by every sender TP rank, peer-memory
+    all-reduce between processes.  The reference is the same model in one process."""
     env = dict(os.environ, RRFP_SAME_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tools", "dist_check.py"),
-           hint, str(tp), str(chunks)]
+           hint, str(tp), str(chunks), model]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     line = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]

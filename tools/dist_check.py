@@ -25,7 +25,14 @@ def main():
     hint = sys.argv[1] if len(sys.argv) > 1 else "bf"
     tp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     chunks = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks)
+    mm = None
+    if len(sys.argv) > 4 and sys.argv[4] == "mm":   # config 4: ViT stage(s) + LLM stage(s)
+        from paper_2605_18750_b200.model import MultimodalSpec
+        vit = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=512, vocab=0, seq=512, causal=False)
+        cfg = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=512)
+        mm = MultimodalSpec(vit=vit, llm=cfg, vit_stages=world // 2, patch_tokens=128, d_patch=128,
+                            max_images=4, image_seed=3)
+    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm)
     losses = []
     import time
     wd = float(os.environ.get("RRFP_WATCHDOG", "60"))
@@ -43,7 +50,7 @@ def main():
     pipe.close()
     if rank == 0:
         from paper_2605_18750_b200.pipeline import GpuPipeline
-        ref = GpuPipeline(cfg, 1, 4, hint=hint)
+        ref = GpuPipeline(cfg, world // tp if mm else 1, 4, hint=hint, mm=mm)
         ref_loss = ref.step().item()
         ref.close()
         print(json.dumps({"ranks": out, "single_process_pp1_loss": ref_loss}), flush=True)
