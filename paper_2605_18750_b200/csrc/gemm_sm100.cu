@@ -984,7 +984,17 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   memset(&tc, 0, sizeof(tc));
   memset(&tc2, 0, sizeof(tc2));
   g.tma_st = 0;
-  if (use_pair() && use_tma_store() && g.vec) {
+  // The TMA-store epilogue is used for memory of this device only; a C (or C2)
+  // that lives on a peer GPU (a neighbour stage's mailbox over NVLink) takes the
+  // per-thread st.global epilogue, the path P2P stores are defined for.
+  auto local = [](const void* p) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice && a.device == dev;
+  };
+  if (use_pair() && use_tma_store() && g.vec && local(C) && (!C2 || local(C2))) {
     const bool f32 = (epi == EPI_ACC_F32 || epi == EPI_F32);
     bool ok = make_map(&tc, C, M, N, ldc, f32 ? 32 : 64, 32, f32) == RRFP_OK;
     if (ok && epi == EPI_BIAS_GELU) ok = make_map(&tc2, C2, M, N, ldc2, 64, 32) == RRFP_OK;
