@@ -186,6 +186,7 @@ def iteration_flops(args, cfg):
 
 
 def workload_config(args, n):
+    from paper_2605_18750_b200.model import split_layers
     c = model_config(args)
     if args.model == "mm":
         return {"workload": f"config 4: ViT-H/14 (32 L, d=1280, 256 tok/image, 1..8 images/mb seeded) on stage 0 "
@@ -198,6 +199,8 @@ def workload_config(args, n):
                         f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, C={args.chunks}, M={args.mb}",
             "model": f"gpt-{args.model}-synthetic", "global_batch": args.mb, "seq_len": c.seq,
             "parallelism": par, "hint": args.hint, "jitter": args.jitter,
+            "layer_split": [len(split_layers(c.n_layer, n, s_, args.head_cost if args.chunks == 1 else 0))
+                            for s_ in range(n)],
             "buffer_limit": 32, "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
 
 
@@ -406,13 +409,13 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                            tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args))
+                            tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args), head_cost=args.head_cost)
         return pipe, pipe.vstages
     if args.model == "mm":
         raise SystemExit("--model mm (config 4) needs a pipeline of >= 2 GPUs")
     from paper_2605_18750_b200.pipeline import GpuPipeline
     pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                       tp_size=args.tp, n_chunks=args.chunks)
+                       tp_size=args.tp, n_chunks=args.chunks, head_cost=args.head_cost)
     return pipe, pipe.stages
 
 
@@ -546,6 +549,9 @@ def main():
                     help="1.3b (config 2), 7b (config 3 with --tp 2), mm = ViT-H + 7B (config 4)")
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size per stage (config 3: 2)")
     ap.add_argument("--chunks", type=int, default=1, help="interleaved virtual stages per GPU (C)")
+    ap.add_argument("--head-cost", dest="head_cost", type=float, default=1.4,
+                    help="LM head + loss of the last stage in layer-equivalents for the balanced layer "
+                         "split (measured: F 400 + B 650 us vs 762 us per layer); 0 = even split")
     ap.add_argument("--jitter", default="J0")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--compare", dest="compare", action="store_true", default=None,

@@ -109,10 +109,24 @@ def synthetic_patches(spec: MultimodalSpec, n_mb: int, seed: int, device):
     return (torch.randn(n_mb, spec.vit.seq, spec.d_patch, generator=g, device=device)).to(torch.bfloat16)
 
 
-def split_layers(n_layer: int, n_stages: int, stage: int):
-    base, extra = divmod(n_layer, n_stages)
-    lo = stage * base + min(stage, extra)
-    return list(range(lo, lo + base + (1 if stage < extra else 0)))
+def split_layers(n_layer: int, n_stages: int, stage: int, head_cost: float = 0.0):
+    """Global layer ids of `stage`.  head_cost = 0: even split (earlier stages
+    take the remainder).  head_cost > 0: the last stage also runs the LM head +
+    loss, worth `head_cost` layers; the split minimises the largest stage cost
+    (the pipeline's bottleneck), e.g. 24 layers / 8 stages / head 1.5 ->
+    [4,3,3,3,3,3,3,2] (max 4.0 layer-equivalents instead of 4.5)."""
+    if head_cost <= 0 or n_stages == 1:
+        counts = [n_layer // n_stages + (1 if s < n_layer % n_stages else 0) for s in range(n_stages)]
+    else:
+        m = max(1, math.ceil((n_layer + head_cost) / n_stages))
+        while (n_stages - 1) * m + max(1, math.floor(m - head_cost)) < n_layer:
+            m += 1
+        last = max(1, min(math.floor(m - head_cost), n_layer - (n_stages - 1)))
+        rest = n_layer - last
+        counts = [rest // (n_stages - 1) + (1 if s < rest % (n_stages - 1) else 0)
+                  for s in range(n_stages - 1)] + [last]
+    lo = sum(counts[:stage])
+    return list(range(lo, lo + counts[stage]))
 
 
 def _gen(device, seed):
@@ -235,7 +249,7 @@ class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
                  decompose: bool = False, seed: int = 1234, data_seed: int = 0,
                  fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None,
-                 mm: MultimodalSpec | None = None):
+                 mm: MultimodalSpec | None = None, head_cost: float = 0.0):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
         self.decompose = decompose
@@ -251,7 +265,8 @@ class StageCompute:
         else:
             part, idx, cnt = "gpt", stage, n_stages
         self.part = part
-        self.layers = split_layers(cfg.n_layer, cnt, idx)
+        # head_cost > 0: balance the layer split against the last stage's LM head
+        self.layers = split_layers(cfg.n_layer, cnt, idx, head_cost if part != "vit" else 0.0)
         # prologue: token embedding (GPT stage 0), patch embedding (ViT stage 0), or
         # merge (first LLM stage: projected visual rows arrive in the mailbox, text
         # rows are embedded here); epilogue: LM head + loss, or the ViT projector

@@ -78,3 +78,16 @@ def test_stage_coords_tp_groups():
     assert [stage_coords(g, 4, 1)[:2] for g in range(4)] == [(g, 0) for g in range(4)]
     with pytest.raises(ValueError):
         stage_coords(0, 6, 4)
+
+
+def test_balanced_layer_split():
+    """Layer split against the last stage's LM head (bench --head-cost): every
+    layer exactly once, contiguous, and the max stage cost is minimal."""
+    from paper_2605_18750_b200.model import split_layers
+    for L, N, h in [(24, 8, 1.4), (24, 4, 1.4), (24, 2, 1.4), (32, 4, 1.4), (7, 3, 2.0), (24, 8, 0.0)]:
+        parts = [split_layers(L, N, s, h) for s in range(N)]
+        assert [i for p in parts for i in p] == list(range(L))
+        cost = [len(p) + (h if s == N - 1 else 0) for s, p in enumerate(parts)]
+        even = [len(split_layers(L, N, s)) + (h if s == N - 1 else 0) for s in range(N)]
+        assert max(cost) <= max(even)
+    assert [len(split_layers(24, 8, s, 1.4)) for s in range(8)] == [4, 3, 3, 3, 3, 3, 3, 2]
