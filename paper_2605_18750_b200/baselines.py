@@ -10,7 +10,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .workload import BACKWARD, FORWARD, TaskId, Workload
+from .workload import BACKWARD, FORWARD, WEIGHT, TaskId, Workload
 
 
 class ScheduleDeadlockError(RuntimeError):
@@ -48,13 +48,38 @@ def build_1f1b_schedule(workload: Workload) -> FixedSchedule:
     if workload.decompose_backward:
         raise ValueError("1F1B baseline does not decompose backward")
     n, m = workload.num_stages, workload.num_microbatches
+    return FixedSchedule(tuple(tuple(build_1f1b_schedule_skeleton(n, m, s)) for s in range(n)))
+
+
+def build_zb_h1_schedule(workload: Workload) -> FixedSchedule:
+    """Zero-bubble-H1-like fixed order for a decomposed (B-input / W) workload
+    ("fixed-schedule FIXED mode for arbitrary FixedSchedule
+    JSON, e.g. ZB-like"): 1F1B's F/B skeleton, with stage i deferring each
+    weight-gradient task W(j) until after B(j + N-1-i), so the W tasks fill the
+    cool-down bubbles; the remaining W tasks drain at the end."""
+    if workload.num_chunks != 1:
+        raise ValueError("ZB-H1 schedule covers non-interleaved workloads only")
+    if not workload.decompose_backward:
+        raise ValueError("ZB-H1 schedule needs a decomposed backward (W tasks)")
+    n, m = workload.num_stages, workload.num_microbatches
     orders = []
     for s in range(n):
-        warm = min(m, n - 1 - s)
-        seq = [TaskId(s, j, 0, FORWARD) for j in range(warm)]
-        for j in range(m - warm):
-            seq.append(TaskId(s, warm + j, 0, FORWARD))
-            seq.append(TaskId(s, j, 0, BACKWARD))
-        seq += [TaskId(s, j, 0, BACKWARD) for j in range(m - warm, m)]
+        lag = n - 1 - s
+        seq, next_w = [], 0
+        for t in build_1f1b_schedule_skeleton(n, m, s):
+            seq.append(t)
+            if t.direction == BACKWARD and t.microbatch - lag >= next_w:
+                seq.append(TaskId(s, next_w, 0, WEIGHT))
+                next_w += 1
+        seq += [TaskId(s, j, 0, WEIGHT) for j in range(next_w, m)]
         orders.append(tuple(seq))
     return FixedSchedule(tuple(orders))
+
+
+def build_1f1b_schedule_skeleton(n: int, m: int, s: int):
+    """Stage s's 1F1B F/B order (warm-up min(m, n-1-s) F, alternate, drain)."""
+    warm = min(m, n - 1 - s)
+    seq = [TaskId(s, j, 0, FORWARD) for j in range(warm)]
+    for j in range(m - warm):
+        seq += [TaskId(s, warm + j, 0, FORWARD), TaskId(s, j, 0, BACKWARD)]
+    return seq + [TaskId(s, j, 0, BACKWARD) for j in range(m - warm, m)]

@@ -132,3 +132,26 @@ def test_watchdog_fires_on_impossible_schedule():
     from paper_2605_18750_b200.runtime import LiveWatchdogError
     with pytest.raises(LiveWatchdogError):
         run_gpu(w, "bf", 32, time_scale=1.0, mode="fixed", schedule=bad, watchdog_secs=2)
+
+
+def test_zb_h1_fixed_schedule_on_lanes():
+    """A ZB-H1-like FixedSchedule (W tasks deferred into the cool-down) on the
+    free-running lanes in FIXED mode: per-stage order followed, trace valid."""
+    w = P.generate_workload(_spec(4, 8, decompose_backward=True), 9)
+    sched = P.build_zb_h1_schedule(w)
+    tr, m = run_gpu(w, "bfw", 32, time_scale=1.0, seed=9, mode="fixed", schedule=sched)
+    want = [[(t.direction, t.microbatch, t.chunk) for t in st] for st in sched.per_stage_order]
+    assert _seqs(tr, 4) == want
+    viol = O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=1.0)
+    assert not viol, viol[:5]
+
+
+def test_external_hint_replay_bit_exact():
+    """External ranked hint (arbitration.py:259-278, config hint "file:...") on
+    the lanes in replay mode: the oracle's per-stage order."""
+    w = P.generate_workload(_spec(4, 8), 11)
+    hint = P.HintOrder(kind="external", ranked=(("B", "asc"), ("F", "asc")))
+    tr, _ = run_gpu(w, hint, 32, time_scale=1.0, seed=11, mode="replay")
+    ev, _ = O.run_rrfp(_oracle_w(w), "external", 32, 11, "J0", ranked=(("B", "asc"), ("F", "asc")))
+    want = [[(d, mb, c) for d, mb, c, _, _ in s] for s in O.exec_sequences(ev, 4)]
+    assert _seqs(tr, 4) == want
