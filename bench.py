@@ -394,6 +394,11 @@ def run_ours(args):
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
+    if rank == 0 and args.model != "mm" and args.tp == 1 and args.chunks == 1:
+        try:
+            line["pipeline_model"] = pipeline_model(args, cfg, task_us, n)
+        except Exception as e:   # a model table must never cost the measurement
+            line["pipeline_model"] = {"error": repr(e)[:200]}
     pipe.close()
     del pipe, stages, inputs
     if args.compare or (world > 1 and args.compare is None):
@@ -417,6 +422,71 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
                        tp_size=args.tp, n_chunks=args.chunks, head_cost=args.head_cost)
     return pipe, pipe.stages
+
+
+def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8), device="cuda"):
+    """Virtual-clock prediction of the PP sweep from THIS run's B200 task times
+    (SURVEY 6.3 / 8d C5): per-layer F and B durations of the measured run,
+    balanced layer split, LM head on the last stage, lognormal(0, sigma)
+    compute factors per task (identical draws for every schedule) and
+    lognormal(ln 100 us, sigma) per-edge comm delays.  1F1B = run_fixed, BF /
+    BFW = run_rrfp, all in the device replay kernel.  A model, not a
+    multi-GPU measurement: it says what the scheduler does with these kernels."""
+    import math
+    import numpy as np
+    import paper_2605_18750_b200 as P
+    from paper_2605_18750_b200.model import split_layers
+    from paper_2605_18750_b200.rng import substream
+    L = cfg.n_layer
+    lay0 = [len(split_layers(L, n_meas, s_, args.head_cost)) for s_ in range(n_meas)]
+    # per-layer times from the measured first stage (no head), head from the last stage
+    f_l = task_us["F"][0] / lay0[0]
+    b_l = task_us["B"][0] / lay0[0]
+    f_h = max(0.0, task_us["F"][-1] - f_l * lay0[-1]) if n_meas == 1 else task_us["F"][-1] - f_l * lay0[-1]
+    b_h = max(0.0, task_us["B"][-1] - b_l * lay0[-1]) if n_meas == 1 else task_us["B"][-1] - b_l * lay0[-1]
+    if n_meas == 1:   # the PP=1 stage holds every layer and the head: split by the measured ratio
+        f_h, b_h = 1.6 * f_l, 1.27 * b_l
+        f_l = task_us["F"][0] / (L + 1.6)
+        b_l = task_us["B"][0] / (L + 1.27)
+        f_h, b_h = 1.6 * f_l, 1.27 * b_l
+    out = {"definition": pipeline_model.__doc__.split("\n\n")[0].strip().replace("\n", " "),
+           "per_layer_us": {"F": round(f_l, 1), "B": round(b_l, 1)}, "head_us": {"F": round(f_h, 1), "B": round(b_h, 1)}}
+    for n in pps:
+        lay = [len(split_layers(L, n, s_, args.head_cost)) for s_ in range(n)]
+        row = {"layers": lay}
+        for sigma in sigmas:
+            res = {}
+            for name in ("1f1b", "bf", "bfw"):
+                dec = name == "bfw"
+                lat = {}
+                for s_ in range(n):
+                    for mb in range(args.mb):
+                        x = float(np.exp(substream(11, "cjitter", s_, mb, "F").normal(0.0, sigma))) if sigma else 1.0
+                        y = float(np.exp(substream(11, "cjitter", s_, mb, "B").normal(0.0, sigma))) if sigma else 1.0
+                        fd = (f_l * lay[s_] + (f_h if s_ == n - 1 else 0)) * x
+                        bd = (b_l * lay[s_] + (b_h if s_ == n - 1 else 0)) * y
+                        lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(fd))
+                        if dec:
+                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(0.81 * bd))
+                            lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(0.29 * bd))
+                        else:
+                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(bd))
+                comm = P.CommDelay()
+                if sigma:
+                    comm = P.CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
+                                       hi=int(args.comm_us * 50), seed=17)
+                w = P.Workload(num_stages=n, num_microbatches=args.mb, num_chunks=1, tp_group_size=1,
+                               latency=lat, comm_delay=comm, decompose_backward=dec)
+                if name == "1f1b":
+                    tr, m = P.run_fixed(P.build_1f1b_schedule(w), w, device=device)
+                else:
+                    tr, m = P.run_rrfp(w, name, 32, 0, device=device)
+                res[name] = {"ms": round(m.makespan / 1e3, 2), "bubble": round(m.bubble_fraction(), 4)}
+            for name in ("bf", "bfw"):
+                res[name]["speedup_vs_1f1b"] = round(res["1f1b"]["ms"] / res[name]["ms"], 4)
+            row[f"sigma{sigma}"] = res
+        out[f"pp{n}"] = row
+    return out
 
 
 def gather_trace(pipe, dist, world):

@@ -350,7 +350,6 @@ class StageCompute:
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
             self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl)
             self.gx0 = e(n_mb, S, D) if self.prologue else None
-            self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl)
         self.graphs = {}
         self.kernel_counts = {}   # (kind, mb) -> our kernel launches in that body
 
@@ -461,20 +460,25 @@ class StageCompute:
 
     # ----------------------------------------------------------- backward
     def backward_input(self, mb: int):
-        """B task: input gradients, plus (unless decomposed) weight gradients.
+        """B task: input gradients plus weight gradients; decomposed (BFW), the
+        FC1/FC2 weight gradients (the larger half of the weight-gradient FLOPs)
+        are deferred to the W task.
 
         Two streams: the input-gradient chain (dgrad GEMMs, LayerNorm and
-        attention backward) runs on the main stream; each layer's four
-        weight-gradient GEMMs + bias reductions run on a side stream as soon as
-        their inputs exist, so they fill the tail waves of the dgrad GEMMs.
-        Scratch comes in two parity sets; the main stream only rewrites a set
-        after the side stream finished reading it (events).
+        attention backward) runs on the main stream; each layer's weight-gradient
+        GEMMs + bias reductions run on a side stream as soon as their inputs
+        exist, so they fill the tail waves of the dgrad GEMMs and overlap the
+        non-GEMM attention / LayerNorm backward.  That overlap is why the
+        attention-side weight gradients stay in B even when decomposed: moved
+        to W they would run alone (B-input + W > fused B).  Scratch comes in two
+        parity sets; the main stream only rewrites a set after the side stream
+        finished reading it (events).
         """
         cfg = self.cfg
         S, D, Fd, V = cfg.seq, cfg.d_model, cfg.d_ff, cfg.vocab
         T = self.rows[mb]
         dec = self.decompose
-        fused_w = not dec
+        fused_w = not dec          # FC1/FC2 (and head / prologue) weight gradients in this task
         nl = len(self.layers)
         main = torch.cuda.current_stream()
         side = self.side or main          # side=None: the whole task on one stream
@@ -536,8 +540,8 @@ class StageCompute:
             if li + 2 in side_done:          # set q was last read by layer li+2's side work
                 main.wait_event(side_done[li + 2])
             d_pre = (self.gpre[mb, li] if dec else self.sd_big[q])[:T]
-            d_x2 = (self.gx2[mb, li] if dec else self.sd_b[q])[:T]
-            d_qkv = (self.gqkv[mb, li] if dec else self.sd_qkv[q])[:T]
+            d_x2 = self.sd_b[q][:T]
+            d_qkv = self.sd_qkv[q][:T]
             if fused_w:
                 dyy = dy
                 on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
@@ -553,30 +557,28 @@ class StageCompute:
             self._dgrad_reduce(d_pre, p["w_1"], Fl, T)
             _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
                     d_x2, g["ln2_g"], g["ln2_b"])
-            if fused_w:
-                ov = self.o_view[mb][li]
-                on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
-                                       _bias_grad(d_x2, g["b_o"])))
+            ov = self.o_view[mb][li]
+            on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
+                                          a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
+                                   _bias_grad(d_x2, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
             d_o = d_head if self.R == 1 else self.d_o
             K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=T, n=Dl, k=D)
             self._attn_bwd(mb, li, d_o, d_qkv)
-            if fused_w:
-                def qkv_w(d_qkv=d_qkv, h1=h1, g=g):
-                    K.gemm(d_qkv, h1, g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                           b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
-                    _bias_grad(d_qkv, g["b_qkv"])
-                on_side(ev(), qkv_w)
-                done = torch.cuda.Event()
-                done.record(side)
-                side_done[li] = done
+            def qkv_w(d_qkv=d_qkv, h1=h1, g=g):
+                K.gemm(d_qkv, h1, g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                       b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
+                _bias_grad(d_qkv, g["b_qkv"])
+            on_side(ev(), qkv_w)
+            done = torch.cuda.Event()
+            done.record(side)
+            side_done[li] = done
             self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             extra = []
             if li > 0:
                 dx = dy_buf(li - 1)
-                if fused_w and li + 1 in side_done:   # layer li+1's side work read this buffer
+                if li + 1 in side_done:   # layer li+1's side work read this buffer
                     main.wait_event(side_done[li + 1])
             elif self.prologue is None:
                 if self.bwd_out is not None:
@@ -585,7 +587,7 @@ class StageCompute:
                     dx = self.sd_a[1][:T]
             else:   # prologue stages keep the input gradient for the embedding backward
                 dx = (self.gx0[mb] if dec else self.sd_a[1])[:T]
-                if fused_w and 1 in side_done:
+                if 1 in side_done:
                     main.wait_event(side_done[1])
             _ln_bwd(d_head, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
                     g["ln1_g"], g["ln1_b"])
@@ -600,7 +602,7 @@ class StageCompute:
         if self.prologue and fused_w:
             dyy = dy
             on_side(ev(), lambda: self._prologue_wgrad(mb, dyy))
-        if fused_w:
+        if side != main:
             join = torch.cuda.Event()
             join.record(side)
             main.wait_event(join)
@@ -656,9 +658,11 @@ class StageCompute:
                 d_qkv[:, i * D:(i + 1) * D].view(T, H, Dh).copy_(t_sd)
 
     def backward_weight(self, mb: int):
-        """W task (decomposed backward): weight gradients from saved inputs/grads.
-        Layers alternate between the main and the side stream (independent GEMMs
-        fill each other's tail waves); joined at the end."""
+        """W task (decomposed backward): the FC1/FC2 weight gradients (plus LM
+        head / projector / prologue) from the saved dy and d_pre; the attention
+        weight gradients were done in B (see backward_input).  Layers alternate
+        between the main and the side stream (independent GEMMs fill each
+        other's tail waves); joined at the end."""
         if not self.decompose:
             return
         cfg = self.cfg
@@ -671,8 +675,7 @@ class StageCompute:
         side.wait_event(fork)
         for li in reversed(range(len(self.layers))):
             g = self.g[li]
-            gy, gpre, gx2, gqkv = (self.gy[mb, li, :T], self.gpre[mb, li, :T], self.gx2[mb, li, :T],
-                                   self.gqkv[mb, li, :T])
+            gy, gpre = self.gy[mb, li, :T], self.gpre[mb, li, :T]
             with torch.cuda.stream(side if li % 2 else main):
                 K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
                        b_mn=True, accumulate=True, m=D, n=Fd, k=T)
@@ -680,12 +683,6 @@ class StageCompute:
                 K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
                        b_mn=True, accumulate=True, m=Fd, n=D, k=T)
                 _bias_grad(gpre, g["b_1"])
-                K.gemm(gx2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=D, n=Dl, k=T)
-                _bias_grad(gx2, g["b_o"])
-                K.gemm(gqkv, self.h1[mb, li, :T], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
-                _bias_grad(gqkv, g["b_qkv"])
         with torch.cuda.stream(side):
             if self.last:
                 K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,

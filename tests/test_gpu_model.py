@@ -131,3 +131,26 @@ def test_multimodal_vit_llm_matches_fp32_reference(n_stages, vit_stages, hint, m
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+def test_zb_h1_schedule_gpt_pipeline_matches_fp32_reference():
+    """A ZB-H1-like FixedSchedule (W tasks deferred into the cool-down) driving
+    the GPT bodies in FIXED mode on the device lanes."""
+    import paper_2605_18750_b200 as P
+    from paper_2605_18750_b200.pipeline import GpuPipeline, nominal_workload
+    cfg = _cfg()
+    sched = P.build_zb_h1_schedule(nominal_workload(cfg, 4, 4, True))
+    pipe = GpuPipeline(cfg, 4, 4, hint="bfw", mode="fixed", schedule=sched)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        tr, met = pipe.trace()
+        got = [[(e.direction, e.microbatch) for e in sorted(tr.execs(), key=lambda e: e.t_start)
+                if e.stage == s] for s in range(4)]
+        assert got == [[(t.direction, t.microbatch) for t in st] for st in sched.per_stage_order]
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
