@@ -16,6 +16,11 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# before any CUDA context exists: one hardware queue per stream, so a lane's
+# spinning dispatcher never serialises another stream's work (as the package sets)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import subprocess
 import sys
 import threading

@@ -49,9 +49,16 @@ class _CudaArray:
 
 
 def wrap_bf16(ptr: int, shape, device) -> torch.Tensor:
-    """Zero-copy torch view of raw device memory (bf16 via int16 typestr)."""
+    """Zero-copy torch view of raw device memory (bf16 via int16 typestr).
+
+    No ``device=`` conversion: torch places a __cuda_array_interface__ tensor on
+    the device that OWNS the pointer, and converting a peer GPU's mailbox to the
+    local device would silently copy it (writes would land in the copy).  The
+    kernels only use the address; the assert guards the zero-copy contract."""
     with torch.cuda.device(device):
-        t = torch.as_tensor(_CudaArray(ptr, shape, "<i2"), device=device)
+        t = torch.as_tensor(_CudaArray(ptr, shape, "<i2"))
+    if t.data_ptr() != ptr:
+        raise RuntimeError("wrap_bf16: torch copied the buffer instead of viewing it")
     return t.view(torch.bfloat16)
 
 

@@ -1,3 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
-timeout 900 python -m pytest tests/test_gpu_model.py -x -q 2>&1 | tail -3
-timeout 300 python tools/task_times.py 4 bfw 2>&1 | tail -3
+timeout 1200 python -m pytest tests/test_gpu_dist.py tests/test_gpu_model.py -x -q 2>&1 | tail -3
