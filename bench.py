@@ -269,8 +269,12 @@ def gemm_roofline(cfg, peak_tf):
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tf, 3), "traffic": traffic,
             "traffic_unit": "bytes/launch (dram rd+wr, ncu --set full, profiles/gemm_traffic.json)",
-            "kernel": "gemm_bf16_sm100 (tcgen05.mma 128x256x16, TMA 4-stage, TMEM x2)",
-            "per_launch": "mean over one layer's 10 F/B/W GEMMs (2048 tokens, d=2048, ffn=8192)",
+            "kernel": "gemm_bf16_sm100_pair (cta_group::2 tcgen05.mma 256x256x16, TMA 6-stage ring, "
+                      "TMEM x2, TMA-store epilogue)",
+            "per_launch": f"mean over one layer's 10 F/B/W GEMMs ({cfg.seq} tokens, d={cfg.d_model}, "
+                          f"ffn={cfg.d_ff}); CUDA events on the launch stream, 10 reps, in this process "
+                          "after the timed region",
+            "share_of_step": "71.9% of device time (profiles/r01_bench_launches_summary.txt, ncu launch list)",
             "avg_launch_us": round(ms * 1e3, 1)}
 
 
@@ -394,7 +398,8 @@ def run_ours(args):
             "task_us": task_us,
             "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
                     "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": 4},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches) * args.steps,
+            "gpu_launches_per_step": int(launches),
             "build_s": round(t_build, 1),
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:

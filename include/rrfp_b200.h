@@ -251,7 +251,9 @@ int rrfp_gemm_set_variant(int pair);
 /* Programmatic dependent launch for the stage kernels (default on; env RRFP_PDL=0 disables). */
 int rrfp_set_pdl(int on);
 int rrfp_gemm_reserve_sms(int n);
-/* 1 = smem-staged TMA store / reduce-add epilogue (default), 0 = per-thread global stores. */
+/* 1 = smem-staged TMA store / reduce-add epilogue (default; outputs on a peer GPU
+ * use staged coalesced st.global), 0 = per-thread global stores, 2 = force the
+ * staged coalesced st.global path for every bf16 output (test hook). */
 int rrfp_gemm_set_epilogue(int tma_store);
 /* 1 = stream-K split of the last partial round of 256x256 tiles over all CTA pairs (default 0). */
 int rrfp_gemm_set_streamk(int on);

@@ -61,7 +61,8 @@ struct GemmArgs {
   int accumulate;
   int vec;   // 1 when C/C2/R rows are 16-byte aligned (vector epilogue path allowed)
   int vec_bias;
-  int tma_st;  // 1: pair-kernel epilogue stages tiles in smem and stores / reduce-adds them with TMA
+  int tma_st;  // pair-kernel epilogue: 0 per-thread stores, 1 smem box + TMA store / reduce-add,
+               // 2 smem box + coalesced st.global (bf16 output on a peer GPU: NVLink writes)
   // stream-K tail (pair kernel): tiles [0, sk_full) run data-parallel, one per
   // cluster per round; the sk_W = (tiles - sk_full) * kblocks k-block iterations
   // of the last, partial round are split evenly over all clusters.  A tile split
@@ -262,6 +263,25 @@ __device__ __forceinline__ void stage_row_sw128(uint8_t* box, int lane, const ui
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[4 * j]), "r"(w[4 * j + 1]),
                  "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
                  : "memory");
+  }
+}
+
+// Copy a warp's staged SWIZZLE_128B box (32 rows x 128 B) to global memory with
+// coalesced 16-byte stores: 8 lanes cover one 128-byte row segment, so each warp
+// instruction writes 4 whole row segments (what NVLink peer writes want; the
+// per-thread path writes 32 rows x 16 B per instruction).
+__device__ __forceinline__ void box_store_coalesced(const uint8_t* box, int lane, char* gbase, long long ld_bytes,
+                                                    int rows_valid, int bytes_valid) {
+  const int c16 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i;
+    if (r < rows_valid && c16 * 16 < bytes_valid) {
+      uint4 v;
+      const uint32_t a = sm100::smem_u32(box + r * 128 + ((c16 ^ (r & 7)) << 4));
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+      *reinterpret_cast<uint4*>(gbase + (long long)r * ld_bytes + c16 * 16) = v;
+    }
   }
 }
 
@@ -750,10 +770,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (EPI == EPI_BIAS_GELU) stage_row_sw128(wbuf + 4096, lane, w2);
           sm100::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            sm100::tma_store_2d(&tmC, box, col, row0);
-            if (EPI == EPI_BIAS_GELU) sm100::tma_store_2d(&tmC2, wbuf + 4096, col, row0);
-            sm100::bulk_commit();
+          if (g.tma_st == 1) {
+            if (lane == 0) {
+              sm100::tma_store_2d(&tmC, box, col, row0);
+              if (EPI == EPI_BIAS_GELU) sm100::tma_store_2d(&tmC2, wbuf + 4096, col, row0);
+              sm100::bulk_commit();
+            }
+          } else {   // peer-GPU destination: coalesced generic stores from the box
+            const int rv = min(32, g.M - row0), bv = min(128, (g.N - col) * 2);
+            box_store_coalesced(box, lane, reinterpret_cast<char*>(g.C) + ((long long)row0 * g.ldc + col) * 2,
+                                g.ldc * 2, rv, bv);
+            if (EPI == EPI_BIAS_GELU)
+              box_store_coalesced(wbuf + 4096, lane,
+                                  reinterpret_cast<char*>(g.C2) + ((long long)row0 * g.ldc2 + col) * 2,
+                                  g.ldc2 * 2, rv, bv);
+            __syncwarp();
           }
           ++unit;
         }
@@ -994,11 +1025,15 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
     return a.type == cudaMemoryTypeDevice && a.device == dev;
   };
-  if (use_pair() && use_tma_store() && g.vec && local(C) && (!C2 || local(C2))) {
-    const bool f32 = (epi == EPI_ACC_F32 || epi == EPI_F32);
-    bool ok = make_map(&tc, C, M, N, ldc, f32 ? 32 : 64, 32, f32) == RRFP_OK;
-    if (ok && epi == EPI_BIAS_GELU) ok = make_map(&tc2, C2, M, N, ldc2, 64, 32) == RRFP_OK;
-    g.tma_st = ok ? 1 : 0;
+  const bool f32 = (epi == EPI_ACC_F32 || epi == EPI_F32);
+  if (use_pair() && use_tma_store() && g.vec) {
+    if (g_tma_store != 2 && local(C) && (!C2 || local(C2))) {
+      bool ok = make_map(&tc, C, M, N, ldc, f32 ? 32 : 64, 32, f32) == RRFP_OK;
+      if (ok && epi == EPI_BIAS_GELU) ok = make_map(&tc2, C2, M, N, ldc2, 64, 32) == RRFP_OK;
+      g.tma_st = ok ? 1 : 0;
+    } else if (!f32) {
+      g.tma_st = 2;
+    }
   }
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
@@ -1026,7 +1061,7 @@ extern "C" int rrfp_gemm_set_streamk(int on) {
 
 // 1 = smem-staged TMA store / reduce-add epilogue, 0 = per-thread global stores
 extern "C" int rrfp_gemm_set_epilogue(int tma_store) {
-  g_tma_store = tma_store ? 1 : 0;
+  g_tma_store = tma_store < 0 ? 0 : tma_store;
   return RRFP_OK;
 }
 

@@ -5,8 +5,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 1), (1, 0), (0, 0)], ids=["pair-tma-store", "pair-st-global", "single"],
-                autouse=True)
+@pytest.fixture(params=[(1, 1), (1, 2), (1, 0), (0, 0)],
+                ids=["pair-tma-store", "pair-staged-coalesced", "pair-st-global", "single"], autouse=True)
 def variant(request):
     from paper_2605_18750_b200 import _lib
     pair, tma = request.param

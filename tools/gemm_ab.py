@@ -15,7 +15,7 @@ calls = bench.roofline_gemm_calls(GPTConfig())
 L = _lib.lib()
 def setv(tma, sk):
     return lambda: (L.rrfp_gemm_set_epilogue(tma), L.rrfp_gemm_set_streamk(sk))
-variants = [("tma+streamK", setv(1, 1)), ("tma, DP only", setv(1, 0)), ("st.global+streamK", setv(0, 1))]
+variants = [("tma store", setv(1, 0)), ("staged coalesced", setv(2, 0)), ("per-thread st", setv(0, 0))]
 res = {}
 for vname, setv in variants:
     setv()
