@@ -305,6 +305,12 @@ def run_ours(args):
     pipe, stages = build_pipe(cfg, args, hint, mode, world, PRESETS[args.jitter])
     t_build = time.perf_counter() - t_build
     _log(f"built in {t_build:.1f}s")
+    clock_cal = None
+    if dist:   # cross-GPU %globaltimer offsets, so the gathered trace is on one clock
+        off, rtt = pipe.calibrate_clocks()
+        allc = [None] * world
+        dist.all_gather_object(allc, (off, rtt))
+        clock_cal = {"offset_ns_vs_rank0": [c[0] for c in allc], "best_rtt_ns": [c[1] for c in allc]}
     # the step's input data held by this rank's stages (tokens / image patches /
     # targets): copied from pinned host memory every step of the e2e loop
     inputs = []
@@ -401,6 +407,7 @@ def run_ours(args):
             "gpu_launches": int(launches) * args.steps,
             "gpu_launches_per_step": int(launches),
             "build_s": round(t_build, 1),
+            "clock_calibration": clock_cal,
             "clocks": clk.summary()}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
@@ -506,7 +513,7 @@ def gather_trace(pipe, dist, world):
     ev, t0n = pipe.last_events
     if dist:
         allev = [None] * world
-        dist.all_gather_object(allev, ([(e.t0, e.t1, e.kind, e.stage, e.rank, e.task) for e in ev], t0n))
+        dist.all_gather_object(allev, pipe.aligned_events())   # one clock: rank 0's
         ev = []
         for lst, _ in allev:
             for t in lst:
@@ -558,6 +565,8 @@ def compare_variants(cfg, args, world, dist, barrier):
         if world == 1 and name == "bfw" and cfg.n_layer * args.mb > 8 * 32:
             continue          # PP=1 BFW keeps every W pending: memory-bound, meaningless
         pipe, stages = build_pipe(cfg, args, hint, mode, world, jit)
+        if dist:
+            pipe.calibrate_clocks()
         for _ in range(2):
             pipe.step()
         nominal = pipe.nominal_us()

@@ -208,6 +208,15 @@ int rrfp_tp_allreduce(rrfp_tp* t, int rows, int cols, const void* bias, const vo
 /* *err = 1 if a peer wait timed out (20 s) since creation */
 int rrfp_tp_error(rrfp_tp* t, int* err);
 void rrfp_tp_destroy(rrfp_tp* t);
+
+/* Cross-GPU %globaltimer calibration for wall traces (replaces the single
+ * process clock the reference's validate_trace assumes, validate.py:117-131):
+ * NTP-style ping-pong over peer memory between two ranks' 16-byte slots
+ * (cudaMalloc'd, IPC-exchanged).  role 0 (initiator) returns offset = peer
+ * clock - own clock and the best round trip; role 1 responds.  Round ids are
+ * base+1..base+rounds, growing across calls on a slot.  Blocking. */
+int rrfp_clock_pingpong(void* mine, void* peer, int role, int rounds, long long base, long long* offset_ns,
+                        long long* rtt_ns);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */

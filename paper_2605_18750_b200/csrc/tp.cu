@@ -239,3 +239,66 @@ extern "C" void rrfp_tp_destroy(rrfp_tp* t) {
   cudaFree(t->seq);
   delete t;
 }
+
+// ------------------------------------------------------------------------
+// Cross-GPU %globaltimer calibration (wall traces from
+// several GPUs on one clock, so validate_trace precedence (validate.py:117-131)
+// and the breakdown can run on them).  NTP-style ping-pong between two
+// single-thread kernels over peer memory: the initiator stamps t0, the
+// responder answers with its own timer t_r, the initiator stamps t1;
+// offset = t_r - (t0 + t1) / 2 of the round with the smallest t1 - t0.
+// slot layout (u64): [0] round, [1] responder stamp.
+namespace {
+__global__ void clock_pingpong_kernel(unsigned long long* mine, unsigned long long* peer, int role, int rounds,
+                                      unsigned long long base, long long* out) {
+  if (threadIdx.x != 0) return;
+  long long best_rtt = -1, best_off = 0;
+  for (int i = 1; i <= rounds; ++i) {
+    const unsigned long long want = base + i;
+    const unsigned long long t_start = now_ns();
+    if (role == 0) {
+      const unsigned long long t0 = now_ns();
+      st_release_sys64(&peer[0], want);
+      while (ld_acquire_sys64(&mine[0]) < want) {
+        if (now_ns() - t_start > 5000000000ull) { out[2] = -1; return; }
+      }
+      const unsigned long long t1 = now_ns();
+      const long long tr = (long long)ld_acquire_sys64(&mine[1]);
+      const long long rtt = (long long)(t1 - t0);
+      if (best_rtt < 0 || rtt < best_rtt) { best_rtt = rtt; best_off = tr - (long long)((t0 + t1) / 2); }
+    } else {
+      while (ld_acquire_sys64(&mine[0]) < want) {
+        if (now_ns() - t_start > 5000000000ull) { out[2] = -1; return; }
+      }
+      peer[1] = now_ns();
+      __threadfence_system();
+      st_release_sys64(&peer[0], want);
+    }
+  }
+  out[0] = best_off;
+  out[1] = best_rtt;
+  out[2] = 0;
+}
+}  // namespace
+
+// role 0: initiator (reference clock) -> *offset_ns = peer clock - my clock,
+// *rtt_ns = best round trip; role 1: responder.  `mine` / `peer` are 16-byte
+// slots (own memory / the other GPU's slot through IPC); round ids are
+// base+1 .. base+rounds and must grow from call to call on a slot (both sides
+// pass the same base).  Blocks until done.
+extern "C" int rrfp_clock_pingpong(void* mine, void* peer, int role, int rounds, long long base,
+                                   long long* offset_ns, long long* rtt_ns) {
+  if (!mine || !peer || rounds < 1) return rrfp_fail(RRFP_E_INVALID, "clock ping-pong: bad arguments");
+  long long* out = nullptr;
+  RRFP_CUDA_TRY(cudaMalloc(&out, 3 * sizeof(long long)));
+  clock_pingpong_kernel<<<1, 32>>>((unsigned long long*)mine, (unsigned long long*)peer, role, rounds,
+                                   (unsigned long long)base, out);
+  RRFP_CUDA_TRY(cudaGetLastError());
+  long long h[3];
+  RRFP_CUDA_TRY(cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(out);
+  if (h[2] != 0) return rrfp_fail(RRFP_E_CUDA, "clock ping-pong timed out (peer not running?)");
+  if (offset_ns) *offset_ns = role == 0 ? h[0] : 0;
+  if (rtt_ns) *rtt_ns = role == 0 ? h[1] : 0;
+  return RRFP_OK;
+}

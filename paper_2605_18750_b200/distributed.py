@@ -132,6 +132,8 @@ class DistPipeline:
         if R > 1:
             from .tp import TpComm
             self.comm = TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", self.device))
+        self.clock_slot = IpcBuffer(16, self.device)      # cross-GPU timer calibration
+        self.clock_offset_ns = 0                          # this rank's clock - rank 0's clock
         self.vstages = []
         for v in self.vids:
             fb, bb = self.bufs[(v, "fwd")], self.bufs[(v, "bwd")]
@@ -158,10 +160,13 @@ class DistPipeline:
         mine = {"stage": s, "tp_rank": r,
                 "mbox": {v: (hd(self.bufs[(v, "fwd")]), hd(self.bufs[(v, "bwd")]), shapes[v]) for v in self.vids},
                 "lane": self.group.ipc_handles()[(s, r)],
-                "tp": self.comm.ipc_handles() if self.comm else None}
+                "tp": self.comm.ipc_handles() if self.comm else None,
+                "clock": self.clock_slot.handle()}
         allh = [None] * self.gworld
         dist.all_gather_object(allh, mine, group=group)
         by = {(h["stage"], h["tp_rank"]): h for h in allh}
+        self._clock_peers = [h["clock"] for h in allh]     # by global rank
+        self._group = group
         if self.comm:
             self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
 
@@ -193,6 +198,43 @@ class DistPipeline:
         # every rank instantiates + uploads its lane graph before ANY rank launches
         self.group.prepare()
         dist.barrier(group=group)
+
+    def calibrate_clocks(self, rounds: int = 16):
+        """Offsets of every rank's %globaltimer against rank 0's (ping-pong over
+        peer memory, one pair at a time); afterwards ``clock_offset_ns`` maps this
+        rank's device timestamps onto rank 0's clock (subtract it).  Collective.
+        Returns (offset_ns, best_rtt_ns) of this rank ((0, 0) on rank 0)."""
+        import ctypes as C
+        import torch.distributed as dist
+        L = _lib.lib()
+        me = self.grank
+        measured = {}
+        for peer in range(1, self.gworld):
+            dist.barrier(group=self._group)
+            if me not in (0, peer):
+                continue
+            other = peer if me == 0 else 0
+            opened = self.__dict__.setdefault("_clock_opened", {})
+            if other not in opened:
+                opened[other] = open_handle(self._clock_peers[other])
+            ptr = opened[other]
+            o, t = C.c_longlong(), C.c_longlong()
+            _lib.check(L.rrfp_clock_pingpong(self.clock_slot.ptr, C.c_void_p(ptr), 0 if me == 0 else 1, rounds,
+                                             C.c_longlong(peer * (rounds + 1)), C.byref(o), C.byref(t)))
+            if me == 0:
+                measured[peer] = (o.value, t.value)
+        table = [measured if me == 0 else None]       # rank 0 hands every rank its offset
+        dist.broadcast_object_list(table, src=0, group=self._group)
+        off, rtt = table[0].get(me, (0, 0))
+        self.clock_offset_ns = off
+        return off, rtt
+
+    def aligned_events(self):
+        """The last iteration's device events as tuples (t0, t1, kind, stage, rank,
+        task) on rank 0's clock (see calibrate_clocks), and the aligned t0."""
+        ev, t0 = self.last_events
+        d = self.clock_offset_ns
+        return [(e.t0 - d, e.t1 - d, e.kind, e.stage, e.rank, e.task) for e in ev], t0 - d
 
     def nominal_us(self, group=None):
         """Per-stage mean F/B/W durations (µs) of the last iteration, gathered

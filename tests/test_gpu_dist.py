@@ -38,3 +38,25 @@ def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks, 
             assert abs(l - ref) / ref < 1e-2, (l, ref)
     per_stage = 4 * chunks * (3 if hint == "bfw" else 2)
     assert all(r["n_exec"] == per_stage and r["tp_err"] == 0 for r in res["ranks"])
+    # wall trace over all processes on rank 0's clock (ping-pong calibration):
+    # precedence / exclusivity / completeness of validate_trace hold (task
+    # durations are real kernel times, not the nominal table: "duration" is skipped)
+    import rrfp_oracle as O
+    from paper_2605_18750_b200 import _lib
+    from paper_2605_18750_b200.runtime import wall_trace
+    from paper_2605_18750_b200.workload import Workload
+    for r in res["ranks"]:
+        assert r["rank"] == 0 or abs(r["clock"][0]) <= max(r["clock"][1], 20_000), r["clock"]  # one GPU: ~0
+    evs = []
+    for r in res["ranks"]:
+        for t in r["events"][0]:
+            e = _lib.Event()
+            e.t0, e.t1, e.kind, e.stage, e.rank, e.task = t
+            evs.append(e)
+    w = Workload.from_json(res["workload"])
+    tr, _ = wall_trace(w, evs, min(r["events"][1] for r in res["ranks"]))
+    tup = [(e.t_start, e.t_end, e.stage, e.rank, e.microbatch, e.chunk, e.direction, e.event_kind)
+           for e in tr.events]
+    viol = [v for v in O.validate(tup, O.from_workload_json(res["workload"]), slack=(5, 1.05, 400),
+                                  clock="wall") if v[0] != "duration"]
+    assert not viol, viol[:5]

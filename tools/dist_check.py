@@ -44,16 +44,20 @@ def main():
         losses.append(None if loss is None else loss.item())
     ev, t0 = pipe.last_events
     n_exec = sum(1 for e in ev if e.kind == 0)
-    out = [None] * world
+    off, rtt = pipe.calibrate_clocks()
+    aligned = pipe.aligned_events()
+    out = [None] * world   # (pipe is kept for its workload description)
     tp_err = pipe.comm.error() if pipe.comm else 0
-    dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec, "tp_err": tp_err})
+    dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec, "tp_err": tp_err,
+                                 "clock": [off, rtt], "events": aligned})
     pipe.close()
     if rank == 0:
         from paper_2605_18750_b200.pipeline import GpuPipeline
         ref = GpuPipeline(cfg, world // tp if mm else 1, 4, hint=hint, mm=mm)
         ref_loss = ref.step().item()
         ref.close()
-        print(json.dumps({"ranks": out, "single_process_pp1_loss": ref_loss}), flush=True)
+        print(json.dumps({"ranks": out, "single_process_pp1_loss": ref_loss,
+                          "workload": pipe.workload.to_json()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
