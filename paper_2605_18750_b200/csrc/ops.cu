@@ -43,9 +43,31 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
 }
 
 // ------------------------------------------------------------- LayerNorm
+// One CTA per row, D/8 threads (one 16-byte chunk of x / dy / g each): every
+// load is issued up front, 8+ CTAs per SM keep enough bytes in flight to run at
+// HBM/L2 speed (the previous warp-per-row kernels held a whole row per thread
+// group in ~150 registers: one CTA per SM, latency-bound).
+
+// sum of a and b over the CTA (warp shuffles, then one smem exchange)
+__device__ __forceinline__ void block_sum2(float& a, float& b, float* sh) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0) { sh[w] = a; sh[32 + w] = b; }
+  __syncthreads();
+  float ta = 0.f, tb = 0.f;
+  for (int i = 0; i < nw; ++i) { ta += sh[i]; tb += sh[32 + i]; }
+  a = ta;
+  b = tb;
+  __syncthreads();   // sh may be reused by the caller
+}
+
+// Forward: one WARP per row (the row in registers, no CTA barrier): measured
+// faster than the row-per-CTA form, whose two CTA reductions cost more than
+// they save on a 16 MB pass.
 // y = (x - mean) * rstd * g + b; one warp per row; D = 256 * NV.
 template <int NV>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* __restrict__ x,
                                                      const __nv_bfloat16* __restrict__ g,
                                                      const __nv_bfloat16* __restrict__ b,
                                                      __nv_bfloat16* __restrict__ y,
@@ -87,66 +109,39 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   if (lane == 0) { mean_out[warp] = mean; rstd_out[warp] = rstd; }
 }
 
+
 // dx = rstd * (dxh - xhat * mean(dxh * xhat) - mean(dxh)) + dres, dxh = dy * g
-// One warp per row, the row held in registers (single pass over x, dy).
-template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
+__global__ void __launch_bounds__(1024) ln_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
     const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
-    __nv_bfloat16* __restrict__ dx, int rows) {
+    __nv_bfloat16* __restrict__ dx, int D) {
+  __shared__ float sh[64];
   sm100::griddep_launch();
   sm100::griddep_wait();
-  constexpr int D = 256 * NV;
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (row >= rows) return;
+  const int row = blockIdx.x, c = threadIdx.x * 8;
+  const size_t off = (size_t)row * D + c;
+  float xv[8], dv[8], gv[8], rv[8];
+  load8(x + off, xv);
+  load8(dy + off, dv);
+  load8(g + c, gv);
+  if (dres) load8(dres + off, rv);
   const float mean = mean_in[row], rstd = rstd_in[row];
-  const __nv_bfloat16* xr = x + (size_t)row * D;
-  const __nv_bfloat16* dr = dy + (size_t)row * D;
-  // the row stays in registers as packed bf16 (2 x NV x 16 B); all loads issued up front
-  uint4 xq[NV], dq[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = (i * 32 + lane) * 8;
-    xq[i] = *reinterpret_cast<const uint4*>(xr + c);
-    dq[i] = *reinterpret_cast<const uint4*>(dr + c);
-  }
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = (i * 32 + lane) * 8;
-    float gv[8];
-    load8(g + c, gv);
-    const __nv_bfloat162* xh2 = reinterpret_cast<const __nv_bfloat162*>(&xq[i]);
-    const __nv_bfloat162* dh2 = reinterpret_cast<const __nv_bfloat162*>(&dq[i]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 xv = __bfloat1622float2(xh2[j]), dv = __bfloat1622float2(dh2[j]);
-      const float xa = (xv.x - mean) * rstd, xb = (xv.y - mean) * rstd;
-      const float da = dv.x * gv[2 * j], db = dv.y * gv[2 * j + 1];
-      s1 += da * xa + db * xb;
-      s2 += da + db;
-    }
+  for (int j = 0; j < 8; ++j) {
+    xv[j] = (xv[j] - mean) * rstd;   // xhat
+    dv[j] *= gv[j];                  // dxh
+    s1 += dv[j] * xv[j];
+    s2 += dv[j];
   }
-  s1 = warp_sum(s1) * (1.f / D);
-  s2 = warp_sum(s2) * (1.f / D);
+  block_sum2(s1, s2, sh);
+  s1 *= 1.f / D;
+  s2 *= 1.f / D;
+  float o[8];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = (i * 32 + lane) * 8;
-    float gv[8], o[8], rv[8];
-    load8(g + c, gv);
-    if (dres) load8(dres + (size_t)row * D + c, rv);
-    const __nv_bfloat162* xh2 = reinterpret_cast<const __nv_bfloat162*>(&xq[i]);
-    const __nv_bfloat162* dh2 = reinterpret_cast<const __nv_bfloat162*>(&dq[i]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 xv = __bfloat1622float2(xh2[j]), dv = __bfloat1622float2(dh2[j]);
-      const float xa = (xv.x - mean) * rstd, xb = (xv.y - mean) * rstd;
-      o[2 * j] = rstd * (dv.x * gv[2 * j] - xa * s1 - s2) + (dres ? rv[2 * j] : 0.f);
-      o[2 * j + 1] = rstd * (dv.y * gv[2 * j + 1] - xb * s1 - s2) + (dres ? rv[2 * j + 1] : 0.f);
-    }
-    store8(dx + (size_t)row * D + c, o);
-  }
+  for (int j = 0; j < 8; ++j) o[j] = rstd * (dv[j] - xv[j] * s1 - s2) + (dres ? rv[j] : 0.f);
+  store8(dx + off, o);
 }
 
 // dg[c] += sum_r dy[r,c] * (x[r,c]-mean[r])*rstd[r];  db[c] += sum_r dy[r,c]
@@ -348,26 +343,32 @@ __global__ void copy_rows_kernel(char* __restrict__ dst, long long ldd, const ch
 
 }  // namespace
 
-#define LAUNCH_NV(KERNEL, D, ...)                                                          \
-  if ((D) % 256) return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d not a multiple of 256", (int)(D)); \
-  switch ((D) / 256) {                                                                     \
-    case 1: RRFP_CUDA_TRY(rrfp_launch(KERNEL<1>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 2: RRFP_CUDA_TRY(rrfp_launch(KERNEL<2>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 3: RRFP_CUDA_TRY(rrfp_launch(KERNEL<3>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 4: RRFP_CUDA_TRY(rrfp_launch(KERNEL<4>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 5: RRFP_CUDA_TRY(rrfp_launch(KERNEL<5>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 6: RRFP_CUDA_TRY(rrfp_launch(KERNEL<6>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 8: RRFP_CUDA_TRY(rrfp_launch(KERNEL<8>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    case 16: RRFP_CUDA_TRY(rrfp_launch(KERNEL<16>, grid, dim3(256), 0, st, __VA_ARGS__)); break; \
-    default: return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported", (int)(D)); \
-  }
+// LayerNorm widths: multiples of 256 up to 8192 (D/8 threads per row-CTA)
+static int ln_width_ok(int D) {
+  if (D < 256 || D > 8192 || D % 256)
+    return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported (multiple of 256, <= 8192)", D);
+  return RRFP_OK;
+}
 
 extern "C" int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean,
                                   float* rstd, int rows, int D, float eps, void* stream) {
+  if (int rc = ln_width_ok(D)) return rc;
+  if (rows <= 0) return RRFP_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid((rows + 7) / 8);
-  LAUNCH_NV(ln_fwd_kernel, D, (const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
-            (const __nv_bfloat16*)b, (__nv_bfloat16*)y, mean, rstd, rows, eps);
+  const dim3 grid((rows + 7) / 8), block(256);
+  const __nv_bfloat16 *xx = (const __nv_bfloat16*)x, *gg = (const __nv_bfloat16*)g, *bb = (const __nv_bfloat16*)b;
+  __nv_bfloat16* yy = (__nv_bfloat16*)y;
+  switch (D / 256) {
+    case 1: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<1>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 2: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<2>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 3: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<3>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 4: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<4>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 5: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<5>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 6: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<6>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 8: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<8>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    case 16: RRFP_CUDA_TRY(rrfp_launch(ln_fwd_warp_kernel<16>, grid, block, 0, st, xx, gg, bb, yy, mean, rstd, rows, eps)); break;
+    default: return rrfp_fail(RRFP_E_INVALID, "LayerNorm width %d unsupported", D);
+  }
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }
@@ -376,10 +377,11 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
                                   const void* g, const void* dres, void* dx, float* dg, float* db,
                                   int rows, int D, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid((rows + 7) / 8);
-  if (D > 4096) return rrfp_fail(RRFP_E_INVALID, "LayerNorm bwd width %d too large", D);
-  LAUNCH_NV(ln_bwd_dx_kernel, D, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd,
-            (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, rows);
+  if (int rc = ln_width_ok(D)) return rc;
+  if (rows <= 0) return RRFP_OK;
+  RRFP_CUDA_TRY(rrfp_launch(ln_bwd_dx_kernel, dim3(rows), dim3(D / 8), 0, st, (const __nv_bfloat16*)dy,
+                            (const __nv_bfloat16*)x, mean, rstd, (const __nv_bfloat16*)g,
+                            (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, D));
   RRFP_CUDA_TRY(cudaGetLastError());
   if (dg || db) {
     const int rpb = 64;

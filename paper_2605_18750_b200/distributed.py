@@ -161,11 +161,13 @@ class DistPipeline:
                 "mbox": {v: (hd(self.bufs[(v, "fwd")]), hd(self.bufs[(v, "bwd")]), shapes[v]) for v in self.vids},
                 "lane": self.group.ipc_handles()[(s, r)],
                 "tp": self.comm.ipc_handles() if self.comm else None,
-                "clock": self.clock_slot.handle()}
+                "clock": self.clock_slot.handle(),
+                "gpu_uuid": str(torch.cuda.get_device_properties(self.device).uuid)}
         allh = [None] * self.gworld
         dist.all_gather_object(allh, mine, group=group)
         by = {(h["stage"], h["tp_rank"]): h for h in allh}
         self._clock_peers = [h["clock"] for h in allh]     # by global rank
+        self._gpu_uuid = [h["gpu_uuid"] for h in allh]
         self._group = group
         if self.comm:
             self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
@@ -199,19 +201,25 @@ class DistPipeline:
         self.group.prepare()
         dist.barrier(group=group)
 
-    def calibrate_clocks(self, rounds: int = 16):
+    def calibrate_clocks(self, rounds: int = 16, force: bool = False):
         """Offsets of every rank's %globaltimer against rank 0's (ping-pong over
         peer memory, one pair at a time); afterwards ``clock_offset_ns`` maps this
         rank's device timestamps onto rank 0's clock (subtract it).  Collective.
+        Ranks on the same GPU share one timer (offset 0) unless ``force`` (tests).
         Returns (offset_ns, best_rtt_ns) of this rank ((0, 0) on rank 0)."""
         import ctypes as C
         import torch.distributed as dist
         L = _lib.lib()
         me = self.grank
         measured = {}
+        calls = self._clock_calls = getattr(self, "_clock_calls", 0) + 1   # same count on every rank
         for peer in range(1, self.gworld):
             dist.barrier(group=self._group)
             if me not in (0, peer):
+                continue
+            if not force and self._gpu_uuid[peer] == self._gpu_uuid[0]:   # same GPU: one timer
+                if me == 0:
+                    measured[peer] = (0, 0)
                 continue
             other = peer if me == 0 else 0
             opened = self.__dict__.setdefault("_clock_opened", {})
@@ -219,8 +227,9 @@ class DistPipeline:
                 opened[other] = open_handle(self._clock_peers[other])
             ptr = opened[other]
             o, t = C.c_longlong(), C.c_longlong()
+            base = (calls * self.gworld + peer) * (rounds + 1)   # round ids grow on every slot
             _lib.check(L.rrfp_clock_pingpong(self.clock_slot.ptr, C.c_void_p(ptr), 0 if me == 0 else 1, rounds,
-                                             C.c_longlong(peer * (rounds + 1)), C.byref(o), C.byref(t)))
+                                             C.c_longlong(base), C.byref(o), C.byref(t)))
             if me == 0:
                 measured[peer] = (o.value, t.value)
         table = [measured if me == 0 else None]       # rank 0 hands every rank its offset
