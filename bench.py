@@ -418,6 +418,22 @@ def run_ours(args):
             line["pipeline_model"] = {"error": repr(e)[:200]}
     pipe.close()
     del pipe, stages, inputs
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    if args.emulate_pp > 1 and world == 1:
+        # a fresh process: the PP=1 pipeline's ~110 GB must not share the GPU with it
+        cmd = [sys.executable, os.path.abspath(__file__), "--emulate-only", "--emulate-pp", str(args.emulate_pp),
+               "--steps", str(args.steps), "--warmup", str(args.warmup), "--mb", str(args.mb),
+               "--sigmas", args.sigmas, "--compare-jitter", args.compare_jitter, "--comm-us", str(args.comm_us),
+               "--head-cost", str(args.head_cost), "--model", args.model]
+        if args.layers:
+            cmd += ["--layers", str(args.layers)]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        sys.stderr.write(p.stderr[-4000:])
+        lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+        line["emulated_pp"] = json.loads(lines[-1]) if (p.returncode == 0 and lines) else \
+            {"error": f"rc={p.returncode}: {p.stderr[-300:]}"}
     if args.compare or (world > 1 and args.compare is None):
         line["variants"] = compare_variants(cfg, args, world, dist, barrier)
     if rank == 0:
@@ -503,6 +519,73 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
                 res[name]["speedup_vs_1f1b"] = round(res["1f1b"]["ms"] / res[name]["ms"], 4)
             row[f"sigma{sigma}"] = res
         out[f"pp{n}"] = row
+    return out
+
+
+def emulated_pp(args, cfg):
+    """PP=N on ONE B200 (opt-in, --emulate-pp N): N device lanes in this process,
+    each stage's GEMM grids confined to 148/N SMs (the stage's share of the GPU;
+    the GEMMs are 72 % of the step), mailboxes in local memory.  Same kernels,
+    same dispatcher, same injected jitter as the multi-GPU run; 1F1B vs BF vs
+    BFW at every --sigmas value.  An emulation: idle stages lend their SMs to
+    the other stages' non-GEMM kernels, so bubbles cost less than on separate
+    GPUs (1F1B is flattered, not RRFP)."""
+    import gc
+    import math
+    import torch
+    from paper_2605_18750_b200.jitter import PRESETS
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from paper_2605_18750_b200.runtime import wall_trace
+    from paper_2605_18750_b200.workload import CommDelay
+    N = args.emulate_pp
+    cap = (torch.cuda.get_device_properties(0).multi_processor_count // N) & ~1
+    sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
+    out = {"n_stages": N, "gemm_sm_cap": cap, "definition": emulated_pp.__doc__.split("\n\n")[0]
+           .replace("\n", " ").replace("    ", " "), "variants": {}}
+    cur = torch.cuda.current_stream()
+    for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
+        t0 = time.perf_counter()
+        pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.compare_jitter],
+                           head_cost=args.head_cost, gemm_sm_cap=cap)
+        build_s = time.perf_counter() - t0
+        for _ in range(2):
+            pipe.step()
+        nominal = pipe.nominal_us()
+        for sigma in sigmas:
+            comm = CommDelay()
+            if sigma > 0:
+                comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
+                                 hi=int(args.comm_us * 50), seed=17)
+            pipe.group.set_comm_delay(comm)
+            pipe.set_lognormal_jitter(sigma, seed=11, nominal_us=nominal)
+            pipe.step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            for _ in range(args.steps):
+                pipe.launch()
+                pipe.wait()
+            for st in pipe.group.streams.values():
+                cur.wait_stream(st)
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            tr, met = pipe.trace()
+            out["variants"][f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
+                "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
+                "bubble_fraction": round(met.bubble_fraction(), 4), "build_s": round(build_s, 1)}
+            _log(f"emulated PP={N} {name} sigma={sigma}: {ms:.1f} ms")
+        pipe.close()
+        del pipe
+        gc.collect()
+        torch.cuda.empty_cache()
+    v = out["variants"]
+    for sigma in sigmas:
+        base = v.get(f"1f1b@{args.compare_jitter}+sigma{sigma}")
+        for name in ("bf", "bfw"):
+            x = v.get(f"{name}@{args.compare_jitter}+sigma{sigma}")
+            if base and x:
+                x["speedup_vs_1f1b"] = round(base["ms"] / x["ms"], 4)
     return out
 
 
@@ -652,7 +735,16 @@ def main():
     ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0",
                     help="J-preset jitter table (jitter.py PRESETS) applied to every comparison variant")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
+    ap.add_argument("--emulate-only", dest="emulate_only", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=0,
+                    help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "
+                         "1F1B vs BF vs BFW at every --sigmas")
     args = ap.parse_args()
+    if args.emulate_only:
+        import torch
+        torch.cuda.set_device(0)
+        print(json.dumps(emulated_pp(args, model_config(args))), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

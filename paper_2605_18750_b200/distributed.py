@@ -303,3 +303,11 @@ class DistPipeline:
         if self.comm:
             self.comm.close()
             self.comm = None
+        for st in self.vstages or []:
+            st.release()
+        self.vstages = []
+        self.stage = None
+        for b in self.bufs.values():
+            if b is not None:
+                b.free()
+        self.bufs = {}

@@ -352,6 +352,7 @@ class StageCompute:
             self.gx0 = e(n_mb, S, D) if self.prologue else None
         self.graphs = {}
         self.kernel_counts = {}   # (kind, mb) -> our kernel launches in that body
+        self.gemm_sm_cap = 0      # > 0: GEMM grids confined to this many SMs (see run_task)
 
     # ------------------------------------------------------------ wiring
     def connect_outputs(self, fwd_out=None, bwd_out=None):
@@ -698,6 +699,15 @@ class StageCompute:
         join.record(side)
         main.wait_event(join)
 
+    def release(self):
+        """Drop every device buffer and captured graph now (a pipeline's stages
+        hold ~100 GB at PP=1; bench builds several pipelines in one process)."""
+        self.graphs.clear()
+        self.attn_aux = self.o_view = None
+        for k in list(vars(self)):
+            if isinstance(getattr(self, k), (torch.Tensor, list, dict)) and k not in ("layers", "rows", "T_v"):
+                setattr(self, k, None)
+
     def zero_grads(self):
         extra = [d for d in (self.g_emb, self.g_head, self.g_pe, self.g_proj) if d]
         for gd in self.g + extra:
@@ -708,12 +718,23 @@ class StageCompute:
 
     # ----------------------------------------------------------- capture
     def run_task(self, kind: str, mb: int):
-        if kind == "F":
-            self.forward(mb)
-        elif kind == "B":
-            self.backward_input(mb)
-        else:
-            self.backward_weight(mb)
+        # GEMM grids of this stage's bodies are fixed at capture: an SM cap
+        # (gemm_sm_cap) confines them to that many SMs (several stages sharing
+        # one GPU as a PP emulation); 0 = the whole GPU
+        L = _lib.lib()
+        if self.gemm_sm_cap:
+            L.rrfp_gemm_reserve_sms(max(0, torch.cuda.get_device_properties(self.device).multi_processor_count
+                                        - self.gemm_sm_cap))
+        try:
+            if kind == "F":
+                self.forward(mb)
+            elif kind == "B":
+                self.backward_input(mb)
+            else:
+                self.backward_weight(mb)
+        finally:
+            if self.gemm_sm_cap:
+                L.rrfp_gemm_reserve_sms(0)
 
     def warmup(self, stream=None):
         """Run every body once eagerly (cuDNN plan selection, module loads,

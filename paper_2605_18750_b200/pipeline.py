@@ -95,7 +95,7 @@ class GpuPipeline:
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
                  schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
-                 n_chunks: int = 1, mm=None, head_cost: float = 0.0):
+                 n_chunks: int = 1, mm=None, head_cost: float = 0.0, gemm_sm_cap: int = 0):
         if mm is not None and (tp_size > 1 or n_chunks > 1):
             raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
         if isinstance(hint, str):
@@ -128,6 +128,9 @@ class GpuPipeline:
                                    mm=mm, head_cost=head_cost if C == 1 else 0.0)
                       for r in range(R)] for v in range(V)]
         self.stages = [row[0] for row in self.grid]
+        for row in self.grid:
+            for st in row:
+                st.gemm_sm_cap = gemm_sm_cap
         for v in range(V):
             for r in range(R):
                 nxt = self.grid[v + 1] if v + 1 < V else None
@@ -231,3 +234,7 @@ class GpuPipeline:
             for c in comms:
                 c.close()
         self.comms = {}
+        for row in self.grid or []:
+            for st in row:
+                st.release()
+        self.grid = self.stages = None
