@@ -551,6 +551,7 @@ def emulated_pp(args, cfg):
         for _ in range(2):
             pipe.step()
         nominal = pipe.nominal_us()
+        pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
         for sigma in sigmas:
             comm = CommDelay()
             if sigma > 0:
@@ -653,6 +654,7 @@ def compare_variants(cfg, args, world, dist, barrier):
         for _ in range(2):
             pipe.step()
         nominal = pipe.nominal_us()
+        pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
         for sigma in sigmas:
             comm = CommDelay()
             if sigma > 0:

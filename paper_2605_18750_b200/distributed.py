@@ -258,6 +258,18 @@ class DistPipeline:
         dist.all_gather_object(allv, mine, group=group)
         return allv[::self.R]
 
+    def set_nominal_latency(self, nominal_us):
+        """Per-stage measured F/B/W means (µs, e.g. from nominal_us()) become the
+        workload's latency table: the J-preset jitter pads then scale with the
+        real task times instead of the construction-time placeholders."""
+        from .workload import TaskId
+        lat = {}
+        for t in self.workload.latency:
+            v = nominal_us[t.stage].get(t.direction, 0.0)
+            lat[TaskId(t.stage, t.microbatch, t.chunk, t.direction)] = max(1, int(round(v)))
+        self.group.set_latency(lat)
+        self.workload = self.group.w
+
     def set_lognormal_jitter(self, sigma: float, seed: int = 0, nominal_us=None, group=None):
         """Lognormal compute jitter floors for THIS rank's stage; nominal task
         times are gathered from every rank's last iteration."""

@@ -89,6 +89,7 @@ class LaneGroup:
         tb = lower(workload, hint, buffer_limit, seed, jitter, tp)
         self.tables = tb
         self._seed, self._jitter, self._tp = seed, jitter, tp
+        self.compute_kind = compute_kind
         self.injected = tb.injected
         placement = placement or [[0] * r for _ in range(n)]
         self.local = local or [(s, k) for s in range(n) for k in range(r)]
@@ -181,6 +182,30 @@ class LaneGroup:
         for (s, k), h in self.lanes.items():
             dur, _, dskew, fixed, floor = self._tables[(s, k)]
             comm = np.ascontiguousarray(np.rint(tb.comm[s] * 1000.0 * self.scale).astype(np.int64))
+            self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
+            _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew), _ptr(fixed),
+                                                      _ptr(floor) if floor is not None else None))
+        self.w = w
+
+    def set_latency(self, latency: dict):
+        """Replace the workload's nominal per-task latencies (e.g. the measured
+        task times of the real bodies) and re-derive the J-preset jitter pads
+        from them (jitter.py:97-118: the injected delay scales with the
+        observed latency EMA), between iterations.  Real-body lanes only."""
+        from dataclasses import replace
+        if self.compute_kind != 1:
+            raise ValueError("set_latency is for lanes running real task bodies")
+        w = replace(self.w, latency=dict(latency))
+        tb = lower(w, self.hint, self.tables.desc.buffer_limit, self._seed, self._jitter, self._tp)
+        self.injected = tb.injected
+        mw = tb.desc.MW
+        for (s, k), h in self.lanes.items():
+            _, comm, dskew, fixed, floor = self._tables[(s, k)]
+            dur = np.zeros((3, tb.keys))
+            for t, v in self.injected.items():
+                if t.stage == s:
+                    dur[DIR_IDX[t.direction], key_of(t.microbatch, t.chunk, mw)] = v
+            dur = np.ascontiguousarray(np.rint(dur * 1000.0 * self.scale).astype(np.int64))
             self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew), _ptr(fixed),
                                                       _ptr(floor) if floor is not None else None))
