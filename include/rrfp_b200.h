@@ -269,6 +269,7 @@ int rrfp_gemm_set_streamk(int on);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                        int rows, int D, float eps, void* stream);
+/* layernorm_bwd: dx = NULL computes only the parameter gradients (dg, db += ...). */
 int rrfp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                        const void* g, const void* dres, void* dx, float* dg, float* db, int rows,
                        int D, void* stream);

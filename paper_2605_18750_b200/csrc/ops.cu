@@ -379,10 +379,12 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = ln_width_ok(D)) return rc;
   if (rows <= 0) return RRFP_OK;
-  RRFP_CUDA_TRY(rrfp_launch(ln_bwd_dx_kernel, dim3(rows), dim3(D / 8), 0, st, (const __nv_bfloat16*)dy,
-                            (const __nv_bfloat16*)x, mean, rstd, (const __nv_bfloat16*)g,
-                            (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, D));
-  RRFP_CUDA_TRY(cudaGetLastError());
+  if (dx) {   // dx == NULL: parameter gradients only (e.g. on a side stream)
+    RRFP_CUDA_TRY(rrfp_launch(ln_bwd_dx_kernel, dim3(rows), dim3(D / 8), 0, st, (const __nv_bfloat16*)dy,
+                              (const __nv_bfloat16*)x, mean, rstd, (const __nv_bfloat16*)g,
+                              (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, D));
+    RRFP_CUDA_TRY(cudaGetLastError());
+  }
   if (dg || db) {
     const int rpb = 64;
     dim3 g2((D + 255) / 256, (rows + rpb - 1) / rpb);
