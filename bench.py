@@ -738,9 +738,9 @@ def main():
                     help="J-preset jitter table (jitter.py PRESETS) applied to every comparison variant")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     ap.add_argument("--emulate-only", dest="emulate_only", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=0,
+    ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "
-                         "1F1B vs BF vs BFW at every --sigmas")
+                         "1F1B vs BF vs BFW at every --sigmas (default 8; 0 = off)")
     args = ap.parse_args()
     if args.emulate_only:
         import torch
