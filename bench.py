@@ -274,7 +274,7 @@ def gemm_roofline(cfg, peak_tf):
             "per_launch": f"mean over one layer's 10 F/B/W GEMMs ({cfg.seq} tokens, d={cfg.d_model}, "
                           f"ffn={cfg.d_ff}); CUDA events on the launch stream, 10 reps, in this process "
                           "after the timed region",
-            "share_of_step": "71.9% of device time (profiles/r01_bench_launches_summary.txt, ncu launch list)",
+            "share_of_step": "73.1% of device time (profiles/r01_bench_launches_summary_final.txt, ncu launch list)",
             "avg_launch_us": round(ms * 1e3, 1)}
 
 
