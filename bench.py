@@ -127,7 +127,7 @@ def run_reference(args):
         mks.append(mk)
     dt = (time.perf_counter() - t0) / args.steps
     v = 1.0 / dt
-    cores = len(os.sched_getaffinity(0))
+    cores = 3 * n     # threads run_live uses (sender / receiver / worker per stage); GIL-bound
     line = {"metric": METRIC, "value": round(v, 4), "unit": "iter/s", "impl": "reference",
             "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
@@ -135,7 +135,8 @@ def run_reference(args):
             "tokens_per_s": round(v * args.mb * 2048, 1),
             "config": workload_config(args, n),
             "cpu_baseline": {"value": round(v, 4), "unit": "iter/s", "cores": cores, "kind": "port",
-                             "sample": f"oracle.run_live: {3 * n} threads, {n}x{args.mb} tasks, "
+                             "sample": f"oracle.run_live: {3 * n} threads (GIL-bound; host has "
+                                       f"{len(os.sched_getaffinity(0))} cores), {n}x{args.mb} tasks, "
                                        f"task durations = B200-measured GPT-1.3B per-task times"},
             "e2e": {"value": round(v, 4), "unit": "iter/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
