@@ -279,31 +279,45 @@ __device__ __forceinline__ float block_reduce(float v, bool is_max, float* sh) {
   return r;
 }
 
+// single pass over the row: each thread keeps an online (max, sum-exp) pair,
+// rescaled once per 8-element chunk; pairs are merged across the CTA
 __global__ void __launch_bounds__(512) xent_fwd_kernel(const __nv_bfloat16* __restrict__ logits, long long ld,
                                                        const int32_t* __restrict__ target, int V,
                                                        float* __restrict__ loss, float* __restrict__ lse_out) {
   sm100::griddep_launch();
   sm100::griddep_wait();
-  __shared__ float sh[32];
+  __shared__ float shm[32], shs[32];
   const __nv_bfloat16* row = logits + (size_t)blockIdx.x * ld;
-  float m = -INFINITY;
+  float m = -INFINITY, s = 0.f;
   for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
     float f[8];
     load8(row + c, f);
+    float cm = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) if (c + j < V) m = fmaxf(m, f[j]);
-  }
-  m = block_reduce(m, true, sh);
-  float s = 0.f;
-  for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
-    float f[8];
-    load8(row + c, f);
+    for (int j = 0; j < 8; ++j) if (c + j < V) cm = fmaxf(cm, f[j]);
+    if (cm > m) { s *= __expf(m - cm); m = cm; }
 #pragma unroll
     for (int j = 0; j < 8; ++j) if (c + j < V) s += __expf(f[j] - m);
   }
-  s = block_reduce(s, false, sh);
+  // merge (m, s) pairs: warp, then across warps
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, om);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { shm[w] = m; shs[w] = s; }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const float lse = m + __logf(s);
+    float M = -INFINITY, Ssum = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      const float nm = fmaxf(M, shm[i]);
+      Ssum = (M == -INFINITY ? 0.f : Ssum * __expf(M - nm)) + (shm[i] == -INFINITY ? 0.f : shs[i] * __expf(shm[i] - nm));
+      M = nm;
+    }
+    const float lse = M + __logf(Ssum);
     lse_out[blockIdx.x] = lse;
     loss[blockIdx.x] = lse - __bfloat162float(row[target[blockIdx.x]]);
   }
