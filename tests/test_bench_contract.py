@@ -1,0 +1,38 @@
+"""bench.py's JSON contract on CPU: the reference arm (the reference's CPU
+runtime on the host cores) and the virtual-clock pipeline model (host twin)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--mb", "4"], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["config"]["layer_split"] == [24]
+
+
+def test_pipeline_model_on_host_twin():
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2605_18750_b200.model import GPTConfig
+    args = argparse.Namespace(head_cost=1.4, mb=8, comm_us=100.0)
+    out = bench.pipeline_model(args, GPTConfig(), {"F": [6400.0], "B": [12700.0]}, 1, pps=(2, 8),
+                               device="cpu")
+    assert out["pp8"]["layers"] == [4, 3, 3, 3, 3, 3, 3, 2]
+    for pp in ("pp2", "pp8"):
+        for sig in ("sigma0.0", "sigma0.5"):
+            r = out[pp][sig]
+            assert r["1f1b"]["ms"] > 0 and r["bf"]["speedup_vs_1f1b"] > 0.8
+    # jitter makes every schedule slower
+    assert out["pp8"]["sigma0.5"]["1f1b"]["ms"] > out["pp8"]["sigma0.0"]["1f1b"]["ms"]
