@@ -1,0 +1,28 @@
+"""Config 3 shapes on one B200: GPT-7B layers (d=4096, 32 heads, ffn 16384),
+TP=2 x PP=4 as 8 lanes in one process (reduced depth / microbatches so it fits
+one GPU), BF and BFW; loss at init ~ log(V), TP error words clear (dev tool)."""
+import math, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2605_18750_b200.model import GPTConfig
+from paper_2605_18750_b200.pipeline import GpuPipeline
+cfg = GPTConfig(n_layer=8, d_model=4096, n_head=32, d_ff=16384)
+for hint in ("bf", "bfw"):
+    t0 = time.time()
+    pipe = GpuPipeline(cfg, 4, 4, hint=hint, tp_size=2, head_cost=1.4)
+    build = time.time() - t0
+    losses = []
+    for _ in range(3):
+        t0 = time.time()
+        losses.append(pipe.step(watchdog_secs=120).item())
+        dt = time.time() - t0
+    errs = [st.tp.error() for row in pipe.grid for st in row]
+    tr, met = pipe.trace()
+    print(f"{hint}: build {build:.1f}s step {dt*1e3:.0f} ms losses {[round(l, 4) for l in losses]} "
+          f"expected {math.log(cfg.vocab) + cfg.init_std ** 2 * cfg.d_model / 2:.4f} tp_err {errs} execs {len(tr.execs())} bubble {met.bubble_fraction():.3f}",
+          flush=True)
+    # at init the logits are ~N(0, s^2), s = init_std * sqrt(d): E[CE] = log V + s^2 / 2
+    want = math.log(cfg.vocab) + (cfg.init_std ** 2 * cfg.d_model) / 2
+    assert all(e == 0 for e in errs) and all(abs(l - want) < 0.1 for l in losses), (losses, want)
+    pipe.close()
+print("config3 ok")

@@ -1,2 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
-timeout 900 python -m pytest tests/test_gpu_ops.py tests/test_gpu_model.py -x -q 2>&1 | tail -15
+timeout 900 python tools/config3_check.py 2>&1 | grep -v "^\s*File\|^\s*\^" | tail -8
