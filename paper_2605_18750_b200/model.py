@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -331,6 +332,19 @@ class StageCompute:
         self.m1, self.r1, self.m2, self.r2 = f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S), f32(n_mb, nl, S)
         self.attn_aux = [[None] * nl for _ in range(n_mb)]
         self.o_view = [[None] * nl for _ in range(n_mb)]   # attention output as [S, D]
+        # attention core: cuDNN SDPA through the frontend graph API (attention.py) reading
+        # the packed QKV and writing O / stats / packed dQKV into our own slots;
+        # RRFP_ATTN=torch selects the aten op (separate dQ/dK/dV, copied in)
+        self.attn_impl = os.environ.get("RRFP_ATTN", "cudnn_fe")
+        self._sdpa = {}
+        if self.attn_impl == "cudnn_fe" and nl:
+            from .attention import sdpa_graphs
+            self.attn_o = e(n_mb, nl, S, Dl)
+            self.attn_st = f32(n_mb, nl, self.Hl, S)
+            for T in sorted(set(self.rows)):
+                self._sdpa[T] = sdpa_graphs(T, self.Hl, cfg.d_head, cfg.causal, dev, S)
+            ws = max(g.workspace_bytes for g in self._sdpa.values())
+            self.attn_ws = torch.empty(max(ws, 16), device=dev, dtype=torch.uint8)
         if self.last:
             self.hf, self.mf, self.rf = e(n_mb, S, D), f32(n_mb, S), f32(n_mb, S)
             self.logits = e(n_mb, S, V)
@@ -370,6 +384,12 @@ class StageCompute:
     # ------------------------------------------------------------ forward
     def _attn_fwd(self, qkv, mb, li):
         T, H, Dh, D = qkv.shape[0], self.Hl, self.cfg.d_head, self.Dl
+        if self._sdpa:
+            o = self.attn_o[mb, li, :T]
+            self._sdpa[T].forward(qkv.data_ptr(), o.data_ptr(), self.attn_st[mb, li].data_ptr(),
+                                  self.attn_ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            self.o_view[mb][li] = o
+            return
         q = qkv[:, :D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         k = qkv[:, D:2 * D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         v = qkv[:, 2 * D:].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
@@ -640,6 +660,11 @@ class StageCompute:
         cfg = self.cfg
         T, H, Dh, D = d_qkv.shape[0], self.Hl, cfg.d_head, self.Dl
         qkv = self.qkv[mb, li, :T]
+        if self._sdpa:   # dQ, dK, dV straight into the packed gradient the QKV GEMMs read
+            self._sdpa[T].backward(qkv.data_ptr(), self.o_view[mb][li].data_ptr(), d_o.data_ptr(),
+                                   self.attn_st[mb, li].data_ptr(), d_qkv.data_ptr(),
+                                   self.attn_ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            return
         q = qkv[:, :D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         k = qkv[:, D:2 * D].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
         v = qkv[:, 2 * D:].view(T, H, Dh).transpose(0, 1).unsqueeze(0)
@@ -742,6 +767,7 @@ class StageCompute:
         the ranks of a TP group can warm up concurrently (their all-reduces
         wait for each other on the device).  Returns the stream."""
         stream = stream or torch.cuda.Stream(self.device)
+        stream.wait_stream(torch.cuda.current_stream(self.device))   # parameter / data init
         with torch.cuda.stream(stream):
             for mb in range(self.M):
                 for kind in ("F", "B", "W") if self.decompose else ("F", "B"):

@@ -146,6 +146,11 @@ class GpuPipeline:
                 c.local_only = True
         streams = {(v, r): torch.cuda.Stream(torch.device("cuda", devices[v % N]))
                    for v in range(V) for r in range(R)}
+        # the warm-up streams must see the parameter / token initialisation queued on the
+        # current stream: an embedding reading a token buffer that is still being written
+        # (with a recycled allocation's bytes in it) indexes out of bounds
+        for stream in streams.values():
+            stream.wait_stream(torch.cuda.current_stream(stream.device))
         for mb in range(n_mb):
             for kind in kinds:
                 for (v, r), stream in streams.items():

@@ -7,16 +7,18 @@ import torch
 from paper_2605_18750_b200.model import GPTConfig
 from paper_2605_18750_b200.pipeline import GpuPipeline
 cfg = GPTConfig(n_layer=8, d_model=4096, n_head=32, d_ff=16384)
-for hint in ("bf", "bfw"):
+hints = sys.argv[1].split(",") if len(sys.argv) > 1 else ["bf", "bfw"]
+tp_size = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+for hint in hints:
     t0 = time.time()
-    pipe = GpuPipeline(cfg, 4, 4, hint=hint, tp_size=2, head_cost=1.4)
+    pipe = GpuPipeline(cfg, 4, 4, hint=hint, tp_size=tp_size, head_cost=1.4)
     build = time.time() - t0
     losses = []
     for _ in range(3):
         t0 = time.time()
         losses.append(pipe.step(watchdog_secs=120).item())
         dt = time.time() - t0
-    errs = [st.tp.error() for row in pipe.grid for st in row]
+    errs = [st.tp.error() if st.tp else 0 for row in pipe.grid for st in row]
     tr, met = pipe.trace()
     print(f"{hint}: build {build:.1f}s step {dt*1e3:.0f} ms losses {[round(l, 4) for l in losses]} "
           f"expected {math.log(cfg.vocab) + cfg.init_std ** 2 * cfg.d_model / 2:.4f} tp_err {errs} execs {len(tr.execs())} bubble {met.bubble_fraction():.3f}",
