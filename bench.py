@@ -246,6 +246,7 @@ def gemm_roofline(cfg, peak_tf):
     import torch
     calls = roofline_gemm_calls(cfg)
     st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())   # operands initialised on the current stream
     with torch.cuda.stream(st):
         for fn, _ in calls:
             fn()
