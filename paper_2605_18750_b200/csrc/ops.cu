@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(256) ln_param_grad_kernel(
 #pragma unroll
   for (int j = 0; j < 8; ++j) { ag[j] = 0.f; ab[j] = 0.f; }
   if (c0 < D) {
+#pragma unroll 4
     for (int r = r0 + warp; r < r1; r += 8) {
       float xv[8], dv[8];
       load8(x + (size_t)r * D + c0, xv);
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 #pragma unroll
   for (int j = 0; j < 8; ++j) a[j] = 0.f;
   if (c0 < cols) {
+#pragma unroll 4
     for (int r = r0 + warp; r < r1; r += 8) {
       float v[8];
       load8(dy + (size_t)r * ld + c0, v);
@@ -400,7 +402,7 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
     RRFP_CUDA_TRY(cudaGetLastError());
   }
   if (dg || db) {
-    const int rpb = 64;
+    const int rpb = 32;   // 2 rows per warp (unrolled): enough CTAs in flight per SM
     dim3 g2((D + 255) / 256, (rows + rpb - 1) / rpb);
     RRFP_CUDA_TRY(rrfp_launch(ln_param_grad_kernel, g2, dim3(256), 0, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
                                              rstd, dg, db, rows, D, rpb));
