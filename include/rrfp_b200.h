@@ -217,6 +217,9 @@ void rrfp_tp_destroy(rrfp_tp* t);
  * base+1..base+rounds, growing across calls on a slot.  Blocking. */
 int rrfp_clock_pingpong(void* mine, void* peer, int role, int rounds, long long base, long long* offset_ns,
                         long long* rtt_ns);
+/* One process driving several GPUs (GpuPipeline(devices=[...])): enable dev -> peer
+ * access for the neighbours' plain-pointer mailbox / inbox stores.  Idempotent. */
+int rrfp_enable_peer_access(int dev, int peer);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */

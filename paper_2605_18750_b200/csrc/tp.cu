@@ -302,3 +302,22 @@ extern "C" int rrfp_clock_pingpong(void* mine, void* peer, int role, int rounds,
   if (rtt_ns) *rtt_ns = role == 0 ? h[1] : 0;
   return RRFP_OK;
 }
+
+// Single-process multi-GPU pipelines (GpuPipeline(devices=[...])): neighbour
+// stages store into each other's mailboxes / inboxes with plain pointers, which
+// needs peer access enabled in both directions (the multi-process path gets it
+// from cudaIpcMemLazyEnablePeerAccess).  Idempotent.
+extern "C" int rrfp_enable_peer_access(int dev, int peer) {
+  if (dev == peer) return RRFP_OK;
+  int can = 0;
+  RRFP_CUDA_TRY(cudaDeviceCanAccessPeer(&can, dev, peer));
+  if (!can) return rrfp_fail(RRFP_E_CUDA, "GPU %d cannot access GPU %d (no P2P / NVLink)", dev, peer);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  RRFP_CUDA_TRY(cudaSetDevice(dev));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); e = cudaSuccess; }
+  cudaSetDevice(cur);
+  RRFP_CUDA_TRY(e);
+  return RRFP_OK;
+}

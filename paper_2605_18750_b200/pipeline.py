@@ -113,6 +113,12 @@ class GpuPipeline:
                          num_chunks=C, tp_group_size=R, latency=w.latency, comm_delay=comm_delay,
                          decompose_backward=decompose)
         self.workload = w
+        if len(set(devices)) > 1:   # one process, several GPUs: neighbours store into each other
+            from . import _lib
+            for a in set(devices):
+                for b in set(devices):
+                    if a != b:
+                        _lib.check(_lib.lib().rrfp_enable_peer_access(a, b))
         self.comms = {}
         if R > 1:   # one TP group per lane (its virtual stages run one task at a time)
             from .tp import TpComm

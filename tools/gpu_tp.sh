@@ -1,2 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
-timeout 600 python -m pytest tests/test_gpu_ops.py tests/test_gpu_model.py -q 2>&1 | tail -1
+timeout 600 python -m pytest tests/test_gpu_ops.py tests/test_gpu_model.py -q > gpurun_out/t.log 2>&1; echo rc=$?
+tail -3 gpurun_out/t.log
