@@ -426,6 +426,7 @@ def run_ours(args):
     if args.emulate_pp > 1 and world == 1:
         # a fresh process: the PP=1 pipeline's ~110 GB must not share the GPU with it
         cmd = [sys.executable, os.path.abspath(__file__), "--emulate-only", "--emulate-pp", str(args.emulate_pp),
+               "--w-split", args.w_split,
                "--steps", str(args.steps), "--warmup", str(args.warmup), "--mb", str(args.mb),
                "--sigmas", args.sigmas, "--compare-jitter", args.compare_jitter, "--comm-us", str(args.comm_us),
                "--head-cost", str(args.head_cost), "--model", args.model]
@@ -449,13 +450,14 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                            tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args), head_cost=args.head_cost)
+                            tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args), head_cost=args.head_cost,
+                            w_split=args.w_split)
         return pipe, pipe.vstages
     if args.model == "mm":
         raise SystemExit("--model mm (config 4) needs a pipeline of >= 2 GPUs")
     from paper_2605_18750_b200.pipeline import GpuPipeline
     pipe = GpuPipeline(cfg, 1, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
-                       tp_size=args.tp, n_chunks=args.chunks, head_cost=args.head_cost)
+                       tp_size=args.tp, n_chunks=args.chunks, head_cost=args.head_cost, w_split=args.w_split)
     return pipe, pipe.stages
 
 
@@ -548,7 +550,7 @@ def emulated_pp(args, cfg):
     for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
         t0 = time.perf_counter()
         pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.compare_jitter],
-                           head_cost=args.head_cost, gemm_sm_cap=cap)
+                           head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split)
         build_s = time.perf_counter() - t0
         for _ in range(2):
             pipe.step()
@@ -739,6 +741,8 @@ def main():
     ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0",
                     help="J-preset jitter table (jitter.py PRESETS) applied to every comparison variant")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
+    ap.add_argument("--w-split", dest="w_split", default="fc", choices=["fc", "all"],
+                    help="BFW: weight gradients deferred to the W task (fc: FC1/FC2; all: all four)")
     ap.add_argument("--emulate-only", dest="emulate_only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "

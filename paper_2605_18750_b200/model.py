@@ -250,10 +250,15 @@ class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
                  decompose: bool = False, seed: int = 1234, data_seed: int = 0,
                  fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None,
-                 mm: MultimodalSpec | None = None, head_cost: float = 0.0):
+                 mm: MultimodalSpec | None = None, head_cost: float = 0.0, w_split: str = "fc"):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
         self.decompose = decompose
+        if w_split not in ("fc", "all"):
+            raise ValueError("w_split must be 'fc' or 'all'")
+        # decomposed backward: which weight gradients the W task takes -- "fc": FC1/FC2
+        # (default; the attention ones overlap the attention backward in B), "all": all four
+        self.w_split = w_split
         self.mm = mm
         # which part of the model this stage holds (config 4: ViT stages, then LLM stages)
         if mm is not None:
@@ -364,6 +369,8 @@ class StageCompute:
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
             self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl)
             self.gx0 = e(n_mb, S, D) if self.prologue else None
+            if w_split == "all":
+                self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl)
         self.graphs = {}
         self.kernel_counts = {}   # (kind, mb) -> our kernel launches in that body
         self.gemm_sm_cap = 0      # > 0: GEMM grids confined to this many SMs (see run_task)
@@ -510,10 +517,13 @@ class StageCompute:
             e.record(main)
             return e
 
+        side_used = []
+
         def on_side(after, fn):
             if side == main:
                 fn()
                 return
+            side_used.append(True)
             with torch.cuda.stream(side):
                 side.wait_event(after)
                 fn()
@@ -561,8 +571,9 @@ class StageCompute:
             if li + 2 in side_done:          # set q was last read by layer li+2's side work
                 main.wait_event(side_done[li + 2])
             d_pre = (self.gpre[mb, li] if dec else self.sd_big[q])[:T]
-            d_x2 = self.sd_b[q][:T]
-            d_qkv = self.sd_qkv[q][:T]
+            defer_attn = dec and self.w_split == "all"
+            d_x2 = (self.gx2[mb, li] if defer_attn else self.sd_b[q])[:T]
+            d_qkv = (self.gqkv[mb, li] if defer_attn else self.sd_qkv[q])[:T]
             if fused_w:
                 dyy = dy
                 on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
@@ -579,9 +590,10 @@ class StageCompute:
             _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
                     d_x2, g["ln2_g"], g["ln2_b"])
             ov = self.o_view[mb][li]
-            on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
-                                          a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
-                                   _bias_grad(d_x2, g["b_o"])))
+            if not defer_attn:
+                on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
+                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
+                                       _bias_grad(d_x2, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
             d_o = d_head if self.R == 1 else self.d_o
             K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=T, n=Dl, k=D)
@@ -590,10 +602,11 @@ class StageCompute:
                 K.gemm(d_qkv, h1, g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
                        b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
                 _bias_grad(d_qkv, g["b_qkv"])
-            on_side(ev(), qkv_w)
-            done = torch.cuda.Event()
-            done.record(side)
-            side_done[li] = done
+            if not defer_attn:
+                on_side(ev(), qkv_w)
+                done = torch.cuda.Event()
+                done.record(side)
+                side_done[li] = done
             self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             extra = []
@@ -623,7 +636,7 @@ class StageCompute:
         if self.prologue and fused_w:
             dyy = dy
             on_side(ev(), lambda: self._prologue_wgrad(mb, dyy))
-        if side != main:
+        if side_used:   # (a side stream never forked into a capture must not be joined)
             join = torch.cuda.Event()
             join.record(side)
             main.wait_event(join)
@@ -709,6 +722,14 @@ class StageCompute:
                 K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
                        b_mn=True, accumulate=True, m=Fd, n=D, k=T)
                 _bias_grad(gpre, g["b_1"])
+                if self.w_split == "all":
+                    gx2, gqkv = self.gx2[mb, li, :T], self.gqkv[mb, li, :T]
+                    K.gemm(gx2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=D, n=Dl, k=T)
+                    _bias_grad(gx2, g["b_o"])
+                    K.gemm(gqkv, self.h1[mb, li, :T], g["w_qkv"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=3 * Dl, n=D, k=T)
+                    _bias_grad(gqkv, g["b_qkv"])
         with torch.cuda.stream(side):
             if self.last:
                 K.gemm(self.logits[mb], self.hf[mb], self.g_head["w_lm"], epi=K.EPI_ACC_F32, a_mn=True,

@@ -34,13 +34,14 @@ def test_eager_single_stage_matches_fp32_reference():
     assert not compare(ref_grads, device_grads([st]))
 
 
-@pytest.mark.parametrize("n_stages,hint,mode,head_cost", [(1, "bf", "free", 0), (2, "bf", "free", 0),
-                                                          (4, "bfw", "free", 0), (2, "bf", "fixed", 0),
-                                                          (4, "bf", "replay", 0), (2, "bfw", "free", 1.4)])
-def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode, head_cost):
+@pytest.mark.parametrize("n_stages,hint,mode,head_cost,w_split", [
+    (1, "bf", "free", 0, "fc"), (2, "bf", "free", 0, "fc"), (4, "bfw", "free", 0, "fc"),
+    (2, "bf", "fixed", 0, "fc"), (4, "bf", "replay", 0, "fc"), (2, "bfw", "free", 1.4, "fc"),
+    (2, "bfw", "free", 0, "all")])
+def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode, head_cost, w_split):
     from paper_2605_18750_b200.pipeline import GpuPipeline
     cfg = _cfg()
-    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, head_cost=head_cost)
+    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, head_cost=head_cost, w_split=w_split)
     if head_cost:
         assert [len(st.layers) for st in pipe.stages] == [3, 1]   # balanced against the LM head
     try:
