@@ -1,3 +1,1 @@
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
-timeout 600 python -m pytest tests/test_gpu_model.py -q > gpurun_out/t.log 2>&1; echo rc=$?; tail -1 gpurun_out/t.log
-timeout 1500 python bench.py --emulate-only --emulate-pp 8 --steps 3 --warmup 3 --sigmas 0.5 --w-split all > gpurun_out/emu_all.json 2> gpurun_out/emu_all.err; echo rc=$?
+timeout 600 python tools/sdpa_plans.py 2>&1 | tail -40
