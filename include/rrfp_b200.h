@@ -184,6 +184,9 @@ int rrfp_runtime_inbox(rrfp_runtime* rt, void** dev_ptr, size_t* bytes);
 int rrfp_runtime_inbox_ipc(rrfp_runtime* rt, void* handle64);
 /* Open a peer's IPC handle; returns a device pointer usable in this process. */
 int rrfp_ipc_open(const void* handle64, void** dev_ptr);
+/* Unmap a pointer returned by rrfp_ipc_open (every opener closes before its peer's
+ * next allocation can be opened again). */
+int rrfp_ipc_close(void* dev_ptr);
 /* cudaMalloc'd (IPC-exportable) buffer for mailbox slots; handle of such a buffer. */
 int rrfp_ipc_alloc(size_t bytes, void** dev_ptr);
 int rrfp_ipc_handle(void* dev_ptr, void* handle64);

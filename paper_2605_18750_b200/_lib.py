@@ -79,7 +79,7 @@ EXPORTS = [
     "rrfp_arbitrate", "rrfp_update_backpressure", "rrfp_replay_workspace_bytes",
     "rrfp_replay_event_capacity", "rrfp_replay_host", "rrfp_replay_device",
     "rrfp_runtime_create", "rrfp_runtime_destroy", "rrfp_runtime_inbox", "rrfp_runtime_inbox_ipc",
-    "rrfp_ipc_open", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
+    "rrfp_ipc_open", "rrfp_ipc_close", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
     "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status",
     "rrfp_spin", "rrfp_last_error", "rrfp_abi_version", "rrfp_gemm_bf16", "rrfp_gemm_set_variant", "rrfp_set_pdl",
     "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_embedding_fwd",

@@ -589,6 +589,15 @@ extern "C" int rrfp_ipc_open(const void* handle64, void** dev_ptr) {
   return RRFP_OK;
 }
 
+// Unmap a peer buffer opened with rrfp_ipc_open (a later pipeline that opens the
+// peer's next buffer -- possibly at the same address -- would otherwise fail with
+// "resource already mapped").
+extern "C" int rrfp_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return RRFP_OK;
+  RRFP_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return RRFP_OK;
+}
+
 extern "C" int rrfp_ipc_alloc(size_t bytes, void** dev_ptr) {
   if (!dev_ptr || !bytes) return rrfp_fail(RRFP_E_INVALID, "bad ipc alloc");
   RRFP_CUDA_TRY(cudaMalloc(dev_ptr, bytes));

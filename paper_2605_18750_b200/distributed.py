@@ -83,10 +83,20 @@ class IpcBuffer:
             self.ptr = None
 
 
-def open_handle(handle: bytes) -> int:
+def open_handle(handle: bytes, track: list | None = None) -> int:
+    """Map a peer's IPC buffer; `track` collects the pointer so the owner can
+    unmap it (close_handles) when it is torn down."""
     p = C.c_void_p()
     _lib.check(_lib.lib().rrfp_ipc_open(handle, C.byref(p)))
+    if track is not None:
+        track.append(p.value)
     return p.value
+
+
+def close_handles(ptrs: list):
+    for ptr in ptrs:
+        _lib.check(_lib.lib().rrfp_ipc_close(C.c_void_p(ptr)))
+    ptrs.clear()
 
 
 class DistPipeline:
@@ -133,6 +143,7 @@ class DistPipeline:
             from .tp import TpComm
             self.comm = TpComm(r, R, (cfg.seq, cfg.d_model), torch.device("cuda", self.device))
         self.clock_slot = IpcBuffer(16, self.device)      # cross-GPU timer calibration
+        self._opened = []                                 # peer buffers this rank mapped
         self.clock_offset_ns = 0                          # this rank's clock - rank 0's clock
         self.vstages = []
         for v in self.vids:
@@ -174,8 +185,8 @@ class DistPipeline:
             self.comm.connect_ipc([by[(s, q)]["tp"] for q in range(R)])
 
         def mailboxes(v, which):   # virtual stage v's F (0) / B (1) mailbox on every TP rank
-            dst = [wrap_bf16(open_handle(by[(v % n, q)]["mbox"][v][which]), by[(v % n, q)]["mbox"][v][2][which],
-                             self.device) for q in range(R)]
+            dst = [wrap_bf16(open_handle(by[(v % n, q)]["mbox"][v][which], self._opened),
+                             by[(v % n, q)]["mbox"][v][2][which], self.device) for q in range(R)]
             return [[d[mb] for d in dst] for mb in range(n_mb)]
 
         for st, v in zip(self.vstages, self.vids):
@@ -225,7 +236,7 @@ class DistPipeline:
             other = peer if me == 0 else 0
             opened = self.__dict__.setdefault("_clock_opened", {})
             if other not in opened:
-                opened[other] = open_handle(self._clock_peers[other])
+                opened[other] = open_handle(self._clock_peers[other], self._opened)
             ptr = opened[other]
             o, t = C.c_longlong(), C.c_longlong()
             base = (calls * self.gworld + peer) * (rounds + 1)   # round ids grow on every slot
@@ -316,6 +327,8 @@ class DistPipeline:
         if self.comm:
             self.comm.close()
             self.comm = None
+        close_handles(self._opened)
+        self.__dict__.pop("_clock_opened", None)
         for st in self.vstages or []:
             st.release()
         self.vstages = []
@@ -324,3 +337,6 @@ class DistPipeline:
             if b is not None:
                 b.free()
         self.bufs = {}
+        if self.clock_slot is not None:
+            self.clock_slot.free()
+            self.clock_slot = None

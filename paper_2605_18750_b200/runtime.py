@@ -253,12 +253,14 @@ class LaneGroup:
         """Multi-process wiring: ``handles`` maps every lane to its 64-byte IPC
         handle (gathered with torch.distributed); local lanes use plain pointers."""
         inboxes = {}
+        self._opened = getattr(self, "_opened", [])
         for lane, hd in handles.items():
             if lane in self.lanes:
                 inboxes[lane] = self.inbox(lane)
             else:
                 p = C.c_void_p()
                 _lib.check(self.L.rrfp_ipc_open(hd, C.byref(p)))
+                self._opened.append(p.value)
                 inboxes[lane] = p.value
         self.connect(inboxes)
 
@@ -312,6 +314,9 @@ class LaneGroup:
         for h in self.lanes.values():
             self.L.rrfp_runtime_destroy(h)
         self.lanes = {}
+        for ptr in getattr(self, "_opened", []):   # peer inboxes mapped by connect_ipc
+            self.L.rrfp_ipc_close(C.c_void_p(ptr))
+        self._opened = []
 
     def __del__(self):
         try:

@@ -69,13 +69,14 @@ class TpComm:
         """handles[q] = (partial handle, board handle) of TP rank q (own included)."""
         from .distributed import open_handle
         parts, boards = [], []
+        self._opened = getattr(self, "_opened", [])
         for q, (ph, bh) in enumerate(handles):
             if q == self.rank:
                 parts.append(self.part_ptr)
                 boards.append(self.board_ptr)
             else:
-                parts.append(open_handle(ph))
-                boards.append(open_handle(bh))
+                parts.append(open_handle(ph, self._opened))
+                boards.append(open_handle(bh, self._opened))
         self.connect(parts, boards)
 
     # ---------------------------------------------------------- collective
@@ -96,6 +97,8 @@ class TpComm:
         return e.value
 
     def close(self):
+        from .distributed import close_handles
+        close_handles(getattr(self, "_opened", []))
         if self.h:
             _lib.lib().rrfp_tp_destroy(self.h)
             self.h = None
