@@ -60,3 +60,21 @@ def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks, 
     viol = [v for v in O.validate(tup, O.from_workload_json(res["workload"]), slack=(5, 1.05, 400),
                                   clock="wall") if v[0] != "duration"]
     assert not viol, viol[:5]
+
+
+def test_second_pipeline_in_the_same_processes():
+    """bench.py builds one DistPipeline per variant: closing a pipeline must unmap
+    every peer IPC buffer (lane inboxes, mailboxes, TP boards, clock slots) so the
+    next one can map the peers' new buffers."""
+    env = dict(os.environ, RRFP_SAME_DEVICE="1", RRFP_REBUILD="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tools", "dist_check.py"),
+           "bf", "2", "1"]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]
+    res = json.loads(line[-1])
+    ref = res["single_process_pp1_loss"]
+    for r in res["ranks"]:
+        if r["losses"][0] is not None:
+            assert len(r["losses"]) == 3 and all(abs(l - ref) / ref < 1e-2 for l in r["losses"])

@@ -49,6 +49,15 @@ def main():
     aligned = pipe.aligned_events()
     out = [None] * world   # (pipe is kept for its workload description)
     tp_err = pipe.comm.error() if pipe.comm else 0
+    if os.environ.get("RRFP_REBUILD") == "1":
+        # a second pipeline in the same processes (bench builds one per variant):
+        # peer buffers must have been unmapped, warm-up must see fresh init
+        wl = pipe.workload
+        pipe.close()
+        pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm)
+        loss2 = pipe.step(watchdog_secs=wd)
+        losses.append(None if loss2 is None else loss2.item())
+        ev, t0 = pipe.last_events
     dist.all_gather_object(out, {"rank": rank, "losses": losses, "n_exec": n_exec, "tp_err": tp_err,
                                  "clock": [off, rtt], "events": aligned})
     pipe.close()
