@@ -272,6 +272,8 @@ int rrfp_gemm_reserve_sms(int n);
 int rrfp_gemm_set_epilogue(int tma_store);
 /* 1 = stream-K split of the last partial round of 256x256 tiles over all CTA pairs (default 0). */
 int rrfp_gemm_set_streamk(int on);
+/* pair-kernel k-block depth: 64 (6-stage ring, default) or 128 (3 stages). */
+int rrfp_gemm_set_bk(int bk);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                        int rows, int D, float eps, void* stream);

@@ -534,23 +534,34 @@ __global__ void __launch_bounds__(256, 1)
 // The leader CTA issues the MMAs; TMA completions of both CTAs land on the
 // leader's full barrier; MMA commits multicast to both CTAs' empty / tmem-full
 // barriers; both epilogues release the leader's tmem-empty barrier.
-constexpr int P_BM = 256, P_BN = 256, P_STAGES = 6;
-constexpr int P_A_BYTES = 128 * BK * 2;      // this CTA's 128 rows of A
-constexpr int P_B_BYTES = 128 * BK * 2;      // this CTA's 128 rows (N/2) of B
+// k-block depth PBK (64 or 128; same 192 KB of operand ring: 6 or 3 stages).
+// A K-major operand stage holds PBK/64 SW128 panels of [128 rows x 64 k]; an
+// MN-major one two 64-wide MN panels of [PBK k-rows x 64].
+constexpr int P_BM = 256, P_BN = 256;
+constexpr int P_RING_BYTES = 6 * 2 * 128 * 64 * 2;   // 192 KB
+template <int PBK> struct PairCfg {
+  static constexpr int STAGES = 6 * 64 / PBK;
+  static constexpr int A_BYTES = 128 * PBK * 2;      // this CTA's 128 rows of A
+  static constexpr int B_BYTES = 128 * PBK * 2;      // this CTA's 128 rows (N/2) of B
+};
+constexpr int P_STAGES = 6;                          // (barrier array size: max stages)
 constexpr int P_EPI_BYTES = 4 * 2 * 4096;     // per epilogue warp: two 32-row x 128-byte staging boxes
-constexpr int P_SMEM_BYTES = P_STAGES * (P_A_BYTES + P_B_BYTES) + P_EPI_BYTES + 1024 + 256;
+constexpr int P_SMEM_BYTES = P_RING_BYTES + P_EPI_BYTES + 1024 + 256;
 constexpr int P_TMEM_COLS = 2 * P_BN;
 
-template <int EPI, int A_MN, int B_MN>
+template <int EPI, int A_MN, int B_MN, int PBK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_sm100_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                          GemmArgs g) {
+  constexpr int NST = PairCfg<PBK>::STAGES;
+  constexpr int P_A_BYTES = PairCfg<PBK>::A_BYTES, P_B_BYTES = PairCfg<PBK>::B_BYTES;
+  constexpr int PANEL = 128 * 64 * 2;   // one SW128 K-major panel of 128 rows
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + P_STAGES * P_A_BYTES;
-  uint8_t* sEpi = sB + P_STAGES * P_B_BYTES;   // 1024-aligned
+  uint8_t* sB = smem + NST * P_A_BYTES;
+  uint8_t* sEpi = smem + P_RING_BYTES;   // 1024-aligned
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + P_EPI_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + P_STAGES;
@@ -564,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
-    for (int s = 0; s < P_STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
     sm100::fence_barrier_init();
   }
@@ -577,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   sm100::griddep_wait();
 
   const int num_tiles = g.tiles_m * g.tiles_n;
-  const int kblocks = (g.K + BK - 1) / BK;
+  const int kblocks = (g.K + PBK - 1) / PBK;
   const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
   // f32 accumulate: every split segment reduce-adds into C by itself (no fix-up)
   const bool direct = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
@@ -598,18 +609,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           uint8_t* a_dst = sA + stage * P_A_BYTES;
           uint8_t* b_dst = sB + stage * P_B_BYTES;
           if (!A_MN) {
-            sm100::tma_load_2d_pair(a_dst, &tmA, bar, kb * BK, m0);
+#pragma unroll
+            for (int h = 0; h < PBK / 64; ++h)
+              sm100::tma_load_2d_pair(a_dst + h * PANEL, &tmA, bar, kb * PBK + h * 64, m0);
           } else {
-            sm100::tma_load_2d_pair(a_dst, &tmA, bar, m0, kb * BK);
-            sm100::tma_load_2d_pair(a_dst + 64 * BK * 2, &tmA, bar, m0 + 64, kb * BK);
+            sm100::tma_load_2d_pair(a_dst, &tmA, bar, m0, kb * PBK);
+            sm100::tma_load_2d_pair(a_dst + 64 * PBK * 2, &tmA, bar, m0 + 64, kb * PBK);
           }
           if (!B_MN) {
-            sm100::tma_load_2d_pair(b_dst, &tmB, bar, kb * BK, n0);
+#pragma unroll
+            for (int h = 0; h < PBK / 64; ++h)
+              sm100::tma_load_2d_pair(b_dst + h * PANEL, &tmB, bar, kb * PBK + h * 64, n0);
           } else {
-            sm100::tma_load_2d_pair(b_dst, &tmB, bar, n0, kb * BK);
-            sm100::tma_load_2d_pair(b_dst + 64 * BK * 2, &tmB, bar, n0 + 64, kb * BK);
+            sm100::tma_load_2d_pair(b_dst, &tmB, bar, n0, kb * PBK);
+            sm100::tma_load_2d_pair(b_dst + 64 * PBK * 2, &tmB, bar, n0 + 64, kb * PBK);
           }
-          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -631,15 +646,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint32_t a_base = sm100::smem_u32(sA + stage * P_A_BYTES);
           const uint32_t b_base = sm100::smem_u32(sB + stage * P_B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = A_MN ? sm100::umma_desc_sw128(a_base + k * 16 * 128, 64 * BK * 2, 1024)
-                               : sm100::umma_desc_sw128(a_base + k * 32, 16, 1024);
-            uint64_t bd = B_MN ? sm100::umma_desc_sw128(b_base + k * 16 * 128, 64 * BK * 2, 1024)
-                               : sm100::umma_desc_sw128(b_base + k * 32, 16, 1024);
+          for (int k = 0; k < PBK / 16; ++k) {
+            const uint32_t kp = (k >> 2) * PANEL + (k & 3) * 32;   // K-major: panel, then 32 B per k16
+            uint64_t ad = A_MN ? sm100::umma_desc_sw128(a_base + k * 16 * 128, 64 * PBK * 2, 1024)
+                               : sm100::umma_desc_sw128(a_base + kp, 16, 1024);
+            uint64_t bd = B_MN ? sm100::umma_desc_sw128(b_base + k * 16 * 128, 64 * PBK * 2, 1024)
+                               : sm100::umma_desc_sw128(b_base + kp, 16, 1024);
             sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != u.k0) || (k != 0));
           }
           sm100::mma_commit_pair(&empty[stage], 0x3);
-          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         sm100::mma_commit_pair(&tfull[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -857,6 +873,16 @@ bool use_tma_store() {
   return g_tma_store != 0;
 }
 
+int g_pair_bk = -1;   // pair-kernel k-block depth: 64 (6 stages) or 128 (3 stages); env RRFP_GEMM_BK
+
+int pair_bk() {
+  if (g_pair_bk < 0) {
+    const char* e = getenv("RRFP_GEMM_BK");
+    g_pair_bk = (e && atoi(e) == 128) ? 128 : 64;
+  }
+  return g_pair_bk;
+}
+
 bool use_pair() {
   if (g_pair < 0) {
     const char* e = getenv("RRFP_GEMM_PAIR");
@@ -910,10 +936,10 @@ SkWorkspace* sk_workspace(cudaStream_t st, int clusters) {
   return &(g_ws[key] = w);
 }
 
-template <int EPI, int A_MN, int B_MN>
+template <int EPI, int A_MN, int B_MN, int PBK>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
                 GemmArgs g, cudaStream_t st) {
-  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN>;
+  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK>;
   static bool attr = false;
   if (!attr) {
     RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES));
@@ -924,7 +950,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   int tiles = g.tiles_m * g.tiles_n;
   int pairs = (g_num_sms - g_reserve_sms) / 2;
   if (pairs < 1) pairs = 1;
-  const int kblocks = (g.K + BK - 1) / BK;
+  const int kblocks = (g.K + PBK - 1) / PBK;
   g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
   const int tail = tiles % pairs;
@@ -967,10 +993,16 @@ int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   if (use_pair()) {
-    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0>(ta, tb, tc, tc2, g, st);
-    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1>(ta, tb, tc, tc2, g, st);
-    if (a_mn && b_mn) return launch_pair<EPI, 1, 1>(ta, tb, tc, tc2, g, st);
-    return launch_pair<EPI, 1, 0>(ta, tb, tc, tc2, g, st);
+    if (pair_bk() == 128) {
+      if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 128>(ta, tb, tc, tc2, g, st);
+      if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 128>(ta, tb, tc, tc2, g, st);
+      if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 128>(ta, tb, tc, tc2, g, st);
+      return launch_pair<EPI, 1, 0, 128>(ta, tb, tc, tc2, g, st);
+    }
+    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 64>(ta, tb, tc, tc2, g, st);
+    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 64>(ta, tb, tc, tc2, g, st);
+    if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 64>(ta, tb, tc, tc2, g, st);
+    return launch_pair<EPI, 1, 0, 64>(ta, tb, tc, tc2, g, st);
   }
   if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
   if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
@@ -993,9 +1025,10 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   if ((epi == EPI_RESID || epi == EPI_GELU_BWD) && !R) return rrfp_fail(RRFP_E_INVALID, "epilogue needs R");
   CUtensorMap ta, tb;
   const int brows = use_pair() ? 128 : BN;   // rows of B per CTA (the pair splits N)
-  int rc = a_mn ? make_map(&ta, A, K, M, lda, 64, BK) : make_map(&ta, A, M, K, lda, BK, BM);
+  const int mn_krows = use_pair() ? pair_bk() : BK;   // k-rows per MN-major box
+  int rc = a_mn ? make_map(&ta, A, K, M, lda, 64, mn_krows) : make_map(&ta, A, M, K, lda, BK, BM);
   if (rc) return rc;
-  rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, BK) : make_map(&tb, B, N, K, ldb, BK, brows);
+  rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, mn_krows) : make_map(&tb, B, N, K, ldb, BK, brows);
   if (rc) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
@@ -1062,6 +1095,12 @@ extern "C" int rrfp_gemm_set_streamk(int on) {
 // 1 = smem-staged TMA store / reduce-add epilogue, 0 = per-thread global stores
 extern "C" int rrfp_gemm_set_epilogue(int tma_store) {
   g_tma_store = tma_store < 0 ? 0 : tma_store;
+  return RRFP_OK;
+}
+
+// pair-kernel k-block depth: 64 (default) or 128
+extern "C" int rrfp_gemm_set_bk(int bk) {
+  g_pair_bk = bk == 128 ? 128 : 64;
   return RRFP_OK;
 }
 

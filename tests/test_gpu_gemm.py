@@ -5,16 +5,19 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 1), (1, 2), (1, 0), (0, 0)],
-                ids=["pair-tma-store", "pair-staged-coalesced", "pair-st-global", "single"], autouse=True)
+@pytest.fixture(params=[(1, 1, 64), (1, 1, 128), (1, 2, 64), (1, 0, 64), (0, 0, 64)],
+                ids=["pair-tma-store", "pair-bk128", "pair-staged-coalesced", "pair-st-global", "single"],
+                autouse=True)
 def variant(request):
     from paper_2605_18750_b200 import _lib
-    pair, tma = request.param
+    pair, tma, bk = request.param
     _lib.lib().rrfp_gemm_set_variant(pair)
     _lib.lib().rrfp_gemm_set_epilogue(tma)
+    _lib.lib().rrfp_gemm_set_bk(bk)
     yield request.param
     _lib.lib().rrfp_gemm_set_variant(1)
     _lib.lib().rrfp_gemm_set_epilogue(1)
+    _lib.lib().rrfp_gemm_set_bk(64)
 
 
 def _rand(*shape, scale=1.0):

@@ -13,9 +13,9 @@ names = ["qkv fwd", "proj fwd+R", "fc1 fwd gelu", "fc2 fwd+R", "fc2 dgrad gelu'"
          "fc2 wgrad f32+=", "fc1 wgrad f32+=", "qkv wgrad f32+="]
 calls = bench.roofline_gemm_calls(GPTConfig())
 L = _lib.lib()
-def setv(tma, sk):
-    return lambda: (L.rrfp_gemm_set_epilogue(tma), L.rrfp_gemm_set_streamk(sk))
-variants = [("tma store", setv(1, 0)), ("staged coalesced", setv(2, 0)), ("per-thread st", setv(0, 0))]
+def setv(tma, sk, bk=64):
+    return lambda: (L.rrfp_gemm_set_epilogue(tma), L.rrfp_gemm_set_streamk(sk), L.rrfp_gemm_set_bk(bk))
+variants = [("bk64 (6 stages)", setv(1, 0, 64)), ("bk128 (3 stages)", setv(1, 0, 128))]
 res = {}
 for vname, setv in variants:
     setv()
