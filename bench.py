@@ -427,6 +427,7 @@ def run_ours(args):
         # a fresh process: the PP=1 pipeline's ~110 GB must not share the GPU with it
         cmd = [sys.executable, os.path.abspath(__file__), "--emulate-only", "--emulate-pp", str(args.emulate_pp),
                "--w-split", args.w_split,
+               *([] if args.green else ["--no-green"]),
                "--steps", str(args.steps), "--warmup", str(args.warmup), "--mb", str(args.mb),
                "--sigmas", args.sigmas, "--compare-jitter", args.compare_jitter, "--comm-us", str(args.comm_us),
                "--head-cost", str(args.head_cost), "--model", args.model]
@@ -527,13 +528,13 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
 
 
 def emulated_pp(args, cfg):
-    """PP=N on ONE B200 (opt-in, --emulate-pp N): N device lanes in this process,
-    each stage's GEMM grids confined to 148/N SMs (the stage's share of the GPU;
-    the GEMMs are 72 % of the step), mailboxes in local memory.  Same kernels,
-    same dispatcher, same injected jitter as the multi-GPU run; 1F1B vs BF vs
-    BFW at every --sigmas value.  An emulation: idle stages lend their SMs to
-    the other stages' non-GEMM kernels, so bubbles cost less than on separate
-    GPUs (1F1B is flattered, not RRFP)."""
+    """PP=N on ONE B200 (--emulate-pp N): N device lanes in this process, each
+    stage on its own disjoint SM partition (CUDA green context, 16 SMs at N=8):
+    every kernel of a stage's bodies -- GEMMs, attention, LayerNorm -- runs only
+    on its partition, so an idle stage's SMs stay idle as on separate GPUs.
+    Mailboxes in local memory.  Same kernels, dispatcher and injected jitter as
+    the multi-GPU run; 1F1B vs BF vs BFW at every --sigmas value.  (--no-green:
+    only the GEMM grids are capped and idle SMs are borrowed by other stages.)"""
     import gc
     import math
     import torch
@@ -544,13 +545,16 @@ def emulated_pp(args, cfg):
     N = args.emulate_pp
     cap = (torch.cuda.get_device_properties(0).multi_processor_count // N) & ~1
     sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
-    out = {"n_stages": N, "gemm_sm_cap": cap, "definition": emulated_pp.__doc__.split("\n\n")[0]
-           .replace("\n", " ").replace("    ", " "), "variants": {}}
+    out = {"n_stages": N, "gemm_sm_cap": cap, "green_partitions": bool(args.green),
+           "definition": emulated_pp.__doc__.split("\n\n")[0].replace("\n", " ").replace("    ", " "),
+           "variants": {}}
     cur = torch.cuda.current_stream()
     for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
         t0 = time.perf_counter()
         pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.compare_jitter],
-                           head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split)
+                           head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split,
+                           green=args.green)
+        out["gemm_sm_cap"] = getattr(pipe, "green_sms", cap) if args.green else cap
         build_s = time.perf_counter() - t0
         for _ in range(2):
             pipe.step()
@@ -743,6 +747,8 @@ def main():
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     ap.add_argument("--w-split", dest="w_split", default="fc", choices=["fc", "all"],
                     help="BFW: weight gradients deferred to the W task (fc: FC1/FC2; all: all four)")
+    ap.add_argument("--no-green", dest="green", action="store_false",
+                    help="emulation without SM partitions (GEMM grids capped only)")
     ap.add_argument("--emulate-only", dest="emulate_only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "

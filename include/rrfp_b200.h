@@ -223,6 +223,9 @@ int rrfp_clock_pingpong(void* mine, void* peer, int role, int rounds, long long 
 /* One process driving several GPUs (GpuPipeline(devices=[...])): enable dev -> peer
  * access for the neighbours' plain-pointer mailbox / inbox stores.  Idempotent. */
 int rrfp_enable_peer_access(int dev, int peer);
+/* Single-GPU pipeline emulation: n disjoint SM partitions (green contexts) of
+ * >= min_sms SMs; two streams per partition in streams[2i], streams[2i+1]. */
+int rrfp_green_streams(int device, int n, int min_sms, void** streams, int* sms);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */

@@ -22,6 +22,7 @@
 //
 // Inbox flags carry the iteration epoch, so nothing is ever reset; an
 // iteration barrier in `init` keeps epochs of a lane group in step.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <string.h>
@@ -747,11 +748,51 @@ static int build_graph(rrfp_runtime* rt) {
 // Build + instantiate + upload the lane graph while the device is idle (every
 // lane of a job must be prepared before any lane is launched: a running lane
 // spins on its peers, and graph instantiation/upload must not queue behind it).
+// A lane whose stream belongs to a green context (single-GPU pipeline emulation,
+// green.cu) builds its graph with that context current, so the dispatcher's
+// kernel nodes share the context of the captured bodies (a conditional body
+// mixing contexts does not instantiate).
+static int build_graph_on_stream_ctx(rrfp_runtime* rt, cudaStream_t st) {
+  using get_g_t = CUresult (*)(CUstream, CUgreenCtx*);
+  using from_g_t = CUresult (*)(CUcontext*, CUgreenCtx);
+  using push_t = CUresult (*)(CUcontext);
+  using pop_t = CUresult (*)(CUcontext*);
+  static get_g_t get_g = nullptr;
+  static from_g_t from_g = nullptr;
+  static push_t push = nullptr;
+  static pop_t pop = nullptr;
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p;
+    if (cudaGetDriverEntryPoint("cuStreamGetGreenCtx", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) get_g = (get_g_t)p;
+    if (cudaGetDriverEntryPoint("cuCtxFromGreenCtx", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) from_g = (from_g_t)p;
+    if (cudaGetDriverEntryPoint("cuCtxPushCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) push = (push_t)p;
+    if (cudaGetDriverEntryPoint("cuCtxPopCurrent", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) pop = (pop_t)p;
+  }
+  CUgreenCtx g = nullptr;
+  CUcontext c = nullptr;
+  if (get_g && from_g && push && pop && st && get_g((CUstream)st, &g) == CUDA_SUCCESS && g &&
+      from_g(&c, g) == CUDA_SUCCESS && c) {
+    if (push(c) != CUDA_SUCCESS) return rrfp_fail(RRFP_E_CUDA, "cuCtxPushCurrent(green) failed");
+    int rc = build_graph(rt);
+    CUcontext dummy;
+    pop(&dummy);
+    return rc;
+  }
+  return build_graph(rt);
+}
+
 extern "C" int rrfp_runtime_prepare(rrfp_runtime* rt, void* stream) {
   if (!rt) return rrfp_fail(RRFP_E_INVALID, "null runtime");
   RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
   if (!rt->built) {
-    int rc = build_graph(rt);
+    int rc = build_graph_on_stream_ctx(rt, (cudaStream_t)stream);
     if (rc) return rc;
   }
   RRFP_CUDA_TRY(cudaGraphUpload(rt->exec, (cudaStream_t)stream));
@@ -764,7 +805,7 @@ extern "C" int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream
   RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
   (void)epoch;
   if (!rt->built) {
-    int rc = build_graph(rt);
+    int rc = build_graph_on_stream_ctx(rt, (cudaStream_t)stream);
     if (rc) return rc;
   }
   *rt->abort_host = 0;

@@ -95,7 +95,8 @@ class GpuPipeline:
                  mode="free", decompose=None, jitter: JitterConfig | None = None, seed: int = 0,
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
                  schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
-                 n_chunks: int = 1, mm=None, head_cost: float = 0.0, gemm_sm_cap: int = 0, w_split: str = "fc"):
+                 n_chunks: int = 1, mm=None, head_cost: float = 0.0, gemm_sm_cap: int = 0, w_split: str = "fc",
+                 green: bool = False):
         if mm is not None and (tp_size > 1 or n_chunks > 1):
             raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
         if isinstance(hint, str):
@@ -134,6 +135,27 @@ class GpuPipeline:
                                    mm=mm, head_cost=head_cost if C == 1 else 0.0, w_split=w_split)
                       for r in range(R)] for v in range(V)]
         self.stages = [row[0] for row in self.grid]
+        # green=True (single-GPU pipeline emulation): every lane gets a disjoint SM
+        # partition (CUDA green context); its bodies are captured on the partition's
+        # streams, so their kernels run only there -- an idle stage's SMs stay idle
+        self.green_streams = {}
+        if green:
+            import ctypes
+            from . import _lib
+            if len(set(devices)) != 1 or R != 1:
+                raise ValueError("green partitions emulate a pipeline on ONE device without TP")
+            arr = (ctypes.c_void_p * (2 * N))()
+            sms = ctypes.c_int()
+            n_sm = torch.cuda.get_device_properties(devices[0]).multi_processor_count
+            _lib.check(_lib.lib().rrfp_green_streams(devices[0], N, max(2, (n_sm // N) & ~1), arr,
+                                                     ctypes.byref(sms)))
+            self.green_sms = sms.value
+            gemm_sm_cap = sms.value & ~1
+            for s_ in range(N):
+                self.green_streams[s_] = (torch.cuda.ExternalStream(arr[2 * s_], device=devices[0]),
+                                          torch.cuda.ExternalStream(arr[2 * s_ + 1], device=devices[0]))
+            for v in range(V):
+                self.grid[v][0].side = self.green_streams[v % N][1]
         for row in self.grid:
             for st in row:
                 st.gemm_sm_cap = gemm_sm_cap
@@ -150,7 +172,8 @@ class GpuPipeline:
         for comms in self.comms.values():
             for c in comms:
                 c.local_only = True
-        streams = {(v, r): torch.cuda.Stream(torch.device("cuda", devices[v % N]))
+        streams = {(v, r): (self.green_streams[v % N][0] if green else
+                            torch.cuda.Stream(torch.device("cuda", devices[v % N])))
                    for v in range(V) for r in range(R)}
         # the warm-up streams must see the parameter / token initialisation queued on the
         # current stream: an embedding reading a token buffer that is still being written
@@ -183,7 +206,8 @@ class GpuPipeline:
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
                                tp=tp or (TpGroup(group_size=R) if R > 1 else None),
                                placement=[[d] * R for d in devices], bodies=bodies, compute_kind=1,
-                               schedule=schedule)
+                               schedule=schedule,
+                               lane_streams={(s_, 0): self.green_streams[s_][0] for s_ in self.green_streams})
         self.last_events = None
 
     def step(self, watchdog_secs: float = 120.0, zero_grads: bool = True):

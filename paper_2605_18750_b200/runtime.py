@@ -66,7 +66,7 @@ class LaneGroup:
                  tp: TpGroup | None = None, mode: str = "free", schedule: FixedSchedule | None = None,
                  placement=None, local=None, bodies=None, compute_kind: int = 0,
                  trace_cap: int | None = None, pad_table_us=None, defer_bodies: bool = False,
-                 floor_table_us=None):
+                 floor_table_us=None, lane_streams=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("run_gpu needs a CUDA device (B200)")
@@ -120,7 +120,8 @@ class LaneGroup:
             _lib.check(self.L.rrfp_runtime_create(C.byref(d), C.byref(h)))
             self.lanes[(s, k)] = h
             dev = torch.device("cuda", placement[s][k])
-            self.streams[(s, k)] = torch.cuda.Stream(dev)
+            # (lane_streams: e.g. a green-context partition's stream, see pipeline.py)
+            self.streams[(s, k)] = (lane_streams or {}).get((s, k)) or torch.cuda.Stream(dev)
             # tables (ns)
             if compute_kind == 0:
                 dur = tb.dur[s].astype(np.float64) * 1000.0 * time_scale

@@ -155,3 +155,21 @@ def test_zb_h1_schedule_gpt_pipeline_matches_fp32_reference():
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+def test_green_partition_pipeline_matches_fp32_reference():
+    """The single-GPU pipeline emulation: each stage on its own SM partition
+    (green context); numerics unchanged."""
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, 4, 4, hint="bfw", green=True)
+    try:
+        assert pipe.green_sms >= 2
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
