@@ -192,7 +192,7 @@ def iteration_flops(args, cfg):
 
 
 def workload_config(args, n):
-    from paper_2605_18750_b200.model import split_layers
+    from paper_2605_18750_b200.model import split_units
     c = model_config(args)
     if args.model == "mm":
         return {"workload": f"config 4: ViT-H/14 (32 L, d=1280, 256 tok/image, 1..8 images/mb seeded) on stage 0 "
@@ -205,8 +205,10 @@ def workload_config(args, n):
                         f"ffn={c.d_ff}, V={c.vocab}, s={c.seq}, mbs=1), PP={n}, TP={args.tp}, C={args.chunks}, M={args.mb}",
             "model": f"gpt-{args.model}-synthetic", "global_batch": args.mb, "seq_len": c.seq,
             "parallelism": par, "hint": args.hint, "jitter": args.jitter,
-            "layer_split": [len(split_layers(c.n_layer, n, s_, args.head_cost if args.chunks == 1 else 0))
-                            for s_ in range(n)],
+            "layer_split": [[f"{l}{pt[0] if pt != 'full' else ''}" for l, pt in
+                             split_units(c.n_layer, n * args.chunks, s_, args.head_cost if args.chunks == 1 else 0,
+                                         stage_split(args))] for s_ in range(n * args.chunks)]
+                           if n * args.chunks > 1 else [c.n_layer],
             "buffer_limit": 32, "l2": "inputs larger than L2 (activations >> 126 MB per step)"}
 
 
@@ -426,8 +428,9 @@ def run_ours(args):
     if args.emulate_pp > 1 and world == 1:
         # a fresh process: the PP=1 pipeline's ~110 GB must not share the GPU with it
         cmd = [sys.executable, os.path.abspath(__file__), "--emulate-only", "--emulate-pp", str(args.emulate_pp),
-               "--w-split", args.w_split,
+               "--w-split", args.w_split, "--split", args.split,
                *([] if args.green else ["--no-green"]),
+               *(["--trace-dir", args.trace_dir] if args.trace_dir else []),
                "--steps", str(args.steps), "--warmup", str(args.warmup), "--mb", str(args.mb),
                "--sigmas", args.sigmas, "--compare-jitter", args.compare_jitter, "--comm-us", str(args.comm_us),
                "--head-cost", str(args.head_cost), "--model", args.model]
@@ -447,12 +450,17 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def stage_split(args):
+    """Stage boundaries at half-layers for the GPT pipeline (model.split_units); config 4 splits at layers."""
+    return "layer" if args.model == "mm" else args.split
+
+
 def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     if world > 1:
         from paper_2605_18750_b200.distributed import DistPipeline
         pipe = DistPipeline(cfg, args.mb, hint=hint, mode=mode, jitter=jitter, comm_delay=comm_delay,
                             tp_size=args.tp, n_chunks=args.chunks, mm=mm_spec(args), head_cost=args.head_cost,
-                            w_split=args.w_split)
+                            w_split=args.w_split, split=stage_split(args))
         return pipe, pipe.vstages
     if args.model == "mm":
         raise SystemExit("--model mm (config 4) needs a pipeline of >= 2 GPUs")
@@ -473,10 +481,14 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
     import math
     import numpy as np
     import paper_2605_18750_b200 as P
-    from paper_2605_18750_b200.model import split_layers
+    from paper_2605_18750_b200.model import ATTN_FRAC, split_units
     from paper_2605_18750_b200.rng import substream
     L = cfg.n_layer
-    lay0 = [len(split_layers(L, n_meas, s_, args.head_cost)) for s_ in range(n_meas)]
+
+    def layer_eq(n, s_):   # the stage's layers in layer-equivalents (half-layers: ATTN_FRAC / 1 - ATTN_FRAC)
+        w = {"full": 1.0, "attn": ATTN_FRAC, "mlp": 1.0 - ATTN_FRAC}
+        return sum(w[pt] for _, pt in split_units(L, n, s_, args.head_cost, stage_split(args)))
+    lay0 = [layer_eq(n_meas, s_) for s_ in range(n_meas)]
     # per-layer times from the measured first stage (no head), head from the last stage
     f_l = task_us["F"][0] / lay0[0]
     b_l = task_us["B"][0] / lay0[0]
@@ -490,7 +502,7 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
     out = {"definition": pipeline_model.__doc__.split("\n\n")[0].strip().replace("\n", " "),
            "per_layer_us": {"F": round(f_l, 1), "B": round(b_l, 1)}, "head_us": {"F": round(f_h, 1), "B": round(b_h, 1)}}
     for n in pps:
-        lay = [len(split_layers(L, n, s_, args.head_cost)) for s_ in range(n)]
+        lay = [round(layer_eq(n, s_), 2) for s_ in range(n)]
         row = {"layers": lay}
         for sigma in sigmas:
             res = {}
@@ -553,7 +565,7 @@ def emulated_pp(args, cfg):
         t0 = time.perf_counter()
         pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.compare_jitter],
                            head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split,
-                           green=args.green)
+                           green=args.green, split=stage_split(args))
         out["gemm_sm_cap"] = getattr(pipe, "green_sms", cap) if args.green else cap
         build_s = time.perf_counter() - t0
         for _ in range(2):
@@ -570,19 +582,26 @@ def emulated_pp(args, cfg):
             pipe.step()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(cur)
-            for _ in range(args.steps):
-                pipe.launch()
-                pipe.wait()
-            for st in pipe.group.streams.values():
-                cur.wait_stream(st)
-            e1.record(cur)
-            torch.cuda.synchronize()
+            with ClockSampler(torch.cuda.current_device()) as clk:
+                e0.record(cur)
+                for _ in range(args.steps):
+                    pipe.launch()
+                    pipe.wait()
+                for st in pipe.group.streams.values():
+                    cur.wait_stream(st)
+                e1.record(cur)
+                torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.steps
             tr, met = pipe.trace()
+            if args.trace_dir:
+                os.makedirs(args.trace_dir, exist_ok=True)
+                tr.dump_jsonl(os.path.join(args.trace_dir, f"pp{N}_{name}_sigma{sigma}.jsonl"))
             out["variants"][f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
                 "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
-                "bubble_fraction": round(met.bubble_fraction(), 4), "build_s": round(build_s, 1)}
+                "bubble_fraction": round(met.bubble_fraction(), 4), "build_s": round(build_s, 1),
+                # all N stages share this GPU's power budget: a schedule that keeps
+                # more stages busy runs at a lower SM clock than on N separate GPUs
+                "sm_mhz": clk.summary()["sm_mhz"]}
             _log(f"emulated PP={N} {name} sigma={sigma}: {ms:.1f} ms")
         pipe.close()
         del pipe
@@ -747,8 +766,12 @@ def main():
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     ap.add_argument("--w-split", dest="w_split", default="fc", choices=["fc", "all"],
                     help="BFW: weight gradients deferred to the W task (fc: FC1/FC2; all: all four)")
+    ap.add_argument("--split", default="half", choices=["half", "layer"],
+                    help="GPT stage boundaries: at half-layers (attention | MLP, balanced; default) or layers")
     ap.add_argument("--no-green", dest="green", action="store_false",
                     help="emulation without SM partitions (GEMM grids capped only)")
+    ap.add_argument("--trace-dir", dest="trace_dir", default=None,
+                    help="write each emulated variant's wall trace (JSONL) here")
     ap.add_argument("--emulate-only", dest="emulate_only", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "

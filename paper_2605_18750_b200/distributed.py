@@ -109,7 +109,8 @@ class DistPipeline:
 
     def __init__(self, cfg, n_mb: int, *, hint="bf", buffer_limit=32, mode="free", jitter=None,
                  seed=0, model_seed=1234, data_seed=0, schedule=None, group=None, comm_delay=None,
-                 tp_size: int = 1, tp=None, n_chunks: int = 1, mm=None, head_cost: float = 0.0, w_split: str = "fc"):
+                 tp_size: int = 1, tp=None, n_chunks: int = 1, mm=None, head_cost: float = 0.0, w_split: str = "fc",
+                 split: str = "layer"):
         import torch.distributed as dist
         from .arbitration import HintOrder, TpGroup
         from .model import StageCompute
@@ -154,7 +155,7 @@ class DistPipeline:
                 fwd_in=wrap_bf16(fb.ptr.value, shapes[v][0], self.device) if fb else None,
                 bwd_in=wrap_bf16(bb.ptr.value, shapes[v][1], self.device) if bb else None,
                 tp_rank=r, tp_size=R, tp=self.comm, mm=mm, head_cost=head_cost if C == 1 else 0.0,
-                w_split=w_split))
+                w_split=w_split, split=split))
         # the lane's first / last virtual stages (loss lives on virtual stage V-1)
         self.stage = self.vstages[-1] if self.vstages[-1].last else self.vstages[0]
         w = nominal_workload(cfg, n, n_mb, decompose, tp_size=R, n_chunks=C)

@@ -130,6 +130,89 @@ def split_layers(n_layer: int, n_stages: int, stage: int, head_cost: float = 0.0
     return list(range(lo, lo + counts[stage]))
 
 
+ATTN_KEYS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o")
+MLP_KEYS = ("ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")
+# attention half's share of a layer's F+B time (LN1 + QKV + SDPA + out-proj vs LN2 +
+# FC1 + FC2): 8·S·D² + 2·S²·D of 26·S·D² matmul FLOPs at S = D (0.385), raised for the
+# SDPA kernels' lower efficiency than the GEMMs' -- measured F+B per half-layer on 16
+# SMs (profiles/r01_emulated_pp8_half.json)
+ATTN_FRAC = 0.42
+
+
+def split_units(n_layer: int, n_stages: int, stage: int, head_cost: float = 0.0,
+                split: str = "layer", attn_frac: float = ATTN_FRAC):
+    """This stage's share of the model as [(global layer, part)], part "full" /
+    "attn" (LN1 -> QKV -> attention -> out-proj + residual) / "mlp" (LN2 -> FC1
+    -> GELU -> FC2 + residual).
+
+    split "layer": whole layers, split_layers().  split "half": stage boundaries
+    may also fall between a layer's attention and MLP halves (the residual
+    stream crossing there is the same [S, D] activation the mailbox carries at a
+    layer boundary); the contiguous partition of the 2·L half-layer units (+ the
+    LM head on the last stage) minimises the largest stage cost, then the sum of
+    squared stage costs.  24 layers / 8 stages / head 1.4: bottleneck 3.32
+    layer-equivalents instead of 4.0."""
+    if split == "layer":
+        return [(l, "full") for l in split_layers(n_layer, n_stages, stage, head_cost)]
+    if split != "half":
+        raise ValueError("split must be 'layer' or 'half'")
+    units = [(l, part) for l in range(n_layer) for part in ("attn", "mlp")]
+    cost = [attn_frac if part == "attn" else 1.0 - attn_frac for _, part in units]
+    bounds = _balanced_partition(cost, n_stages, head_cost, os.environ.get("RRFP_SPLIT_ORDER", "front") == "front")
+    own = units[bounds[stage]:bounds[stage + 1]]
+    out = []
+    for l, part in own:            # attn + mlp of one layer on one stage = "full"
+        if out and out[-1][0] == l:
+            out[-1] = (l, "full")
+        else:
+            out.append((l, part))
+    return out
+
+
+def _balanced_partition(cost, n, tail, front: bool = True):
+    """Cut points b[0..n] of `cost` into n non-empty contiguous segments (the last
+    one also carries `tail`): min over partitions of the max segment cost, ties
+    broken by the smallest sum of squares, then (front) by putting the heavier
+    segments first -- a pipeline's first stages never wait for an activation,
+    so excess work costs least there.  O(n·U²), U = len(cost)."""
+    U = len(cost)
+    if U < n:
+        raise ValueError(f"{U} units cannot fill {n} stages")
+    pre = [0.0]
+    for c in cost:
+        pre.append(pre[-1] + c)
+    seg = lambda i, j, k: pre[j] - pre[i] + (tail if k == n - 1 else 0.0)
+    INF = float("inf")
+
+    def solve(key, cap):
+        # best[k][j]: the first j units in k+1 segments; key(acc, segment cost, k)
+        best = [[INF] * (U + 1) for _ in range(n)]
+        arg = [[-1] * (U + 1) for _ in range(n)]
+        for j in range(1, U + 1):
+            c = seg(0, j, 0)
+            if c <= cap:
+                best[0][j], arg[0][j] = key(0.0, c, 0), 0
+        for k in range(1, n):
+            for j in range(k + 1, U + 1):
+                for i in range(k, j):
+                    c = seg(i, j, k)
+                    if best[k - 1][i] == INF or c > cap:
+                        continue
+                    v = key(best[k - 1][i], c, k)
+                    if v < best[k][j] - 1e-12:
+                        best[k][j], arg[k][j] = v, i
+        b, j = [U], U
+        for k in range(n - 1, 0, -1):
+            j = arg[k][j]
+            b.append(j)
+        return best[n - 1][U], [0] + b[::-1]
+
+    m, _ = solve(lambda acc, c, k: max(acc, c), INF)
+    bias = 1e-4 if front else 0.0
+    _, bounds = solve(lambda acc, c, k: acc + c * c + bias * k * c, m + 1e-9)
+    return bounds
+
+
 def _gen(device, seed):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -246,11 +329,19 @@ class RawBuffer:
         return self._s0 if i == 0 else 1
 
 
+def _half(p: dict, part: str) -> dict:
+    """The parameters a (half-)layer holds on this stage."""
+    if part == "full":
+        return p
+    return {k: p[k] for k in (ATTN_KEYS if part == "attn" else MLP_KEYS)}
+
+
 class StageCompute:
     def __init__(self, cfg: GPTConfig, stage: int, n_stages: int, n_mb: int, device, *,
                  decompose: bool = False, seed: int = 1234, data_seed: int = 0,
                  fwd_in=None, bwd_in=None, tp_rank: int = 0, tp_size: int = 1, tp=None,
-                 mm: MultimodalSpec | None = None, head_cost: float = 0.0, w_split: str = "fc"):
+                 mm: MultimodalSpec | None = None, head_cost: float = 0.0, w_split: str = "fc",
+                 split: str = "layer", attn_frac: float = ATTN_FRAC):
         self.cfg, self.stage, self.n_stages, self.M = cfg, stage, n_stages, n_mb
         self.device = torch.device(device)
         self.decompose = decompose
@@ -271,8 +362,14 @@ class StageCompute:
         else:
             part, idx, cnt = "gpt", stage, n_stages
         self.part = part
-        # head_cost > 0: balance the layer split against the last stage's LM head
-        self.layers = split_layers(cfg.n_layer, cnt, idx, head_cost if part != "vit" else 0.0)
+        # head_cost > 0: balance the layer split against the last stage's LM head;
+        # split "half": stage boundaries may fall inside a layer (split_units), so
+        # the first layer may be its MLP half only and the last its attention half
+        if split != "layer" and part != "gpt":
+            raise ValueError("split='half' is for the GPT pipeline (not config 4)")
+        units = split_units(cfg.n_layer, cnt, idx, head_cost if part != "vit" else 0.0, split, attn_frac)
+        self.layers = [l for l, _ in units]
+        self.parts = [pt for _, pt in units]
         # prologue: token embedding (GPT stage 0), patch embedding (ViT stage 0), or
         # merge (first LLM stage: projected visual rows arrive in the mailbox, text
         # rows are embedded here); epilogue: LM head + loss, or the ViT projector
@@ -297,8 +394,8 @@ class StageCompute:
         lseed = seed + 17 if part == "vit" else seed      # ViT layers: their own init stream
         self.layer_seed = lseed
         with torch.no_grad():
-            self.p = [shard_layer_params(cfg, init_layer_params(cfg, l, dev, lseed), tp_rank, tp_size)
-                      for l in self.layers]
+            self.p = [_half(shard_layer_params(cfg, init_layer_params(cfg, l, dev, lseed), tp_rank, tp_size), pt)
+                      for l, pt in units]
             self.emb = init_embed_params(cfg, dev, seed) if self.prologue in ("tokens", "merge") else None
             self.head = init_head_params(cfg, dev, seed) if self.last else None
             self.pe = init_mm_params(mm, dev, seed, "pe") if self.prologue == "patches" else None
@@ -438,16 +535,28 @@ class StageCompute:
                     K._p(self.tokens[mb, t0:]), K._p(self.emb["wte"]), K._p(self.emb["wpe"][t0:]),
                     K._p(x[t0:]), S - t0, D, K._stream()))
         for li, p in enumerate(self.p):
-            h1, qkv, x2 = self.h1[mb, li, :T], self.qkv[mb, li, :T], self.x2[mb, li, :T]
+            part = self.parts[li]
+            h1, qkv = self.h1[mb, li, :T], self.qkv[mb, li, :T]
             h2, pre, act = self.h2[mb, li, :T], self.pre[mb, li, :T], self.act[mb, li, :T]
-            _ln_fwd(x, p["ln1_g"], p["ln1_b"], h1, self.m1[mb, li, :T], self.r1[mb, li, :T], cfg.eps)
-            K.gemm(h1, p["w_qkv"], qkv, bias=p["b_qkv"])
-            self._attn_fwd(qkv, mb, li)
-            if self.R == 1:
-                K.gemm(self.o_view[mb][li], p["w_o"], x2, epi=K.EPI_RESID, bias=p["b_o"], r=x)
-            else:   # row-parallel: partial sum, then all-reduce (+ b_o + residual) over the TP group
-                K.gemm(self.o_view[mb][li], p["w_o"], self.tp.partial, m=S, n=D, k=self.Dl)
-                self.tp.allreduce([x2], bias=p["b_o"], resid=x)
+            if part == "mlp":         # the attention half ran on the previous stage
+                x2 = x
+            else:
+                # an attention half ending the stage writes the next stage's mailbox
+                x2s = ([o[:T] for o in self._layer_output(mb, li)] if part == "attn"
+                       else [self.x2[mb, li, :T]])
+                x2 = x2s[0]
+                _ln_fwd(x, p["ln1_g"], p["ln1_b"], h1, self.m1[mb, li, :T], self.r1[mb, li, :T], cfg.eps)
+                K.gemm(h1, p["w_qkv"], qkv, bias=p["b_qkv"])
+                self._attn_fwd(qkv, mb, li)
+                if self.R == 1:
+                    K.gemm(self.o_view[mb][li], p["w_o"], x2, epi=K.EPI_RESID, bias=p["b_o"], r=x,
+                           m=T, n=D, k=self.Dl)
+                else:   # row-parallel: partial sum, then all-reduce (+ b_o + residual) over the TP group
+                    K.gemm(self.o_view[mb][li], p["w_o"], self.tp.partial, m=S, n=D, k=self.Dl)
+                    self.tp.allreduce(x2s, bias=p["b_o"], resid=x)
+                if part == "attn":
+                    x = x2
+                    continue
             _ln_fwd(x2, p["ln2_g"], p["ln2_b"], h2, self.m2[mb, li, :T], self.r2[mb, li, :T], cfg.eps)
             K.gemm(h2, p["w_1"], pre, epi=K.EPI_BIAS_GELU, c2=act, bias=p["b_1"])
             outs = [o[:T] for o in self._layer_output(mb, li)]   # last layer: next stage's mailbox
@@ -557,15 +666,29 @@ class StageCompute:
             K.gemm(dyp, pj["w_proj"], dy, b_mn=True, m=T, n=D, k=dyp.shape[1])
         else:
             dy = self.bwd_in[mb][:T]
-            if dec:
+            if dec and self.parts[-1] != "attn":   # (the W task reads it; an attention half: see below)
                 self.gy[mb, nl - 1, :T].copy_(dy)
                 dy = self.gy[mb, nl - 1, :T]
         Dl, Fl = self.Dl, self.Fl
         d_head = self.d_head[:T]
+        def stage_dx():
+            """Destination of the stage's input gradient (+ the other TP ranks' copies)."""
+            if self.prologue is None:
+                if self.bwd_out is not None:
+                    return self.bwd_out[mb][0][:T], [o[:T] for o in self.bwd_out[mb][1:]]
+                dx = self.sd_a[1][:T]
+            else:   # prologue stages keep the input gradient for the embedding backward
+                dx = (self.gx0[mb] if dec else self.sd_a[1])[:T]
+            if 1 in side_done:   # layer 1's side work read sd_a[1]
+                main.wait_event(side_done[1])
+            return dx, []
+
         for li in reversed(range(nl)):
             p, g = self.p[li], self.g[li]
+            part = self.parts[li]
             x = self._layer_input(mb, li)
-            h1, x2, h2 = self.h1[mb, li, :T], self.x2[mb, li, :T], self.h2[mb, li, :T]
+            h1, h2 = self.h1[mb, li, :T], self.h2[mb, li, :T]
+            x2 = x if part == "mlp" else self.x2[mb, li, :T]
             pre, act = self.pre[mb, li, :T], self.act[mb, li, :T]
             q = li % 2
             if li + 2 in side_done:          # set q was last read by layer li+2's side work
@@ -574,26 +697,41 @@ class StageCompute:
             defer_attn = dec and self.w_split == "all"
             d_x2 = (self.gx2[mb, li] if defer_attn else self.sd_b[q])[:T]
             d_qkv = (self.gqkv[mb, li] if defer_attn else self.sd_qkv[q])[:T]
-            if fused_w:
-                dyy = dy
-                on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=T),
-                                       _bias_grad(dyy, g["b_2"])))
-            # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
-            K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D)
-            if fused_w:
-                on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
-                                              a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
-                                       _bias_grad(d_pre, g["b_1"])))
-            # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy)
-            self._dgrad_reduce(d_pre, p["w_1"], Fl, T)
-            _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
-                    d_x2, g["ln2_g"], g["ln2_b"])
+            extra = []
+            if part == "attn":   # the MLP half is on the next stage: dy is the gradient of x2
+                if defer_attn:
+                    d_x2.copy_(dy)
+                else:
+                    d_x2 = dy
+            else:
+                if part == "mlp":    # (always the stage's first layer) LN2 backward ends the stage
+                    d_x2, extra = stage_dx()
+                if fused_w:
+                    dyy = dy
+                    on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
+                                                  a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=T),
+                                           _bias_grad(dyy, g["b_2"])))
+                # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
+                K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D)
+                if fused_w:
+                    on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
+                                                  a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
+                                           _bias_grad(d_pre, g["b_1"])))
+                # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy)
+                self._dgrad_reduce(d_pre, p["w_1"], Fl, T)
+                _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
+                        d_x2, g["ln2_g"], g["ln2_b"])
+                if part == "mlp":
+                    for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
+                        _copy_rows(dst, d_x2, T, D)
+                    dy = d_x2
+                    continue
             ov = self.o_view[mb][li]
             if not defer_attn:
-                on_side(ev(), lambda: (K.gemm(d_x2, ov, g["w_o"], epi=K.EPI_ACC_F32,
+                dxx = d_x2
+                on_side(ev(), lambda: (K.gemm(dxx, ov, g["w_o"], epi=K.EPI_ACC_F32,
                                               a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
-                                       _bias_grad(d_x2, g["b_o"])))
+                                       _bias_grad(dxx, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
             d_o = d_head if self.R == 1 else self.d_o
             K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=T, n=Dl, k=D)
@@ -609,20 +747,12 @@ class StageCompute:
                 side_done[li] = done
             self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
-            extra = []
             if li > 0:
                 dx = dy_buf(li - 1)
                 if li + 1 in side_done:   # layer li+1's side work read this buffer
                     main.wait_event(side_done[li + 1])
-            elif self.prologue is None:
-                if self.bwd_out is not None:
-                    dx, extra = self.bwd_out[mb][0][:T], [o[:T] for o in self.bwd_out[mb][1:]]
-                else:
-                    dx = self.sd_a[1][:T]
-            else:   # prologue stages keep the input gradient for the embedding backward
-                dx = (self.gx0[mb] if dec else self.sd_a[1])[:T]
-                if 1 in side_done:
-                    main.wait_event(side_done[1])
+            else:
+                dx, extra = stage_dx()
             _ln_bwd(d_head, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
                     g["ln1_g"], g["ln1_b"])
             for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
@@ -715,14 +845,16 @@ class StageCompute:
         for li in reversed(range(len(self.layers))):
             g = self.g[li]
             gy, gpre = self.gy[mb, li, :T], self.gpre[mb, li, :T]
+            part = self.parts[li]
             with torch.cuda.stream(side if li % 2 else main):
-                K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=D, n=Fd, k=T)
-                _bias_grad(gy, g["b_2"])
-                K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
-                       b_mn=True, accumulate=True, m=Fd, n=D, k=T)
-                _bias_grad(gpre, g["b_1"])
-                if self.w_split == "all":
+                if part != "attn":
+                    K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=D, n=Fd, k=T)
+                    _bias_grad(gy, g["b_2"])
+                    K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
+                           b_mn=True, accumulate=True, m=Fd, n=D, k=T)
+                    _bias_grad(gpre, g["b_1"])
+                if self.w_split == "all" and part != "mlp":
                     gx2, gqkv = self.gx2[mb, li, :T], self.gqkv[mb, li, :T]
                     K.gemm(gx2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,
                            b_mn=True, accumulate=True, m=D, n=Dl, k=T)

@@ -96,7 +96,7 @@ class GpuPipeline:
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
                  schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
                  n_chunks: int = 1, mm=None, head_cost: float = 0.0, gemm_sm_cap: int = 0, w_split: str = "fc",
-                 green: bool = False):
+                 green: bool = False, split: str = "layer"):
         if mm is not None and (tp_size > 1 or n_chunks > 1):
             raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
         if isinstance(hint, str):
@@ -132,7 +132,8 @@ class GpuPipeline:
         self.grid = [[StageCompute(stage_cfg(v), v, V, n_mb, torch.device("cuda", devices[v % N]),
                                    decompose=decompose, seed=model_seed, data_seed=data_seed,
                                    tp_rank=r, tp_size=R, tp=self.comms[v % N][r] if R > 1 else None,
-                                   mm=mm, head_cost=head_cost if C == 1 else 0.0, w_split=w_split)
+                                   mm=mm, head_cost=head_cost if C == 1 else 0.0, w_split=w_split,
+                                   split=split)
                       for r in range(R)] for v in range(V)]
         self.stages = [row[0] for row in self.grid]
         # green=True (single-GPU pipeline emulation): every lane gets a disjoint SM

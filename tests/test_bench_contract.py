@@ -26,10 +26,17 @@ def test_pipeline_model_on_host_twin():
     sys.path.insert(0, ROOT)
     import bench
     from paper_2605_18750_b200.model import GPTConfig
-    args = argparse.Namespace(head_cost=1.4, mb=8, comm_us=100.0)
+    args = argparse.Namespace(head_cost=1.4, mb=8, comm_us=100.0, model="1.3b", split="layer")
     out = bench.pipeline_model(args, GPTConfig(), {"F": [6400.0], "B": [12700.0]}, 1, pps=(2, 8),
                                device="cpu")
     assert out["pp8"]["layers"] == [4, 3, 3, 3, 3, 3, 3, 2]
+    args.split = "half"
+    half = bench.pipeline_model(args, GPTConfig(), {"F": [6400.0], "B": [12700.0]}, 1, pps=(8,),
+                                device="cpu")
+    assert half["pp8"]["layers"] == [3.42, 3.58, 3, 3, 3, 3, 3, 2.0]   # heavier stages first
+    # without jitter the bottleneck sets the pace: the balanced split is faster
+    assert half["pp8"]["sigma0.0"]["1f1b"]["ms"] <= out["pp8"]["sigma0.0"]["1f1b"]["ms"]
+    assert half["pp8"]["sigma0.0"]["bfw"]["ms"] < out["pp8"]["sigma0.0"]["bfw"]["ms"]
     for pp in ("pp2", "pp8"):
         for sig in ("sigma0.0", "sigma0.5"):
             r = out[pp][sig]

@@ -91,3 +91,31 @@ def test_balanced_layer_split():
         even = [len(split_layers(L, N, s)) + (h if s == N - 1 else 0) for s in range(N)]
         assert max(cost) <= max(even)
     assert [len(split_layers(24, 8, s, 1.4)) for s in range(8)] == [4, 3, 3, 3, 3, 3, 3, 2]
+
+
+def test_half_layer_split_is_optimal_and_contiguous():
+    """split_units('half'): contiguous, covers every (layer, half) once, and its
+    bottleneck equals the brute-force optimum over all cut placements."""
+    import itertools
+    from paper_2605_18750_b200.model import split_units
+    a = 0.42
+    w = {"full": 1.0, "attn": a, "mlp": 1 - a}
+    for L, N, h in [(4, 3, 1.4), (4, 3, 0.0), (5, 4, 1.4), (6, 4, 0.7), (3, 5, 1.4)]:
+        parts = [split_units(L, N, s, h, "half", a) for s in range(N)]
+        flat = []
+        for p in parts:
+            assert p, "empty stage"
+            for l, pt in p:
+                flat += [(l, "attn"), (l, "mlp")] if pt == "full" else [(l, pt)]
+        assert flat == [(l, pt) for l in range(L) for pt in ("attn", "mlp")]
+        got = max(sum(w[pt] for _, pt in p) + (h if s == N - 1 else 0) for s, p in enumerate(parts))
+        cost = [a if i % 2 == 0 else 1 - a for i in range(2 * L)]
+        best = min(max(sum(cost[b[i]:b[i + 1]]) + (h if i == N - 1 else 0) for i in range(N))
+                   for cuts in itertools.combinations(range(1, 2 * L), N - 1)
+                   for b in [(0, *cuts, 2 * L)])
+        assert abs(got - best) < 1e-9, (L, N, h, got, best)
+    # 1.3B at PP=8: 3.58 layer-equivalents at the bottleneck instead of 4.0
+    costs = [sum(w[pt] for _, pt in split_units(24, 8, s, 1.4, "half", a)) + (1.4 if s == 7 else 0)
+             for s in range(8)]
+    assert abs(max(costs) - 3.58) < 1e-9
+    assert [l for l, _ in split_units(24, 8, 0, 1.4, "layer")] == [0, 1, 2, 3]

@@ -16,11 +16,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("hint,tp,nproc,chunks,model", [("bf", 1, 2, 1, "gpt"), ("bfw", 1, 2, 1, "gpt"),
                                                         ("bf", 2, 2, 1, "gpt"), ("bfw", 2, 4, 1, "gpt"),
-                                                        ("bf", 1, 2, 2, "gpt"), ("bfw", 1, 2, 1, "mm")])
+                                                        ("bf", 1, 2, 2, "gpt"), ("bfw", 1, 2, 1, "mm"),
+                                                        ("bfw", 1, 3, 1, "half")])
 def test_multi_process_pipeline_matches_single_process(hint, tp, nproc, chunks, model):
     """PP=2 (tp=1), TP=2 x PP=1, TP=2 x PP=2 and PP=2 x C=2 (chunk wrap across
-    processes), and config 4 (ViT process -> LLM process, variable-row
-    messages): IPC mailboxes written by every sender TP rank, peer-memory
+    processes), config 4 (ViT process -> LLM process, variable-row messages),
+    and PP=3 with stage cuts inside layers (split "half"): IPC mailboxes written by every sender TP rank, peer-memory
     all-reduce between processes.  The reference is the same model in one process."""
     env = dict(os.environ, RRFP_SAME_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",

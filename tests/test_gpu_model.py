@@ -34,16 +34,24 @@ def test_eager_single_stage_matches_fp32_reference():
     assert not compare(ref_grads, device_grads([st]))
 
 
-@pytest.mark.parametrize("n_stages,hint,mode,head_cost,w_split", [
-    (1, "bf", "free", 0, "fc"), (2, "bf", "free", 0, "fc"), (4, "bfw", "free", 0, "fc"),
-    (2, "bf", "fixed", 0, "fc"), (4, "bf", "replay", 0, "fc"), (2, "bfw", "free", 1.4, "fc"),
-    (2, "bfw", "free", 0, "all")])
-def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode, head_cost, w_split):
+@pytest.mark.parametrize("n_stages,hint,mode,head_cost,w_split,split", [
+    (1, "bf", "free", 0, "fc", "layer"), (2, "bf", "free", 0, "fc", "layer"),
+    (4, "bfw", "free", 0, "fc", "layer"), (2, "bf", "fixed", 0, "fc", "layer"),
+    (4, "bf", "replay", 0, "fc", "layer"), (2, "bfw", "free", 1.4, "fc", "layer"),
+    (2, "bfw", "free", 0, "all", "layer"),
+    # stage boundaries inside layers (attention half | MLP half)
+    (3, "bf", "free", 1.4, "fc", "half"), (3, "bfw", "free", 1.4, "fc", "half"),
+    (3, "bfw", "free", 0, "all", "half"), (5, "bf", "fixed", 1.4, "fc", "half")])
+def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode, head_cost, w_split, split):
     from paper_2605_18750_b200.pipeline import GpuPipeline
     cfg = _cfg()
-    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, head_cost=head_cost, w_split=w_split)
-    if head_cost:
+    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, head_cost=head_cost, w_split=w_split,
+                       split=split)
+    if head_cost and split == "layer":
         assert [len(st.layers) for st in pipe.stages] == [3, 1]   # balanced against the LM head
+    if split == "half":   # some stage starts with an MLP half and some ends with an attention half
+        assert any(st.parts[0] == "mlp" for st in pipe.stages)
+        assert any(st.parts[-1] == "attn" for st in pipe.stages)
     try:
         for _ in range(2):        # graphs replay: the second iteration must match too
             loss = pipe.step(watchdog_secs=60).item()
@@ -57,16 +65,17 @@ def test_pipeline_iteration_matches_fp32_reference(n_stages, hint, mode, head_co
         pipe.close()
 
 
-@pytest.mark.parametrize("n_stages,tp,hint,mode", [(1, 2, "bf", "free"), (2, 2, "bf", "free"),
-                                                   (2, 2, "bfw", "free"), (2, 2, "bf", "fixed")])
-def test_tp_pipeline_matches_fp32_reference(n_stages, tp, hint, mode):
+@pytest.mark.parametrize("n_stages,tp,hint,mode,split", [
+    (1, 2, "bf", "free", "layer"), (2, 2, "bf", "free", "layer"), (2, 2, "bfw", "free", "layer"),
+    (2, 2, "bf", "fixed", "layer"), (3, 2, "bfw", "free", "half")])
+def test_tp_pipeline_matches_fp32_reference(n_stages, tp, hint, mode, split):
     """Config 3 on one GPU: TP=2 lanes per stage, column/row-parallel GEMMs and
     the peer-memory all-reduce kernel; loss and (unsharded) gradients against
     the non-parallel fp32 reference; replicated gradients bit-identical across ranks."""
     from paper_2605_18750_b200.pipeline import GpuPipeline
     from ref_gpt import device_grads_tp
     cfg = _cfg()
-    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, tp_size=tp)
+    pipe = GpuPipeline(cfg, n_stages, 4, hint=hint, mode=mode, tp_size=tp, split=split)
     try:
         for _ in range(2):
             loss = pipe.step(watchdog_secs=60).item()

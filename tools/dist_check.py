@@ -26,13 +26,14 @@ def main():
     tp = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     chunks = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     mm = None
+    split = "half" if len(sys.argv) > 4 and sys.argv[4] == "half" else "layer"   # stage cuts inside layers
     if len(sys.argv) > 4 and sys.argv[4] == "mm":   # config 4: ViT stage(s) + LLM stage(s)
         from paper_2605_18750_b200.model import MultimodalSpec
         vit = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=512, vocab=0, seq=512, causal=False)
         cfg = GPTConfig(n_layer=2, d_model=256, n_head=2, d_ff=1024, vocab=512, seq=512)
         mm = MultimodalSpec(vit=vit, llm=cfg, vit_stages=world // 2, patch_tokens=128, d_patch=128,
                             max_images=4, image_seed=3)
-    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm)
+    pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm, split=split)
     losses = []
     import time
     wd = float(os.environ.get("RRFP_WATCHDOG", "60"))
@@ -54,7 +55,7 @@ def main():
         # peer buffers must have been unmapped, warm-up must see fresh init
         wl = pipe.workload
         pipe.close()
-        pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm)
+        pipe = DistPipeline(cfg, 4, hint=hint, tp_size=tp, n_chunks=chunks, mm=mm, split=split)
         loss2 = pipe.step(watchdog_secs=wd)
         losses.append(None if loss2 is None else loss2.item())
         ev, t0 = pipe.last_events
