@@ -367,6 +367,7 @@ def run_ours(args):
         h2d_all = int(hb.item())
     _log("timed region done")
     tr, met = gather_trace(pipe, dist, world)
+    from paper_2605_18750_b200.runtime import dispatch_latency
     bubble = met.bubble_fraction()
     it_s = 1000.0 / ms
     tok = args.mb * cfg.seq
@@ -406,6 +407,7 @@ def run_ours(args):
                                                  "+ per-GPU P2P + TP all-reduce bytes / 770 GB/s"},
             "roofline": roof,
             "task_us": task_us,
+            "dispatch": dispatch_latency(tr, n),
             "e2e": {"value": round(1.0 / e2e_s, 4), "unit": "iter/s",
                     "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": 4},
             "gpu_launches": int(launches) * args.steps,
@@ -552,7 +554,7 @@ def emulated_pp(args, cfg):
     import torch
     from paper_2605_18750_b200.jitter import PRESETS
     from paper_2605_18750_b200.pipeline import GpuPipeline
-    from paper_2605_18750_b200.runtime import wall_trace
+    from paper_2605_18750_b200.runtime import dispatch_latency
     from paper_2605_18750_b200.workload import CommDelay
     N = args.emulate_pp
     cap = (torch.cuda.get_device_properties(0).multi_processor_count // N) & ~1
@@ -599,6 +601,7 @@ def emulated_pp(args, cfg):
             out["variants"][f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
                 "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
                 "bubble_fraction": round(met.bubble_fraction(), 4), "build_s": round(build_s, 1),
+                "dispatch": dispatch_latency(tr, N),
                 # all N stages share this GPU's power budget: a schedule that keeps
                 # more stages busy runs at a lower SM clock than on N separate GPUs
                 "sm_mhz": clk.summary()["sm_mhz"]}
@@ -695,6 +698,10 @@ def compare_variants(cfg, args, world, dist, barrier):
             out[f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
                 "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
                 "bubble_fraction": round(met.bubble_fraction(), 4)}
+            if not dist or dist.get_rank() == 0:   # (rank 0 holds the gathered trace)
+                from paper_2605_18750_b200.runtime import dispatch_latency
+                out[f"{name}@{args.compare_jitter}+sigma{sigma}"]["dispatch"] = \
+                    dispatch_latency(tr, pipe.workload.num_stages)
             _log(f"variant {name} {args.compare_jitter} sigma={sigma}: {ms:.1f} ms")
         pipe.close()
         del pipe, stages

@@ -256,7 +256,7 @@ __device__ __forceinline__ uint32_t dec_code(const rrfp_decision& d) {
   return (uint32_t)d.kind | ((uint32_t)(d.mb & 1023) << 2) | ((uint32_t)(d.chunk & 15) << 12);
 }
 
-__global__ void __launch_bounds__(32, 1) lane_dispatch_kernel(lane_state* L) {
+__device__ void lane_dispatch(lane_state* L) {
   __shared__ uint32_t sF[RRFP_MAX_WORDS], sB[RRFP_MAX_WORDS];
   __shared__ int s_kind, s_exit;
   const int lane = threadIdx.x;
@@ -410,7 +410,10 @@ __device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long l
   int key = rrfp_key(mb, c, d.MW);
   int dkey = rrfp_key(mb, dst_c, d.MW);
   long long delay = L->comm_ns[(size_t)dir * L->KEYS + key];
-  for (int r = 0; r < d.R; ++r) {
+  // TP: rank r flags only rank r of the neighbour stage (the reference's
+  // per-rank delivery, arrival = this rank's end + delay + skew[r]); the bytes
+  // were written to every receiver rank's mailbox by every sender rank
+  for (int r = d.rank; r == d.rank; ++r) {
     lane_inbox* in = dsts[r];
     long long sk = L->dskew_ns[((size_t)dir * L->KEYS + dkey) * d.R + r];
     unsigned long long vis = end + (unsigned long long)(delay + sk);
@@ -428,8 +431,8 @@ __device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long l
     ring_emit(L, 1, end, end + (unsigned long long)delay, -1, rrfp_make_task(dir, d.stage, mb, c));
 }
 
-__global__ void lane_complete_kernel(lane_state* L) {
-  if (threadIdx.x != 0) return;
+// (thread 0) record + publish the task the SWITCH body just ran
+__device__ void lane_complete(lane_state* L) {
   int kind = L->cur_kind;
   if (kind == LANE_NONE) return;
   const rrfp_lane_desc& d = L->d;
@@ -464,6 +467,17 @@ __global__ void lane_complete_kernel(lane_state* L) {
     L->n_w += 1;
   }
   L->cur_kind = LANE_NONE;
+}
+
+// One dispatcher step per loop iteration: complete the task the previous
+// iteration's SWITCH ran (end stamp, jitter pad, sends), then arbitrate the
+// next one and set the SWITCH branch (or end the WHILE).  One kernel node per
+// task instead of a dispatch and a completion kernel: ~1 device-side launch
+// less per decision (tools/dispatch_bench.py).
+__global__ void __launch_bounds__(32, 1) lane_step_kernel(lane_state* L) {
+  if (threadIdx.x == 0) lane_complete(L);
+  __syncwarp();
+  lane_dispatch(L);
 }
 
 // ================================================================ host side
@@ -699,7 +713,7 @@ static int add_kernel(cudaGraphNode_t* node, cudaGraph_t g, const cudaGraphNode_
 static int build_graph(rrfp_runtime* rt) {
   cudaGraph_t g;
   RRFP_CUDA_TRY(cudaGraphCreate(&g, 0));
-  cudaGraphNode_t n_init, n_while, n_final, n_dec, n_sw, n_comp;
+  cudaGraphNode_t n_init, n_while, n_final, n_dec, n_sw;
   int rc = add_kernel(&n_init, g, nullptr, 0, (void*)lane_init_kernel, rt->L);
   if (rc) return rc;
   cudaGraphConditionalHandle hw, hs;
@@ -711,7 +725,7 @@ static int build_graph(rrfp_runtime* rt) {
   cp.conditional.size = 1;
   RRFP_CUDA_TRY(cudaGraphAddNode(&n_while, g, &n_init, 1, &cp));
   cudaGraph_t loop = cp.conditional.phGraph_out[0];
-  if ((rc = add_kernel(&n_dec, loop, nullptr, 0, (void*)lane_dispatch_kernel, rt->L))) return rc;
+  if ((rc = add_kernel(&n_dec, loop, nullptr, 0, (void*)lane_step_kernel, rt->L))) return rc;
   RRFP_CUDA_TRY(cudaGraphConditionalHandleCreate(&hs, loop, 0xFFFFFFFFu, cudaGraphCondAssignDefault));
   cudaGraphNodeParams sp = {};
   sp.type = cudaGraphNodeTypeConditional;
@@ -732,7 +746,6 @@ static int build_graph(rrfp_runtime* rt) {
       if ((rc = add_kernel(&n, b, nullptr, 0, (void*)lane_spin_body_kernel, rt->L))) return rc;
     }
   }
-  if ((rc = add_kernel(&n_comp, loop, &n_sw, 1, (void*)lane_complete_kernel, rt->L))) return rc;
   if ((rc = add_kernel(&n_final, g, &n_while, 1, (void*)lane_final_kernel, rt->L))) return rc;
   // store the handles in the device lane state
   RRFP_CUDA_TRY(cudaMemcpy((char*)rt->L + offsetof(lane_state, h_while), &hw, sizeof(hw),

@@ -362,6 +362,45 @@ def wall_trace(workload: Workload, events, t0_ns: int, time_scale: float = 1.0):
     return Trace(events=final, clock="wall", time_scale=time_scale), met
 
 
+def dispatch_latency(trace, n_stages: int) -> dict:
+    """The device dispatcher's cost per decision, read off a wall trace (SURVEY
+    8d: "the dispatcher is latency-bound, report ns per decision").
+
+    For consecutive tasks of one (stage, rank) lane: if the second was already
+    ready when the first ended (its message had arrived, its F / B had run),
+    the gap between them is pure dispatch cost -- completion kernel, the WHILE
+    iteration, arbitration, the SWITCH into the next body; otherwise the
+    arrival -> start delay is the dispatcher's reaction time to a flag.
+    Returns p50 / p90 in microseconds and the sample counts."""
+    execs = [e for e in trace.events if e.event_kind == "exec"]
+    recv = {(e.stage, e.rank, e.microbatch, e.chunk, e.direction): e.t_start
+            for e in trace.events if e.event_kind == "recv"}
+    end = {(e.stage, e.rank, e.microbatch, e.chunk, e.direction): e.t_end for e in execs}
+    lanes = {}
+    for e in execs:
+        lanes.setdefault((e.stage, e.rank), []).append(e)
+    gaps, react = [], []
+    for (s, r), lst in lanes.items():
+        lst.sort(key=lambda e: e.t_start)
+        for a, b in zip(lst, lst[1:]):
+            key = lambda d: (s, r, b.microbatch, b.chunk, d)
+            if b.direction == "W":
+                ready = end.get(key("B"), 0)
+            elif b.direction == "B" and key("B") not in recv:   # last (virtual) stage: its own F
+                ready = end.get(key("F"), 0)
+            else:
+                ready = recv.get(key(b.direction), 0)           # (stage-0 F: always ready)
+            (gaps if ready <= a.t_end else react).append(
+                b.t_start - (a.t_end if ready <= a.t_end else ready))
+
+    def q(x):
+        if not x:
+            return None
+        x = sorted(x)
+        return {"p50": x[len(x) // 2], "p90": x[int(0.9 * (len(x) - 1))], "n": len(x)}
+    return {"back_to_back_gap_us": q(gaps), "arrival_to_start_us": q(react)}
+
+
 def run_gpu(workload: Workload, hint: HintOrder | str = "bf", buffer_limit: int = 32,
             time_scale: float = 1.0, *, seed: int = 0, jitter: JitterConfig | None = None,
             tp: TpGroup | None = None, watchdog_secs: float = 30.0, mode: str = "free",

@@ -43,3 +43,22 @@ def test_pipeline_model_on_host_twin():
             assert r["1f1b"]["ms"] > 0 and r["bf"]["speedup_vs_1f1b"] > 0.8
     # jitter makes every schedule slower
     assert out["pp8"]["sigma0.5"]["1f1b"]["ms"] > out["pp8"]["sigma0.0"]["1f1b"]["ms"]
+
+
+def test_dispatch_latency_from_trace():
+    """Back-to-back gaps count only when the next task was ready at the previous
+    one's end; otherwise the arrival -> start delay is reported."""
+    from paper_2605_18750_b200.runtime import dispatch_latency
+    from paper_2605_18750_b200.trace import Trace, TraceEvent
+    ev = [TraceEvent(0, 100, 0, None, 0, 0, "F", "exec"),
+          TraceEvent(120, 220, 0, None, 1, 0, "F", "exec"),      # stage-0 F: ready -> gap 20
+          TraceEvent(150, 150, 1, 0, 0, 0, "F", "recv"),
+          TraceEvent(100, 260, 1, 0, 0, 0, "F", "exec"),         # (first on its lane)
+          TraceEvent(300, 300, 1, 0, 1, 0, "F", "recv"),
+          TraceEvent(310, 400, 1, 0, 1, 0, "F", "exec"),         # arrived after the end: react 10
+          TraceEvent(425, 600, 1, 0, 0, 0, "B", "exec"),         # last stage B after its F: gap 25
+          TraceEvent(240, 300, 0, None, 0, 0, "F", "send")]
+    tr = Trace(events=ev) if "events" in Trace.__dataclass_fields__ else Trace(ev)
+    d = dispatch_latency(tr, 2)
+    assert d["back_to_back_gap_us"]["n"] == 2 and d["back_to_back_gap_us"]["p50"] == 25
+    assert d["arrival_to_start_us"] == {"p50": 10, "p90": 10, "n": 1}
