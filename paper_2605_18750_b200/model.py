@@ -465,6 +465,8 @@ class StageCompute:
         self.side = torch.cuda.Stream(dev)
         if decompose:   # gradients kept per (mb, layer) for the deferred W task
             self.gy, self.gpre = e(n_mb, nl, S, D), e(n_mb, nl, S, Fl)
+            # LayerNorm input gradients (the LN1 / LN2 parameter gradients move to W)
+            self.gln1, self.gln2 = e(n_mb, nl, S, D), e(n_mb, nl, S, D)
             self.gx0 = e(n_mb, S, D) if self.prologue else None
             if w_split == "all":
                 self.gx2, self.gqkv = e(n_mb, nl, S, D), e(n_mb, nl, S, 3 * Dl)
@@ -717,10 +719,12 @@ class StageCompute:
                     on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
                                                   a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
                                            _bias_grad(d_pre, g["b_1"])))
-                # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy)
-                self._dgrad_reduce(d_pre, p["w_1"], Fl, T)
-                _ln_bwd(d_head, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
-                        d_x2, g["ln2_g"], g["ln2_b"])
+                # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy);
+                # decomposed: the LN2 parameter gradients are W work (from the saved gln2)
+                ln_dy = self.gln2[mb, li, :T] if dec else d_head
+                self._dgrad_reduce(d_pre, p["w_1"], Fl, T, out=ln_dy)
+                _ln_bwd(ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
+                        d_x2, None if dec else g["ln2_g"], None if dec else g["ln2_b"])
                 if part == "mlp":
                     for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
                         _copy_rows(dst, d_x2, T, D)
@@ -745,7 +749,8 @@ class StageCompute:
                 done = torch.cuda.Event()
                 done.record(side)
                 side_done[li] = done
-            self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T)
+            ln_dy = self.gln1[mb, li, :T] if dec else d_head
+            self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T, out=ln_dy)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             if li > 0:
                 dx = dy_buf(li - 1)
@@ -753,8 +758,8 @@ class StageCompute:
                     main.wait_event(side_done[li + 1])
             else:
                 dx, extra = stage_dx()
-            _ln_bwd(d_head, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
-                    g["ln1_g"], g["ln1_b"])
+            _ln_bwd(ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
+                    None if dec else g["ln1_g"], None if dec else g["ln1_b"])
             for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
                 _copy_rows(dst, dx, T, D)
             dy = dx
@@ -788,16 +793,17 @@ class StageCompute:
             K._p(self.tokens[mb, t0:]), K._p(dx[t0:]), K._p(self.g_emb["wte"]),
             K._p(self.g_emb["wpe"][t0:]), S - t0, D, K._stream()))
 
-    def _dgrad_reduce(self, d_col, w, k, T=None):
-        """Input gradient of a column-parallel layer into self.d_head: d_col . W
-        (K = this rank's columns); under TP a partial sum all-reduced over the group."""
+    def _dgrad_reduce(self, d_col, w, k, T=None, out=None):
+        """Input gradient of a column-parallel layer into `out` (default self.d_head):
+        d_col . W (K = this rank's columns); under TP a partial sum all-reduced over the group."""
         S, D = self.cfg.seq, self.cfg.d_model
         T = S if T is None else T
+        out = self.d_head if out is None else out
         if self.R == 1:
-            K.gemm(d_col, w, self.d_head[:T], b_mn=True, m=T, n=D, k=k)
+            K.gemm(d_col, w, out[:T], b_mn=True, m=T, n=D, k=k)
         else:
             K.gemm(d_col, w, self.tp.partial, b_mn=True, m=S, n=D, k=k)
-            self.tp.allreduce([self.d_head])
+            self.tp.allreduce([out])
 
     def _attn_bwd(self, mb, li, d_o, d_qkv):
         cfg = self.cfg
@@ -828,8 +834,10 @@ class StageCompute:
 
     def backward_weight(self, mb: int):
         """W task (decomposed backward): the FC1/FC2 weight gradients (plus LM
-        head / projector / prologue) from the saved dy and d_pre; the attention
-        weight gradients were done in B (see backward_input).  Layers alternate
+        head / projector / prologue) from the saved dy and d_pre, and the LN1 /
+        LN2 parameter gradients from the saved LayerNorm input gradients (off the
+        B-input chain, where nothing overlapped them); the attention weight
+        gradients were done in B (see backward_input).  Layers alternate
         between the main and the side stream (independent GEMMs fill each
         other's tail waves); joined at the end."""
         if not self.decompose:
@@ -847,6 +855,14 @@ class StageCompute:
             gy, gpre = self.gy[mb, li, :T], self.gpre[mb, li, :T]
             part = self.parts[li]
             with torch.cuda.stream(side if li % 2 else main):
+                # LayerNorm parameter gradients (memory-bound: they overlap the other stream's GEMMs)
+                if part != "attn":
+                    x2 = self._layer_input(mb, li) if part == "mlp" else self.x2[mb, li, :T]
+                    _ln_bwd(self.gln2[mb, li, :T], x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None,
+                            None, None, g["ln2_g"], g["ln2_b"])
+                if part != "mlp":
+                    _ln_bwd(self.gln1[mb, li, :T], self._layer_input(mb, li), self.m1[mb, li, :T],
+                            self.r1[mb, li, :T], None, None, None, g["ln1_g"], g["ln1_b"])
                 if part != "attn":
                     K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
                            b_mn=True, accumulate=True, m=D, n=Fd, k=T)

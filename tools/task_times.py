@@ -29,7 +29,7 @@ def run(single_stream, label):
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-        res[k] = e0.elapsed_time(e1) / 10 * 1e3 / L
+        res[k] = e0.elapsed_time(e1) / 10 * 1e3 / len(st.layers)
     print(f"{label:28s} " + "  ".join(f"{k} {v:7.1f} us/layer" for k, v in res.items()), flush=True)
     del st
     torch.cuda.empty_cache()
