@@ -472,6 +472,9 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     return pipe, pipe.stages
 
 
+B_IN_FRAC, W_FRAC = 0.735, 0.312
+
+
 def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8), device="cuda"):
     """Virtual-clock prediction of the PP sweep from THIS run's B200 task times
     (SURVEY 6.3 / 8d C5): per-layer F and B durations of the measured run,
@@ -519,8 +522,10 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
                         bd = (b_l * lay[s_] + (b_h if s_ == n - 1 else 0)) * y
                         lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(fd))
                         if dec:
-                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(0.81 * bd))
-                            lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(0.29 * bd))
+                            # B-input / W as fractions of the fused B (captured bodies of
+                            # an interior stage, profiles/r01_task_times_ln_in_w.txt: 288 + 122 vs 392)
+                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(B_IN_FRAC * bd))
+                            lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(W_FRAC * bd))
                         else:
                             lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(bd))
                 comm = P.CommDelay()

@@ -667,10 +667,7 @@ class StageCompute:
             dy = dy_buf(nl - 1)
             K.gemm(dyp, pj["w_proj"], dy, b_mn=True, m=T, n=D, k=dyp.shape[1])
         else:
-            dy = self.bwd_in[mb][:T]
-            if dec and self.parts[-1] != "attn":   # (the W task reads it; an attention half: see below)
-                self.gy[mb, nl - 1, :T].copy_(dy)
-                dy = self.gy[mb, nl - 1, :T]
+            dy = self.bwd_in[mb][:T]   # (the W task reads it there too: a slot per microbatch)
         Dl, Fl = self.Dl, self.Fl
         d_head = self.d_head[:T]
         def stage_dx():
@@ -852,7 +849,10 @@ class StageCompute:
         side.wait_event(fork)
         for li in reversed(range(len(self.layers))):
             g = self.g[li]
-            gy, gpre = self.gy[mb, li, :T], self.gpre[mb, li, :T]
+            # the last layer's output gradient is the B mailbox slot itself (interior stages)
+            gy = (self.bwd_in[mb][:T] if li == len(self.layers) - 1 and self.epilogue is None
+                  else self.gy[mb, li, :T])
+            gpre = self.gpre[mb, li, :T]
             part = self.parts[li]
             with torch.cuda.stream(side if li % 2 else main):
                 # LayerNorm parameter gradients (memory-bound: they overlap the other stream's GEMMs)

@@ -372,13 +372,14 @@ def dispatch_latency(trace, n_stages: int) -> dict:
     iteration, arbitration, the SWITCH into the next body; otherwise the
     arrival -> start delay is the dispatcher's reaction time to a flag.
     Returns p50 / p90 in microseconds and the sample counts."""
+    rk = lambda e: 0 if e.rank is None else e.rank     # (TP=1 execs carry rank None, recvs 0)
     execs = [e for e in trace.events if e.event_kind == "exec"]
-    recv = {(e.stage, e.rank, e.microbatch, e.chunk, e.direction): e.t_start
+    recv = {(e.stage, rk(e), e.microbatch, e.chunk, e.direction): e.t_start
             for e in trace.events if e.event_kind == "recv"}
-    end = {(e.stage, e.rank, e.microbatch, e.chunk, e.direction): e.t_end for e in execs}
+    end = {(e.stage, rk(e), e.microbatch, e.chunk, e.direction): e.t_end for e in execs}
     lanes = {}
     for e in execs:
-        lanes.setdefault((e.stage, e.rank), []).append(e)
+        lanes.setdefault((e.stage, rk(e)), []).append(e)
     gaps, react = [], []
     for (s, r), lst in lanes.items():
         lst.sort(key=lambda e: e.t_start)

@@ -52,11 +52,11 @@ def test_dispatch_latency_from_trace():
     from paper_2605_18750_b200.trace import Trace, TraceEvent
     ev = [TraceEvent(0, 100, 0, None, 0, 0, "F", "exec"),
           TraceEvent(120, 220, 0, None, 1, 0, "F", "exec"),      # stage-0 F: ready -> gap 20
-          TraceEvent(150, 150, 1, 0, 0, 0, "F", "recv"),
-          TraceEvent(100, 260, 1, 0, 0, 0, "F", "exec"),         # (first on its lane)
+          TraceEvent(150, 150, 1, 0, 0, 0, "F", "recv"),         # (recvs carry rank 0, TP=1 execs None)
+          TraceEvent(100, 260, 1, None, 0, 0, "F", "exec"),      # (first on its lane)
           TraceEvent(300, 300, 1, 0, 1, 0, "F", "recv"),
-          TraceEvent(310, 400, 1, 0, 1, 0, "F", "exec"),         # arrived after the end: react 10
-          TraceEvent(425, 600, 1, 0, 0, 0, "B", "exec"),         # last stage B after its F: gap 25
+          TraceEvent(310, 400, 1, None, 1, 0, "F", "exec"),      # arrived after the end: react 10
+          TraceEvent(425, 600, 1, None, 0, 0, "B", "exec"),      # last stage B after its F: gap 25
           TraceEvent(240, 300, 0, None, 0, 0, "F", "send")]
     tr = Trace(events=ev) if "events" in Trace.__dataclass_fields__ else Trace(ev)
     d = dispatch_latency(tr, 2)
