@@ -98,6 +98,32 @@ def corpus():
                       "hint": hint, "ranked": ranked, "limit": rng.choice([1, 2, 4, 32]),
                       "jitter": rng.choice(["J0", "J1", "J3"]), "tp": tp,
                       "fixed": c == 1 and not dec})
+    # wide ready sets (more than 32 microbatches: multi-word bitmasks on the device),
+    # limits below M (backpressure), and the config-2/5 shape (PP=8, M=32, BFW)
+    logn = lambda mu, hi: {"kind": "lognormal", "mu": mu, "sigma": 0.4, "lo": 20, "hi": hi}
+    wide = [
+        ("wide-m40", {"num_stages": 4, "num_microbatches": 40, "forward": logn(5.0, 900),
+                      "backward": logn(5.3, 900)}, "bf", None, 32, "J1", None, True),
+        ("wide-m64-c2-bfw", {"num_stages": 4, "num_microbatches": 64, "num_chunks": 2,
+                             "decompose_backward": True, "forward": logn(5.0, 900),
+                             "backward": logn(5.3, 900),
+                             "comm_delay": {"kind": "uniform", "lo": 0, "hi": 40, "seed": 3}},
+         "bfw", None, 16, "J3", None, False),
+        ("pp8-m32-bfw", {"num_stages": 8, "num_microbatches": 32, "decompose_backward": True,
+                         "forward": logn(6.0, 2000), "backward": logn(6.6, 4000),
+                         "comm_delay": {"kind": "lognormal", "mu": 3.0, "sigma": 0.5, "lo": 0,
+                                        "hi": 200, "seed": 17}},
+         "bfw", None, 32, "J0", None, False),
+        ("wide-m100-tp2", {"num_stages": 2, "num_microbatches": 100, "tp_group_size": 2,
+                           "forward": logn(5.0, 900), "backward": logn(5.3, 900)},
+         "fb", None, 32, "J1", {"cost": 5, "skew_lo": 0, "skew_hi": 25}, True),
+        ("wide-m33-c3-external", {"num_stages": 3, "num_microbatches": 33, "num_chunks": 3,
+                                  "forward": logn(5.0, 900), "backward": logn(5.3, 900)},
+         "external", [["B", "asc"], ["F", "desc"]], 8, "J3", None, False),
+    ]
+    for name, spec, hint, ranked, limit, jit, tp, fixed in wide:
+        cases.append({"name": name, "spec": spec, "seed": 11, "hint": hint, "ranked": ranked,
+                      "limit": limit, "jitter": jit, "tp": tp, "fixed": fixed})
     return cases
 
 

@@ -155,3 +155,34 @@ def test_external_hint_replay_bit_exact():
     ev, _ = O.run_rrfp(_oracle_w(w), "external", 32, 11, "J0", ranked=(("B", "asc"), ("F", "asc")))
     want = [[(d, mb, c) for d, mb, c, _, _ in s] for s in O.exec_sequences(ev, 4)]
     assert _seqs(tr, 4) == want
+
+
+def _golden_wide():
+    from golden_util import engine_cases
+    return [c for c in engine_cases() if c["name"].startswith(("wide-", "pp8-")) and "deadlock" not in c]
+
+
+@pytest.mark.parametrize("case", _golden_wide(), ids=lambda c: c["name"])
+def test_wide_golden_cases_on_lanes(case):
+    """More than 32 microbatches (multi-word ready bitmasks), limits below M,
+    TP=2 with 100 microbatches, C=3 external hints: the device lanes replay the
+    reference's per-stage order exactly, and free-running they produce a valid
+    wall trace."""
+    w = P.generate_workload(P.GeneratorSpec.from_json(case["spec"]), case["seed"])
+    hint = (P.HintOrder("external", tuple(tuple(e) for e in case["ranked"]))
+            if case["hint"] == "external" else P.HintOrder(case["hint"]))
+    tp = None
+    if case["tp"]:
+        tp = P.TpGroup(group_size=w.tp_group_size, coordination_round_cost=case["tp"]["cost"],
+                       skew_lo=case["tp"]["skew_lo"], skew_hi=case["tp"]["skew_hi"])
+    jit = P.JITTER_PRESETS[case["jitter"]]
+    scale = min(1.0, 20000.0 / case["metrics"]["makespan"])    # ~20 ms of device time
+    tr, _ = run_gpu(w, hint, case["limit"], time_scale=scale, seed=case["seed"], jitter=jit, tp=tp,
+                    mode="replay")
+    want = [[(d, mb, c) for d, mb, c, _, _ in s] for s in case["exec"]["0"]]
+    assert _seqs(tr, w.num_stages, 0) == want
+    tr, m = run_gpu(w, hint, case["limit"], time_scale=scale, seed=case["seed"], jitter=jit, tp=tp)
+    assert m.total_tasks == w.task_count()
+    viol = [v for v in O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=scale)
+            if v[0] != "duration"]
+    assert not viol, viol[:5]
