@@ -275,6 +275,9 @@ int rrfp_gemm_reserve_sms(int n);
 int rrfp_gemm_set_epilogue(int tma_store);
 /* 1 = stream-K split of the last partial round of 256x256 tiles over all CTA pairs (default 0). */
 int rrfp_gemm_set_streamk(int on);
+/* 1 (default): the last partial wave of 256x256 output tiles runs as 256x128
+   halves when they fit in one round of CTA pairs; 0: plain waves. */
+int rrfp_gemm_set_tail_split(int on);
 /* pair-kernel k-block depth: 64 (6-stage ring, default) or 128 (3 stages). */
 int rrfp_gemm_set_bk(int bk);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */

@@ -74,12 +74,19 @@ struct GemmArgs {
   int sk_W;
   float4* ws;
   int* cnt;
+  // half-width tail (pair kernel, data-parallel schedule): after half_rounds full
+  // rounds of 256x256 tiles the last half_tail tiles (2*half_tail <= clusters) run
+  // as 256x128 halves, one round: the last wave takes half a tile time instead of
+  // a full one (256 tiles on 74 pairs: 3.5 tile times instead of 4).  -1: off.
+  int half_rounds;
+  int half_tail;
 };
 
 enum Role : int { ROLE_FULL = 0, ROLE_OWNER = 1, ROLE_PARTIAL = 2 };
 
 struct Unit {
   int tile, k0, k1, role;
+  int n0, bn;      // first output column of the unit and its width (256, or 128 for a half tile)
   int tail;        // tail-tile index (counter slot), owner / partial only
   int first;       // owner: first contributing cluster (partials in slots first .. cluster-1)
 };
@@ -97,14 +104,24 @@ __device__ __forceinline__ long long sk_start(const GemmArgs& g, int c, int C) {
 __device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int kblocks, int cid, int C,
                                          int i, bool direct, Unit& u) {
   if (!g.sk_W) {
+    if (g.half_rounds >= 0 && i >= g.half_rounds) {
+      const int h = cid + (i - g.half_rounds) * C;
+      if (i > g.half_rounds || h >= 2 * g.half_tail) return false;
+      const int t = g.half_rounds * C + (h >> 1);
+      u.tile = t; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+      u.n0 = (t / g.tiles_m) * 256 + (h & 1) * 128; u.bn = 128;
+      return true;
+    }
     const int t = cid + i * C;
     if (t >= num_tiles) return false;
     u.tile = t; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+    u.n0 = (t / g.tiles_m) * 256; u.bn = 256;
     return true;
   }
   const int n_dp = g.sk_full / C;
   if (i < n_dp) {
     u.tile = cid + i * C; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+    u.n0 = (u.tile / g.tiles_m) * 256; u.bn = 256;
     return true;
   }
   const int j = i - n_dp;
@@ -122,6 +139,7 @@ __device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int k
     return false;
   }
   u.tile = g.sk_full + t; u.k0 = k0; u.k1 = k1; u.tail = t; u.first = cid;
+  u.n0 = (u.tile / g.tiles_m) * 256; u.bn = 256;
   if (direct || (k0 == 0 && k1 == kblocks)) {
     u.role = ROLE_FULL;
   } else if (k1 == kblocks) {
@@ -553,6 +571,7 @@ template <int EPI, int A_MN, int B_MN, int PBK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_sm100_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                         const __grid_constant__ CUtensorMap tmBh,   // K-major B, 64-row box (half tiles)
                          GemmArgs g) {
   constexpr int NST = PairCfg<PBK>::STAGES;
   constexpr int P_A_BYTES = PairCfg<PBK>::A_BYTES, P_B_BYTES = PairCfg<PBK>::B_BYTES;
@@ -600,11 +619,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       Unit u;
       for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
-        const int mb = u.tile % g.tiles_m, nb = u.tile / g.tiles_m;
-        const int m0 = mb * P_BM + rank * 128, n0 = nb * P_BN + rank * 128;
+        const int mb = u.tile % g.tiles_m;
+        // (a half tile still loads 128-row B boxes; the MMA reads the first 64 rows of each)
+        const int m0 = mb * P_BM + rank * 128, n0 = u.n0 + rank * (u.bn >> 1);
+        const bool half = u.bn != P_BN;   // 64 rows of B per CTA (one 64-wide MN panel)
         for (int kb = u.k0; kb < u.k1; ++kb) {
           sm100::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2 * (P_A_BYTES + P_B_BYTES));
+          if (leader) sm100::mbar_arrive_expect_tx(&full[stage], 2 * (P_A_BYTES + (half ? P_B_BYTES / 2 : P_B_BYTES)));
           const uint32_t bar = lead_full0 + stage * 8;
           uint8_t* a_dst = sA + stage * P_A_BYTES;
           uint8_t* b_dst = sB + stage * P_B_BYTES;
@@ -618,11 +639,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           }
           if (!B_MN) {
 #pragma unroll
-            for (int h = 0; h < PBK / 64; ++h)
-              sm100::tma_load_2d_pair(b_dst + h * PANEL, &tmB, bar, kb * PBK + h * 64, n0);
+            for (int h = 0; h < PBK / 64; ++h)   // (a 64-row panel keeps the 128-row panel stride)
+              sm100::tma_load_2d_pair(b_dst + h * PANEL, half ? &tmBh : &tmB, bar, kb * PBK + h * 64, n0);
           } else {
             sm100::tma_load_2d_pair(b_dst, &tmB, bar, n0, kb * PBK);
-            sm100::tma_load_2d_pair(b_dst + 64 * PBK * 2, &tmB, bar, n0 + 64, kb * PBK);
+            if (!half) sm100::tma_load_2d_pair(b_dst + 64 * PBK * 2, &tmB, bar, n0 + 64, kb * PBK);
           }
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
@@ -630,7 +651,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16(P_BM, P_BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = sm100::idesc_bf16(P_BM, P_BN, A_MN, B_MN);
+      constexpr uint32_t idesc_half = sm100::idesc_bf16(P_BM, P_BN / 2, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -640,6 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * P_BN;
+        const uint32_t idesc = u.bn == P_BN ? idesc_full : idesc_half;
         for (int kb = u.k0; kb < u.k1; ++kb) {
           sm100::mbar_wait(&full[stage], phase);
           sm100::tc_fence_after();
@@ -671,11 +694,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     Unit u;
     for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
       const int tile = u.tile;
-      const int mb = tile % g.tiles_m, nb = tile / g.tiles_m;
+      const int mb = tile % g.tiles_m;
       const int row0 = mb * P_BM + rank * 128 + ew * 32;
       const int row = row0 + lane;
       int* cnt = g.cnt ? g.cnt + u.tail * 8 + rank * 4 + ew : nullptr;
-      if (u.role != ROLE_PARTIAL) epilogue_prefetch<EPI>(g, row, nb * P_BN, P_BN);
+      if (u.role != ROLE_PARTIAL) epilogue_prefetch<EPI>(g, row, u.n0, u.bn);
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * P_BN;
@@ -693,7 +716,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       if (u.role == ROLE_PARTIAL) {
         // raw fp32 partial -> this cluster's workspace slot (coalesced), then signal
 #pragma unroll 1
-        for (int c = 0; c < P_BN; c += 32) {
+        for (int c = 0; c < u.bn; c += 32) {
           uint32_t r[32];
           sm100::tmem_ld32(t_row + c, r);
           sm100::tmem_ld_wait();
@@ -708,7 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
       } else if (!g.tma_st) {
 #pragma unroll 1
-        for (int c = 0; c < P_BN; c += 32) {
+        for (int c = 0; c < u.bn; c += 32) {
           uint32_t r[32];
           sm100::tmem_ld32(t_row + c, r);
           sm100::tmem_ld_wait();
@@ -720,13 +743,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
           }
-          if (nb * P_BN + c < g.N) epilogue_chunk<EPI>(g, row, nb * P_BN + c, r);
+          if (u.n0 + c < g.N) epilogue_chunk<EPI>(g, row, u.n0 + c, r);
         }
       } else if (EPI == EPI_ACC_F32 || EPI == EPI_F32) {
         // 32 f32 columns per box: TMA reduce-add (weight-gradient accumulate) or store
 #pragma unroll 1
-        for (int c = 0; c < P_BN; c += 32) {
-          const int col = nb * P_BN + c;
+        for (int c = 0; c < u.bn; c += 32) {
+          const int col = u.n0 + c;
           if (col >= g.N) break;
           uint32_t r[32];
           sm100::tmem_ld32(t_row + c, r);
@@ -755,8 +778,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       } else {
         // 64 bf16 columns per box (two TMEM chunks); GELU also stages gelu(C) for C2
 #pragma unroll 1
-        for (int c = 0; c < P_BN; c += 64) {
-          const int col = nb * P_BN + c;
+        for (int c = 0; c < u.bn; c += 64) {
+          const int col = u.n0 + c;
           if (col >= g.N) break;
           uint32_t w[32];
           uint32_t w2[32];   // gelu(C) (EPI_BIAS_GELU only; dead otherwise)
@@ -904,6 +927,7 @@ std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_ws;
 // the 256x256 pair kernel is bound by L2->SM (TMA) throughput (~11 TB/s of operand
 // traffic at 1.8 GHz), not by wave quantization, so idle SMs in the last round cost
 // little and the fix-up traffic of the split costs more (-10% on one layer).
+int g_tail_split = 1;   // half-width last wave (rrfp_gemm_set_tail_split)
 int g_streamk = -1;
 
 bool use_streamk() {
@@ -938,6 +962,7 @@ SkWorkspace* sk_workspace(cudaStream_t st, int clusters) {
 
 template <int EPI, int A_MN, int B_MN, int PBK>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                const CUtensorMap& tbh,
                 GemmArgs g, cudaStream_t st) {
   auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK>;
   static bool attr = false;
@@ -952,9 +977,16 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   if (pairs < 1) pairs = 1;
   const int kblocks = (g.K + PBK - 1) / PBK;
   g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
+  g.half_rounds = -1; g.half_tail = 0;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
   const int tail = tiles % pairs;
-  if (use_streamk() && tail != 0 && (long long)tail * kblocks >= 2LL * pairs) {
+  if (g_tail_split && tail != 0 && 2 * tail <= pairs) {
+    // last partial wave as 256x128 halves: ceil(tiles / pairs) - 0.5 tile times
+    g.half_rounds = tiles / pairs;
+    g.half_tail = tail;
+    grid = 2 * (g.half_rounds > 0 ? pairs : 2 * tail);
+  }
+  if (g.half_rounds < 0 && use_streamk() && tail != 0 && (long long)tail * kblocks >= 2LL * pairs) {
     const bool direct = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
     SkWorkspace* w = direct ? nullptr : sk_workspace(st, pairs);
     if (direct || w) {
@@ -964,7 +996,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
       grid = 2 * pairs;
     }
   }
-  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, g));
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, g));
   return RRFP_OK;
 }
 
@@ -985,7 +1017,8 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
 }
 
 template <int EPI>
-int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh,
+                    const CUtensorMap& tc,
                     const CUtensorMap& tc2, const GemmArgs& g, cudaStream_t st) {
   if (!g_num_sms) {
     int dev;
@@ -994,15 +1027,15 @@ int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap
   }
   if (use_pair()) {
     if (pair_bk() == 128) {
-      if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 128>(ta, tb, tc, tc2, g, st);
-      if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 128>(ta, tb, tc, tc2, g, st);
-      if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 128>(ta, tb, tc, tc2, g, st);
-      return launch_pair<EPI, 1, 0, 128>(ta, tb, tc, tc2, g, st);
+      if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 128>(ta, tb, tc, tc2, tbh, g, st);
+      if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 128>(ta, tb, tc, tc2, tbh, g, st);
+      if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 128>(ta, tb, tc, tc2, tbh, g, st);
+      return launch_pair<EPI, 1, 0, 128>(ta, tb, tc, tc2, tbh, g, st);
     }
-    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 64>(ta, tb, tc, tc2, g, st);
-    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 64>(ta, tb, tc, tc2, g, st);
-    if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 64>(ta, tb, tc, tc2, g, st);
-    return launch_pair<EPI, 1, 0, 64>(ta, tb, tc, tc2, g, st);
+    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 64>(ta, tb, tc, tc2, tbh, g, st);
+    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 64>(ta, tb, tc, tc2, tbh, g, st);
+    if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 64>(ta, tb, tc, tc2, tbh, g, st);
+    return launch_pair<EPI, 1, 0, 64>(ta, tb, tc, tc2, tbh, g, st);
   }
   if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
   if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
@@ -1030,6 +1063,8 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   if (rc) return rc;
   rc = b_mn ? make_map(&tb, B, K, N, ldb, 64, mn_krows) : make_map(&tb, B, N, K, ldb, BK, brows);
   if (rc) return rc;
+  CUtensorMap tbh = tb;   // K-major B with a 64-row box: each CTA's half of a 256x128 tile
+  if (use_pair() && !b_mn && (rc = make_map(&tbh, B, N, K, ldb, BK, 64))) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
   g.tiles_m = (M + BM - 1) / BM;
@@ -1070,14 +1105,21 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   }
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
-    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
-    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
-    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
-    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
-    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
-    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tc, tc2, g, st);
+    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
   }
   return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
+}
+
+// 1 = run the last partial wave of 256x256 tiles as 256x128 halves when they fit
+// in one round (default), 0 = plain data-parallel waves
+extern "C" int rrfp_gemm_set_tail_split(int on) {
+  g_tail_split = on ? 1 : 0;
+  return RRFP_OK;
 }
 
 // 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel
