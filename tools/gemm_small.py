@@ -1,6 +1,6 @@
 """Interleaved A/B of the stage GEMMs (bench.py's roofline set): full last wave
 vs half-width tail (rrfp_gemm_set_tail_split), 6 alternating rounds of 30
-launches per variant, median per variant; cuBLAS on the small shapes (dev tool)."""
+launches per variant, median per variant (dev tool)."""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -42,8 +42,3 @@ for (fn, fl), nm in zip(calls, names):
 print(f"{'layer':18s} full wave {tot[0]:6.1f}us {ftot / tot[0] / 1e6:5.0f}TF/s   half tail {tot[1]:6.1f}us "
       f"{ftot / tot[1] / 1e6:5.0f}TF/s   {100 * (tot[0] / tot[1] - 1):+.1f}%")
 L.rrfp_gemm_set_tail_split(1)
-a = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
-b = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
-c = torch.empty(2048, 2048, device="cuda", dtype=torch.bfloat16)
-us = t(lambda: torch.mm(a, b.t(), out=c))
-print(f"cuBLAS 2048^3 bf16: {us:.1f}us {2 * 2048**3 / us / 1e6:.0f}TF/s")
