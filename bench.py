@@ -622,6 +622,11 @@ def emulated_pp(args, cfg):
             x = v.get(f"{name}@{args.compare_jitter}+sigma{sigma}")
             if base and x:
                 x["speedup_vs_1f1b"] = round(base["ms"] / x["ms"], 4)
+                if base.get("sm_mhz") and x.get("sm_mhz"):
+                    # the stages share one power-capped GPU here: the speed-up in SM cycles
+                    # (ms x median SM clock), what separate GPUs would see at equal clocks
+                    x["speedup_vs_1f1b_equal_clock"] = round(
+                        base["ms"] * base["sm_mhz"] / (x["ms"] * x["sm_mhz"]), 4)
     return out
 
 
