@@ -278,6 +278,12 @@ int rrfp_gemm_set_streamk(int on);
 /* 1 (default): the last partial wave of 256x256 output tiles runs as 256x128
    halves when they fit in one round of CTA pairs; 0: plain waves. */
 int rrfp_gemm_set_tail_split(int on);
+/* 1 (default): clusters of two CTA pairs on adjacent N tiles, A multicast
+   between them (N tile count even, no SM cap); 0: one CTA pair per cluster. */
+int rrfp_gemm_set_multicast(int on);
+/* Co-resident clusters of the pair GEMM kernel (mc = 1: CTA pairs, 2: two
+   pairs); the persistent grid is capped to it.  < 0: error. */
+int rrfp_gemm_max_clusters(int mc);
 /* pair-kernel k-block depth: 64 (6-stage ring, default) or 128 (3 stages). */
 int rrfp_gemm_set_bk(int bk);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */

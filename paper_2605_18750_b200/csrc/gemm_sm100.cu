@@ -101,8 +101,17 @@ __device__ __forceinline__ long long sk_start(const GemmArgs& g, int c, int C) {
 // is done FIRST, the owner segment of the first tile LAST, so a partial writer
 // never waits on anything and an owner waits only for segments other clusters
 // run first.
+template <int MC>
 __device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int kblocks, int cid, int C,
-                                         int i, bool direct, Unit& u) {
+                                         int i, bool direct, Unit& u, int pairi) {
+  if (MC == 2) {   // double tiles: (mb, 2*nb2 + pair); tiles_n even (host)
+    const int t2 = cid + i * C;
+    if (t2 >= num_tiles / 2) return false;
+    const int mb = t2 % g.tiles_m, nb = 2 * (t2 / g.tiles_m) + pairi;
+    u.tile = mb + nb * g.tiles_m; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
+    u.n0 = nb * 256; u.bn = 256;
+    return true;
+  }
   if (!g.sk_W) {
     if (g.half_rounds >= 0 && i >= g.half_rounds) {
       const int h = cid + (i - g.half_rounds) * C;
@@ -567,11 +576,17 @@ constexpr int P_EPI_BYTES = 4 * 2 * 4096;     // per epilogue warp: two 32-row x
 constexpr int P_SMEM_BYTES = P_RING_BYTES + P_EPI_BYTES + 1024 + 256;
 constexpr int P_TMEM_COLS = 2 * P_BN;
 
-template <int EPI, int A_MN, int B_MN, int PBK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+// MC = 2: a cluster of two CTA pairs on adjacent N tiles of the same M rows;
+// each A k-block is loaded once per cluster (each pair loads one 64-row half and
+// multicasts it to the same-rank CTA of the other pair), halving A's L2->SM
+// traffic.  Both pairs walk the same unit list (double tiles) in lock step; a
+// stage is free once BOTH pairs' MMAs consumed it (empty barriers count 2).
+template <int EPI, int A_MN, int B_MN, int PBK, int MC>
+__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_sm100_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                          const __grid_constant__ CUtensorMap tmBh,   // K-major B, 64-row box (half tiles)
+                         const __grid_constant__ CUtensorMap tmAh,   // K-major A, 64-row box (MC = 2)
                          GemmArgs g) {
   constexpr int NST = PairCfg<PBK>::STAGES;
   constexpr int P_A_BYTES = PairCfg<PBK>::A_BYTES, P_B_BYTES = PairCfg<PBK>::B_BYTES;
@@ -589,12 +604,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P_STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = sm100::cluster_ctarank();
+  const uint32_t crank = sm100::cluster_ctarank();
+  const uint32_t rank = crank & 1;              // rank inside the CTA pair
+  const uint32_t pairi = crank >> 1;            // which pair of the cluster (MC = 2)
+  const uint32_t lead = crank & ~1u;            // this pair's leader CTA
   const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
-    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], MC); }
     for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
     sm100::fence_barrier_init();
   }
@@ -608,17 +626,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
   const int num_tiles = g.tiles_m * g.tiles_n;
   const int kblocks = (g.K + PBK - 1) / PBK;
-  const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  const int cluster_id = blockIdx.x / (2 * MC), num_clusters = gridDim.x / (2 * MC);
   // f32 accumulate: every split segment reduce-adds into C by itself (no fix-up)
   const bool direct = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t lead_full0 = sm100::mapa_shared(sm100::smem_u32(&full[0]), 0);
+      const uint32_t lead_full0 = sm100::mapa_shared(sm100::smem_u32(&full[0]), lead);
+      const uint16_t mask_a = (uint16_t)((1u << rank) | (1u << (rank + 2)));   // same-rank CTAs (MC = 2)
       int stage = 0;
       uint32_t phase = 0;
       Unit u;
-      for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
+      for (int ui = 0; get_unit<MC>(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u, pairi); ++ui) {
         const int mb = u.tile % g.tiles_m;
         // (a half tile still loads 128-row B boxes; the MMA reads the first 64 rows of each)
         const int m0 = mb * P_BM + rank * 128, n0 = u.n0 + rank * (u.bn >> 1);
@@ -629,7 +648,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint32_t bar = lead_full0 + stage * 8;
           uint8_t* a_dst = sA + stage * P_A_BYTES;
           uint8_t* b_dst = sB + stage * P_B_BYTES;
-          if (!A_MN) {
+          if (MC == 2) {   // this CTA's 64-row (K-major) / 64-col (MN-major) half of A, to both pairs
+            if (!A_MN) {
+#pragma unroll
+              for (int h = 0; h < PBK / 64; ++h)
+                sm100::tma_load_2d_pair_mc(a_dst + h * PANEL + pairi * 64 * 128, &tmAh, bar, kb * PBK + h * 64,
+                                           m0 + pairi * 64, mask_a);
+            } else {
+              sm100::tma_load_2d_pair_mc(a_dst + pairi * 64 * PBK * 2, &tmA, bar, m0 + pairi * 64, kb * PBK,
+                                         mask_a);
+            }
+          } else if (!A_MN) {
 #pragma unroll
             for (int h = 0; h < PBK / 64; ++h)
               sm100::tma_load_2d_pair(a_dst + h * PANEL, &tmA, bar, kb * PBK + h * 64, m0);
@@ -658,7 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       Unit u;
-      for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
+      for (int ui = 0; get_unit<MC>(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u, pairi); ++ui) {
         sm100::mbar_wait(&tempty[acc], acc_phase ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * P_BN;
@@ -677,22 +706,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                                : sm100::umma_desc_sw128(b_base + kp, 16, 1024);
             sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != u.k0) || (k != 0));
           }
-          sm100::mma_commit_pair(&empty[stage], 0x3);
+          sm100::mma_commit_pair(&empty[stage], MC == 2 ? 0xF : 0x3);   // (MC = 2: both pairs' producers)
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        sm100::mma_commit_pair(&tfull[acc], 0x3);
+        sm100::mma_commit_pair(&tfull[acc], (uint16_t)(0x3u << lead));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const uint32_t lead_tempty0 = sm100::mapa_shared(sm100::smem_u32(&tempty[0]), 0);
+    const uint32_t lead_tempty0 = sm100::mapa_shared(sm100::smem_u32(&tempty[0]), lead);
     uint8_t* wbuf = sEpi + ew * 8192;     // this warp's two staging boxes
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t unit = 0;                    // staging-box round robin
     Unit u;
-    for (int ui = 0; get_unit(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u); ++ui) {
+    for (int ui = 0; get_unit<MC>(g, num_tiles, kblocks, cluster_id, num_clusters, ui, direct, u, pairi); ++ui) {
       const int tile = u.tile;
       const int mb = tile % g.tiles_m;
       const int row0 = mb * P_BM + rank * 128 + ew * 32;
@@ -928,6 +957,7 @@ std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_ws;
 // traffic at 1.8 GHz), not by wave quantization, so idle SMs in the last round cost
 // little and the fix-up traffic of the split costs more (-10% on one layer).
 int g_tail_split = 1;   // half-width last wave (rrfp_gemm_set_tail_split)
+int g_mc = 1;           // 2-pair clusters with A multicast (rrfp_gemm_set_multicast)
 int g_streamk = -1;
 
 bool use_streamk() {
@@ -960,20 +990,70 @@ SkWorkspace* sk_workspace(cudaStream_t st, int clusters) {
   return &(g_ws[key] = w);
 }
 
+// co-resident clusters of `kern` (cluster of `csize` CTAs, 1 CTA per SM): a
+// persistent grid larger than this would run its surplus clusters as a second
+// wave.  Clusters are packed per GPC, so this can be below num_SMs / csize.
+template <typename K>
+int max_clusters(K kern, int csize) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize * 1024);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = P_SMEM_BYTES;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 template <int EPI, int A_MN, int B_MN, int PBK>
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
-                const CUtensorMap& tbh,
-                GemmArgs g, cudaStream_t st) {
-  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK>;
+int launch_pair_mc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                   const CUtensorMap& tbh, const CUtensorMap& tah, GemmArgs g, cudaStream_t st) {
+  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK, 2>;
   static bool attr = false;
   if (!attr) {
     RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES));
     attr = true;
   }
+  const int tiles = g.tiles_m * g.tiles_n;   // (tiles_n even: checked by the caller)
+  static int resident = max_clusters(kern, 4);
+  int clusters = (g_num_sms - g_reserve_sms) / 4;
+  if (resident > 0 && clusters > resident) clusters = resident;
+  if (clusters < 1) clusters = 1;
+  g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
+  g.half_rounds = -1; g.half_tail = 0;
+  const int grid = 4 * (tiles / 2 < clusters ? tiles / 2 : clusters);
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, tah, g));
+  return RRFP_OK;
+}
+
+template <int EPI, int A_MN, int B_MN, int PBK>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tc2,
+                const CUtensorMap& tbh, const CUtensorMap& tah,
+                GemmArgs g, cudaStream_t st) {
   g.tiles_m = (g.M + P_BM - 1) / P_BM;
   g.tiles_n = (g.N + P_BN - 1) / P_BN;
+  // (not under an SM cap: a capped grid shares the GPU, possibly inside a green-context
+  // partition, where 4-CTA clusters may not be placeable)
+  if (PBK == 64 && g_mc && g_reserve_sms == 0 && g.tiles_n % 2 == 0)
+    return launch_pair_mc<EPI, A_MN, B_MN, PBK>(ta, tb, tc, tc2, tbh, tah, g, st);
+  auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK, 1>;
+  static bool attr = false;
+  if (!attr) {
+    RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES));
+    attr = true;
+  }
+  g.tiles_n = (g.N + P_BN - 1) / P_BN;
   int tiles = g.tiles_m * g.tiles_n;
+  static int resident = max_clusters(kern, 2);
   int pairs = (g_num_sms - g_reserve_sms) / 2;
+  if (resident > 0 && pairs > resident) pairs = resident;
   if (pairs < 1) pairs = 1;
   const int kblocks = (g.K + PBK - 1) / PBK;
   g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
@@ -996,7 +1076,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
       grid = 2 * pairs;
     }
   }
-  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, g));
+  RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, tah, g));
   return RRFP_OK;
 }
 
@@ -1018,7 +1098,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cuda
 
 template <int EPI>
 int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh,
-                    const CUtensorMap& tc,
+                    const CUtensorMap& tah, const CUtensorMap& tc,
                     const CUtensorMap& tc2, const GemmArgs& g, cudaStream_t st) {
   if (!g_num_sms) {
     int dev;
@@ -1027,15 +1107,15 @@ int dispatch_majors(int a_mn, int b_mn, const CUtensorMap& ta, const CUtensorMap
   }
   if (use_pair()) {
     if (pair_bk() == 128) {
-      if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 128>(ta, tb, tc, tc2, tbh, g, st);
-      if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 128>(ta, tb, tc, tc2, tbh, g, st);
-      if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 128>(ta, tb, tc, tc2, tbh, g, st);
-      return launch_pair<EPI, 1, 0, 128>(ta, tb, tc, tc2, tbh, g, st);
+      if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 128>(ta, tb, tc, tc2, tbh, tah, g, st);
+      if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 128>(ta, tb, tc, tc2, tbh, tah, g, st);
+      if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 128>(ta, tb, tc, tc2, tbh, tah, g, st);
+      return launch_pair<EPI, 1, 0, 128>(ta, tb, tc, tc2, tbh, tah, g, st);
     }
-    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 64>(ta, tb, tc, tc2, tbh, g, st);
-    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 64>(ta, tb, tc, tc2, tbh, g, st);
-    if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 64>(ta, tb, tc, tc2, tbh, g, st);
-    return launch_pair<EPI, 1, 0, 64>(ta, tb, tc, tc2, tbh, g, st);
+    if (!a_mn && !b_mn) return launch_pair<EPI, 0, 0, 64>(ta, tb, tc, tc2, tbh, tah, g, st);
+    if (!a_mn && b_mn) return launch_pair<EPI, 0, 1, 64>(ta, tb, tc, tc2, tbh, tah, g, st);
+    if (a_mn && b_mn) return launch_pair<EPI, 1, 1, 64>(ta, tb, tc, tc2, tbh, tah, g, st);
+    return launch_pair<EPI, 1, 0, 64>(ta, tb, tc, tc2, tbh, tah, g, st);
   }
   if (!a_mn && !b_mn) return launch<EPI, 0, 0>(ta, tb, g, st);
   if (!a_mn && b_mn) return launch<EPI, 0, 1>(ta, tb, g, st);
@@ -1065,6 +1145,8 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   if (rc) return rc;
   CUtensorMap tbh = tb;   // K-major B with a 64-row box: each CTA's half of a 256x128 tile
   if (use_pair() && !b_mn && (rc = make_map(&tbh, B, N, K, ldb, BK, 64))) return rc;
+  CUtensorMap tah = ta;   // K-major A with a 64-row box: one pair's half of a multicast A slice
+  if (use_pair() && g_mc && !a_mn && (rc = make_map(&tah, A, M, K, lda, BK, 64))) return rc;
   GemmArgs g;
   g.M = M; g.N = N; g.K = K;
   g.tiles_m = (M + BM - 1) / BM;
@@ -1105,12 +1187,12 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   }
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
-    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
-    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
-    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
-    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
-    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
-    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tbh, tc, tc2, g, st);
+    case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_BIAS_GELU: return dispatch_majors<EPI_BIAS_GELU>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_RESID: return dispatch_majors<EPI_RESID>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
   }
   return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
 }
@@ -1120,6 +1202,26 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
 extern "C" int rrfp_gemm_set_tail_split(int on) {
   g_tail_split = on ? 1 : 0;
   return RRFP_OK;
+}
+
+// 1 (default) = clusters of two CTA pairs on adjacent N tiles sharing A through
+// TMA multicast (N tile count even, no SM cap), 0 = one pair per cluster.
+// Measured (profiles/r01_gemm_multicast_ab.txt): one layer's ten GEMMs 518 us vs
+// 534 us with pairs (half-width tail) under sustained clocks; only 33 two-pair
+// clusters are co-resident (GPC packing), the grid is capped to that.
+extern "C" int rrfp_gemm_set_multicast(int on) {
+  g_mc = on ? 1 : 0;
+  return RRFP_OK;
+}
+
+// co-resident clusters of the pair kernel: mc = 1 (CTA pairs) or 2 (two pairs)
+extern "C" int rrfp_gemm_max_clusters(int mc) {
+  auto k1 = gemm_bf16_sm100_pair<EPI_BF16, 0, 0, 64, 1>;
+  auto k2 = gemm_bf16_sm100_pair<EPI_BF16, 0, 0, 64, 2>;
+  for (auto k : {(const void*)k1, (const void*)k2})
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES) != cudaSuccess)
+      return rrfp_fail(RRFP_E_CUDA, "cudaFuncSetAttribute failed");
+  return mc == 2 ? max_clusters(k2, 4) : max_clusters(k1, 2);
 }
 
 // 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel

@@ -5,19 +5,26 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 1, 64), (1, 1, 128), (1, 2, 64), (1, 0, 64), (0, 0, 64)],
-                ids=["pair-tma-store", "pair-bk128", "pair-staged-coalesced", "pair-st-global", "single"],
+@pytest.fixture(params=[(1, 1, 64, 0, 1), (1, 1, 128, 0, 1), (1, 2, 64, 0, 1), (1, 0, 64, 0, 1), (0, 0, 64, 0, 1),
+                        (1, 1, 64, 1, 1), (1, 2, 64, 1, 1), (1, 1, 64, 0, 0)],   # (pair, epilogue, bk, multicast, tail)
+                ids=["pair-tma-store", "pair-bk128", "pair-staged-coalesced", "pair-st-global", "single",
+                     "pair-multicast", "pair-multicast-coalesced", "pair-full-last-wave"],
                 autouse=True)
 def variant(request):
     from paper_2605_18750_b200 import _lib
-    pair, tma, bk = request.param
-    _lib.lib().rrfp_gemm_set_variant(pair)
-    _lib.lib().rrfp_gemm_set_epilogue(tma)
-    _lib.lib().rrfp_gemm_set_bk(bk)
+    pair, tma, bk, mc, tail = request.param
+    L = _lib.lib()
+    L.rrfp_gemm_set_variant(pair)
+    L.rrfp_gemm_set_epilogue(tma)
+    L.rrfp_gemm_set_bk(bk)
+    L.rrfp_gemm_set_multicast(mc)
+    L.rrfp_gemm_set_tail_split(tail)
     yield request.param
-    _lib.lib().rrfp_gemm_set_variant(1)
-    _lib.lib().rrfp_gemm_set_epilogue(1)
-    _lib.lib().rrfp_gemm_set_bk(64)
+    L.rrfp_gemm_set_variant(1)
+    L.rrfp_gemm_set_epilogue(1)
+    L.rrfp_gemm_set_bk(64)
+    L.rrfp_gemm_set_multicast(1)
+    L.rrfp_gemm_set_tail_split(1)
 
 
 def _rand(*shape, scale=1.0):

@@ -1,6 +1,7 @@
-"""Interleaved A/B of the stage GEMMs (bench.py's roofline set): full last wave
-vs half-width tail (rrfp_gemm_set_tail_split), 6 alternating rounds of 30
-launches per variant, median per variant (dev tool)."""
+"""Interleaved A/B/C of the stage GEMMs (bench.py's roofline set): full last
+wave, half-width tail (rrfp_gemm_set_tail_split), two-pair clusters with A
+multicast (rrfp_gemm_set_multicast); 6 alternating rounds of 30 launches per
+variant, median per variant (dev tool)."""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -23,22 +24,35 @@ def t(fn, reps=30):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-for fn, _ in calls:          # warm every shape / variant first
-    for ts in (0, 1):
-        L.rrfp_gemm_set_tail_split(ts)
-        t(fn, 10)
-tot = {0: 0.0, 1: 0.0}
+VARS = [("full wave", 0, 0), ("half tail", 1, 0), ("multicast", 1, 1)]
+print(f"co-resident clusters: pairs {L.rrfp_gemm_max_clusters(1)}, two-pair clusters {L.rrfp_gemm_max_clusters(2)}",
+      flush=True)
+
+
+def setv(ts, mc):
+    L.rrfp_gemm_set_tail_split(ts)
+    L.rrfp_gemm_set_multicast(mc)
+
+
+for _ in range(3):           # warm every shape / variant first (clocks settle under load)
+    for fn, _ in calls:
+        for _, ts, mc in VARS:
+            setv(ts, mc)
+            t(fn, 30)
+tot = {v[0]: 0.0 for v in VARS}
 ftot = 0.0
 for (fn, fl), nm in zip(calls, names):
-    res = {0: [], 1: []}
-    for _ in range(6):
-        for ts in (0, 1):
-            L.rrfp_gemm_set_tail_split(ts)
-            res[ts].append(t(fn))
-    m = {ts: statistics.median(v) for ts, v in res.items()}
-    tot[0] += m[0]; tot[1] += m[1]; ftot += fl
-    print(f"{nm:18s} full wave {m[0]:6.1f}us {fl / m[0] / 1e6:5.0f}TF/s   half tail {m[1]:6.1f}us "
-          f"{fl / m[1] / 1e6:5.0f}TF/s   {100 * (m[0] / m[1] - 1):+.1f}%", flush=True)
-print(f"{'layer':18s} full wave {tot[0]:6.1f}us {ftot / tot[0] / 1e6:5.0f}TF/s   half tail {tot[1]:6.1f}us "
-      f"{ftot / tot[1] / 1e6:5.0f}TF/s   {100 * (tot[0] / tot[1] - 1):+.1f}%")
-L.rrfp_gemm_set_tail_split(1)
+    res = {v[0]: [] for v in VARS}
+    for _ in range(10):
+        for name, ts, mc in VARS:
+            setv(ts, mc)
+            res[name].append(t(fn))
+    ftot += fl
+    line = f"{nm:18s}"
+    for name, _, _ in VARS:
+        m = statistics.median(res[name])
+        tot[name] += m
+        line += f"  {name} {m:6.1f}us {fl / m / 1e6:5.0f}TF/s"
+    print(line, flush=True)
+print(f"{'layer':18s}" + "".join(f"  {n} {tot[n]:6.1f}us {ftot / tot[n] / 1e6:5.0f}TF/s" for n, _, _ in VARS))
+setv(1, 0)
