@@ -104,9 +104,10 @@ __device__ __forceinline__ long long sk_start(const GemmArgs& g, int c, int C) {
 template <int MC>
 __device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int kblocks, int cid, int C,
                                          int i, bool direct, Unit& u, int pairi) {
-  if (MC == 2) {   // double tiles: (mb, 2*nb2 + pair); tiles_n even (host)
+  if (MC == 2) {   // double tiles: (mb, 2*nb2 + pair); odd tiles_n: the last pair's
+                   // tile lies past N (zero-filled loads, no stores)
     const int t2 = cid + i * C;
-    if (t2 >= num_tiles / 2) return false;
+    if (t2 >= g.tiles_m * ((g.tiles_n + 1) >> 1)) return false;
     const int mb = t2 % g.tiles_m, nb = 2 * (t2 / g.tiles_m) + pairi;
     u.tile = mb + nb * g.tiles_m; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
     u.n0 = nb * 256; u.bn = 256;
@@ -1021,14 +1022,14 @@ int launch_pair_mc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     RRFP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES));
     attr = true;
   }
-  const int tiles = g.tiles_m * g.tiles_n;   // (tiles_n even: checked by the caller)
+  const int dtiles = g.tiles_m * ((g.tiles_n + 1) / 2);
   static int resident = max_clusters(kern, 4);
   int clusters = (g_num_sms - g_reserve_sms) / 4;
   if (resident > 0 && clusters > resident) clusters = resident;
   if (clusters < 1) clusters = 1;
   g.sk_full = 0; g.sk_W = 0; g.ws = nullptr; g.cnt = nullptr;
   g.half_rounds = -1; g.half_tail = 0;
-  const int grid = 4 * (tiles / 2 < clusters ? tiles / 2 : clusters);
+  const int grid = 4 * (dtiles < clusters ? dtiles : clusters);
   RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, tah, g));
   return RRFP_OK;
 }
@@ -1041,7 +1042,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   g.tiles_n = (g.N + P_BN - 1) / P_BN;
   // (not under an SM cap: a capped grid shares the GPU, possibly inside a green-context
   // partition, where 4-CTA clusters may not be placeable)
-  if (PBK == 64 && g_mc && g_reserve_sms == 0 && g.tiles_n % 2 == 0)
+  if (PBK == 64 && g_mc && g_reserve_sms == 0 && g.tiles_n > 1)
     return launch_pair_mc<EPI, A_MN, B_MN, PBK>(ta, tb, tc, tc2, tbh, tah, g, st);
   auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK, 1>;
   static bool attr = false;
