@@ -221,10 +221,17 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
   for (int c = lane * 8; c < D; c += 256) {
     float a[8];
     load8(dx + (size_t)row * D + c, a);
+    // token rows collide across positions: vector reductions (2 x 16 B per 8 columns);
+    // position rows are this thread's alone: plain 16-byte read-modify-write
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      atomicAdd(e + c + j, a[j]);
-      p[c + j] += a[j];
+    for (int h = 0; h < 2; ++h) {
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(e + c + 4 * h), "f"(a[4 * h]),
+                   "f"(a[4 * h + 1]), "f"(a[4 * h + 2]), "f"(a[4 * h + 3])
+                   : "memory");
+      float4* q = reinterpret_cast<float4*>(p + c + 4 * h);
+      float4 v = *q;
+      v.x += a[4 * h]; v.y += a[4 * h + 1]; v.z += a[4 * h + 2]; v.w += a[4 * h + 3];
+      *q = v;
     }
   }
 }

@@ -95,3 +95,26 @@ def test_bias_grad_colsum(rows, cols):
     assert _L().rrfp_bias_grad(_p(dy), C.c_longlong(cols), _p(db), rows, cols, _st()) == 0
     torch.cuda.synchronize()
     torch.testing.assert_close(db, 1 + dy.float().sum(0), rtol=1e-3, atol=1e-2)
+
+
+@pytest.mark.parametrize("rows,D,V", [(256, 2048, 64), (100, 1280, 7), (2048, 2048, 50304)])
+def test_embedding_fwd_bwd(rows, D, V):
+    """x = E[tok] + P[pos]; backward scatter-adds into E (tokens repeat: V small
+    forces collisions) and adds into P, on top of existing gradient values."""
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    tok = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32, generator=g)
+    E = torch.randn(V, D, device="cuda", generator=g).bfloat16()
+    P = torch.randn(rows, D, device="cuda", generator=g).bfloat16()
+    x = torch.empty(rows, D, device="cuda", dtype=torch.bfloat16)
+    L = _L()
+    assert L.rrfp_embedding_fwd(_p(tok), _p(E), _p(P), _p(x), rows, D, _st()) == 0
+    dx = torch.randn(rows, D, device="cuda", generator=g).bfloat16()
+    dE = torch.randn(V, D, device="cuda", generator=g)
+    dP = torch.randn(rows, D, device="cuda", generator=g)
+    wantE = dE.clone().index_add_(0, tok.long(), dx.float())
+    wantP = dP + dx.float()
+    assert L.rrfp_embedding_bwd(_p(tok), _p(dx), _p(dE), _p(dP), rows, D, _st()) == 0
+    torch.cuda.synchronize()
+    _close(x, E.float()[tok.long()] + P.float())
+    torch.testing.assert_close(dE, wantE, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(dP, wantP, rtol=1e-6, atol=1e-6)
