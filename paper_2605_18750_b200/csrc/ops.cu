@@ -440,7 +440,7 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
     RRFP_CUDA_TRY(cudaGetLastError());
   }
   if (dg || db) {
-    const int rpb = 32;   // 2 rows per warp (unrolled): enough CTAs in flight per SM
+    const int rpb = 32;   // 2 rows per warp (unrolled): enough CTAs in flight per SM (64 / 128: slower)
     dim3 g2((D + 255) / 256, (rows + rpb - 1) / rpb);
     RRFP_CUDA_TRY(rrfp_launch(ln_param_grad_kernel, g2, dim3(256), 0, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean,
                                              rstd, dg, db, rows, D, rpb));
