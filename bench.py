@@ -472,7 +472,7 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
     return pipe, pipe.stages
 
 
-B_IN_FRAC, W_FRAC = 0.735, 0.312
+B_IN_FRAC, W_FRAC = 0.714, 0.307
 
 
 def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8), device="cuda"):
@@ -523,7 +523,7 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
                         lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(fd))
                         if dec:
                             # B-input / W as fractions of the fused B (captured bodies of
-                            # an interior stage, profiles/r01_task_times_ln_in_w.txt: 288 + 122 vs 392)
+                            # an interior stage, profiles/r01_task_times_ln_in_w.txt: 274 + 118 vs 384)
                             lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(B_IN_FRAC * bd))
                             lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(W_FRAC * bd))
                         else:
