@@ -273,12 +273,13 @@ def gemm_roofline(cfg, peak_tf):
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tf, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tf, 3), "traffic": traffic,
             "traffic_unit": "bytes/launch (dram rd+wr, ncu --set full, profiles/gemm_traffic.json)",
-            "kernel": "gemm_bf16_sm100_pair (cta_group::2 tcgen05.mma 256x256x16, TMA 6-stage ring, "
-                      "TMEM x2, TMA-store epilogue)",
+            "kernel": "gemm_bf16_sm100_pair (cta_group::2 tcgen05.mma 256x256x16; clusters of two CTA pairs "
+                      "sharing A by TMA multicast; half-width last wave; TMA 6-stage ring, TMEM x2, "
+                      "TMA-store / reduce-add epilogue)",
             "per_launch": f"mean over one layer's 10 F/B/W GEMMs ({cfg.seq} tokens, d={cfg.d_model}, "
                           f"ffn={cfg.d_ff}); CUDA events on the launch stream, 10 reps, in this process "
                           "after the timed region",
-            "share_of_step": "73.1% of device time (profiles/r01_bench_launches_summary_final.txt, ncu launch list)",
+            "share_of_step": "74.5% of device time (profiles/r01_bench_launches_summary_r1end.txt, ncu launch list)",
             "avg_launch_us": round(ms * 1e3, 1)}
 
 
