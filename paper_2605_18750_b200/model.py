@@ -460,6 +460,10 @@ class StageCompute:
         self.sd_b = [e(S, D), e(S, D)]
         self.sd_big = [e(S, Fl), e(S, Fl)]
         self.sd_qkv = [e(S, 3 * Dl), e(S, 3 * Dl)]
+        # LayerNorm input gradients, kept (two parity sets) until the side stream's
+        # parameter-gradient kernels read them (fused backward; decomposed: gln1/gln2)
+        if not decompose:
+            self.sd_ln1, self.sd_ln2 = [e(S, D), e(S, D)], [e(S, D), e(S, D)]
         self.d_head = e(S, D)
         self.d_o = e(S, Dl) if tp_size > 1 else None   # attention-output gradient (this rank's heads)
         self.side = torch.cuda.Stream(dev)
@@ -716,12 +720,16 @@ class StageCompute:
                     on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
                                                   a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
                                            _bias_grad(d_pre, g["b_1"])))
-                # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy);
-                # decomposed: the LN2 parameter gradients are W work (from the saved gln2)
-                ln_dy = self.gln2[mb, li, :T] if dec else d_head
+                # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy).
+                # The LN2 parameter gradients leave the input-gradient chain: side stream
+                # (fused), W task (decomposed, from the saved gln2)
+                ln_dy = (self.gln2[mb, li] if dec else self.sd_ln2[q])[:T]
                 self._dgrad_reduce(d_pre, p["w_1"], Fl, T, out=ln_dy)
-                _ln_bwd(ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy,
-                        d_x2, None if dec else g["ln2_g"], None if dec else g["ln2_b"])
+                _ln_bwd(ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy, d_x2, None, None)
+                if not dec:
+                    on_side(ev(), lambda ln_dy=ln_dy, x2=x2, g=g, li=li: _ln_bwd(
+                        ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None, None, None,
+                        g["ln2_g"], g["ln2_b"]))
                 if part == "mlp":
                     for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
                         _copy_rows(dst, d_x2, T, D)
@@ -743,10 +751,7 @@ class StageCompute:
                 _bias_grad(d_qkv, g["b_qkv"])
             if not defer_attn:
                 on_side(ev(), qkv_w)
-                done = torch.cuda.Event()
-                done.record(side)
-                side_done[li] = done
-            ln_dy = self.gln1[mb, li, :T] if dec else d_head
+            ln_dy = (self.gln1[mb, li] if dec else self.sd_ln1[q])[:T]
             self._dgrad_reduce(d_qkv, p["w_qkv"], 3 * Dl, T, out=ln_dy)
             # LN1 backward (+ residual d_x2) -> gradient of the layer input
             if li > 0:
@@ -755,8 +760,15 @@ class StageCompute:
                     main.wait_event(side_done[li + 1])
             else:
                 dx, extra = stage_dx()
-            _ln_bwd(ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx,
-                    None if dec else g["ln1_g"], None if dec else g["ln1_b"])
+            _ln_bwd(ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx, None, None)
+            if not dec:
+                on_side(ev(), lambda ln_dy=ln_dy, x=x, g=g, li=li: _ln_bwd(
+                    ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], None, None, None,
+                    g["ln1_g"], g["ln1_b"]))
+            if not defer_attn:   # everything this layer queued on the side stream (scratch set q)
+                done = torch.cuda.Event()
+                done.record(side)
+                side_done[li] = done
             for dst in extra:   # the other TP ranks of the previous stage (identical bytes)
                 _copy_rows(dst, dx, T, D)
             dy = dx
