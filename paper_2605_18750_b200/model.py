@@ -611,7 +611,9 @@ class StageCompute:
         attention backward) runs on the main stream; each layer's weight-gradient
         GEMMs + bias reductions run on a side stream as soon as their inputs
         exist, so they fill the tail waves of the dgrad GEMMs and overlap the
-        non-GEMM attention / LayerNorm backward.  That overlap is why the
+        non-GEMM attention / LayerNorm backward; the LayerNorm parameter
+        gradients join them there (from parity-buffered LN input gradients), so
+        the main stream carries only the input-gradient chain.  That overlap is why the
         attention-side weight gradients stay in B even when decomposed: moved
         to W they would run alone (B-input + W > fused B).  Scratch comes in two
         parity sets; the main stream only rewrites a set after the side stream
