@@ -226,6 +226,9 @@ int rrfp_enable_peer_access(int dev, int peer);
 /* Single-GPU pipeline emulation: n disjoint SM partitions (green contexts) of
  * >= min_sms SMs; two streams per partition in streams[2i], streams[2i+1]. */
 int rrfp_green_streams(int device, int n, int min_sms, void** streams, int* sms);
+/* Destroy the 2n streams and n green contexts rrfp_green_streams returned
+ * (streams as returned, after the caller synchronised them). */
+int rrfp_green_destroy(void* const* streams, int n);
 /* Wire neighbours: inbox of the lanes that receive this lane's F output
  * (next stage, all R ranks) and B output (previous stage, all R ranks), and
  * the TP group's agreement board slots.  Pointers may be peer pointers. */

@@ -85,7 +85,7 @@ EXPORTS = [
     "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_gemm_set_tail_split", "rrfp_gemm_set_multicast", "rrfp_gemm_max_clusters", "rrfp_gemm_set_bk", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_embedding_fwd",
     "rrfp_embedding_bwd", "rrfp_bias_grad", "rrfp_copy_rows", "rrfp_xent_fwd", "rrfp_xent_bwd",
     "rrfp_tp_create", "rrfp_tp_buffers", "rrfp_tp_connect", "rrfp_tp_allreduce", "rrfp_tp_error",
-    "rrfp_tp_destroy", "rrfp_clock_pingpong", "rrfp_enable_peer_access", "rrfp_green_streams",
+    "rrfp_tp_destroy", "rrfp_clock_pingpong", "rrfp_enable_peer_access", "rrfp_green_streams", "rrfp_green_destroy",
 ]
 
 _lib = None

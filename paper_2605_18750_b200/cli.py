@@ -1,14 +1,16 @@
 """Command line for the B200 path: the reference's run commands with a ``--gpu`` hook.
 
-    python -m paper_2605_18750_b200 simulate-rrfp [CONFIG] [--gpu] [--set a.b=v ...]
-    python -m paper_2605_18750_b200 simulate-1f1b [CONFIG] [--gpu]
-    python -m paper_2605_18750_b200 live          [CONFIG]
+    python -m paper_2605_18750_b200 simulate-rrfp [--config] CONFIG [--gpu] [--live] [--set a.b=v ...]
+    python -m paper_2605_18750_b200 simulate-1f1b [--config] CONFIG [--gpu]
+    python -m paper_2605_18750_b200 live          [--config] CONFIG
 
 Mirrors ``rrfp.cli`` (cli.py:106-273) for these three commands: the same
 config resolution and flags (--seed --hint --limit --jitter --tp --out
 --watchdog-secs --set), artifacts under ``<out>/<run-id>/`` (config.json,
 trace.jsonl, metrics.json, reports/gantt.csv), a one-line summary, and the
-exit codes 0 ok / 2 config violation / 3 deadlock or watchdog (cli.py:37-39).
+exit codes 0 ok / 2 config violation (incl. a missing or malformed config
+file) / 3 deadlock or watchdog with ``<out>/deadlock_dump.txt`` (cli.py:37-39,
+326-338).
 ``simulate-*`` run the virtual clock on the host twin of the C++ state
 machine, or with ``--gpu`` in the device replay kernel; ``live`` runs the
 device lanes (gpu.mode free|fixed|replay).  Unlike the reference
@@ -98,6 +100,8 @@ def _summary(cmd, cfg, metrics, d):
 
 def cmd_simulate(args, kind: str) -> int:
     args.set = list(args.set or []) + [f"scheduler.kind={kind}"]
+    if kind == "rrfp" and getattr(args, "live", False):     # cli.py:187-188
+        return cmd_live(args)
     cfg = _resolve(args)
     trace, metrics = _simulate(cfg, kind, "cuda" if args.gpu else "cpu")
     d = write_run(cfg, trace, metrics, {"device": "cuda" if args.gpu else "cpu (host twin)"})
@@ -125,6 +129,10 @@ def build_parser() -> argparse.ArgumentParser:
     for name in ("simulate-rrfp", "simulate-1f1b", "live"):
         p = sub.add_parser(name)
         p.add_argument("config", nargs="?")
+        p.add_argument("--config", dest="config_opt", metavar="CONFIG",
+                       help="JSON config path (the reference's spelling, cli.py:277)")
+        p.add_argument("--live", action="store_true",
+                       help="simulate-rrfp: execute on the device lanes instead (cli.py:187-188)")
         p.add_argument("--set", action="append", metavar="KEY.PATH=VALUE")
         p.add_argument("--seed", type=int)
         p.add_argument("--hint")
@@ -138,8 +146,21 @@ def build_parser() -> argparse.ArgumentParser:
     return ap
 
 
+def _write_dump(args, e) -> Path:
+    """The reference's deadlock artefact (cli.py:332-338): <out>/deadlock_dump.txt."""
+    path = Path(getattr(args, "out", None) or "out") / "deadlock_dump.txt"
+    path.parent.mkdir(parents=True, exist_ok=True)
+    path.write_text(str(getattr(e, "dump", "") or e) + "\n")
+    return path
+
+
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
+    if args.config_opt is not None:
+        if args.config is not None and args.config != args.config_opt:
+            print("config error: give the config once (positional or --config)", file=sys.stderr)
+            return EXIT_CONFIG
+        args.config = args.config_opt
     try:
         if args.cmd == "live":
             return cmd_live(args)
@@ -147,12 +168,15 @@ def main(argv=None) -> int:
     except ConfigError as e:
         print(f"config error: {e}", file=sys.stderr)
         return EXIT_CONFIG
+    except (json.JSONDecodeError, FileNotFoundError) as e:   # cli.py:329-331
+        print(f"config error: {e}", file=sys.stderr)
+        return EXIT_CONFIG
     except (EngineDeadlockError, ScheduleDeadlockError) as e:
-        print(f"deadlock: {e}", file=sys.stderr)
+        print(f"deadlock/watchdog: {e} (dump: {_write_dump(args, e)})", file=sys.stderr)
         return EXIT_DEADLOCK
     except Exception as e:   # the runtime's watchdog (LiveWatchdogError) -> exit 3 with its dump
         if type(e).__name__ == "LiveWatchdogError":
-            print(f"watchdog: {e}\n{getattr(e, 'dump', '')}", file=sys.stderr)
+            print(f"deadlock/watchdog: {e} (dump: {_write_dump(args, e)})", file=sys.stderr)
             return EXIT_DEADLOCK
         raise
 

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "../../include/rrfp_b200.h"
 #include "rrfp_common.h"
 
@@ -19,6 +22,9 @@ F entry(const char* name) {
     return nullptr;
   return reinterpret_cast<F>(p);
 }
+// main stream of each partition -> its green context (released by rrfp_green_destroy)
+std::mutex g_mu;
+std::unordered_map<void*, CUgreenCtx> g_ctx_of;
 }  // namespace
 
 // n partitions of >= min_sms SMs each on `device`; per partition two streams
@@ -69,7 +75,34 @@ extern "C" int rrfp_green_streams(int device, int n, int min_sms, void** streams
       return rrfp_fail(RRFP_E_CUDA, "cuGreenCtxStreamCreate");
     streams[2 * i] = a;
     streams[2 * i + 1] = b;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_ctx_of[(void*)a] = g;
   }
   if (sms) *sms = (int)groups[0].sm.smCount;
+  return RRFP_OK;
+}
+
+// Release what rrfp_green_streams created: the 2n streams and the n green
+// contexts (the caller has synchronised them).  Unknown streams are skipped.
+extern "C" int rrfp_green_destroy(void* const* streams, int n) {
+  using sdestroy_t = CUresult (*)(CUstream);
+  using gdestroy_t = CUresult (*)(CUgreenCtx);
+  auto sdestroy = entry<sdestroy_t>("cuStreamDestroy");
+  auto gdestroy = entry<gdestroy_t>("cuGreenCtxDestroy");
+  if (!sdestroy || !gdestroy) return rrfp_fail(RRFP_E_CUDA, "green-context driver entry points unavailable");
+  if (n < 0 || (n > 0 && !streams)) return rrfp_fail(RRFP_E_INVALID, "rrfp_green_destroy: bad arguments");
+  for (int i = 0; i < n; ++i) {
+    CUgreenCtx g = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_ctx_of.find(streams[2 * i]);
+      if (it == g_ctx_of.end()) continue;
+      g = it->second;
+      g_ctx_of.erase(it);
+    }
+    sdestroy((CUstream)streams[2 * i]);
+    if (streams[2 * i + 1]) sdestroy((CUstream)streams[2 * i + 1]);
+    if (gdestroy(g) != CUDA_SUCCESS) return rrfp_fail(RRFP_E_CUDA, "cuGreenCtxDestroy failed");
+  }
   return RRFP_OK;
 }

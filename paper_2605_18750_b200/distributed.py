@@ -298,17 +298,20 @@ class DistPipeline:
             dist.all_gather_object(allv, mine, group=group)
             nominal_us = allv[::self.R]      # TP rank 0 of every stage
         self.nominal_table = nominal_us
-        floors = lognormal_floor_tables(self.world, self.n_mb, nominal_us, sigma, seed, stages=[self.rank])
+        floors = lognormal_floor_tables(self.world, self.n_mb, nominal_us, sigma, seed, stages=[self.rank],
+                                        n_chunks=self.C)
         self.group.set_floor_us(floors)
 
     def kernel_launches_per_step(self):
-        return sum(sum(st.kernel_counts.values()) + 2 * len(st.kernel_counts) for st in self.vstages) + 2
+        # bodies + one dispatcher step per task, the exiting step, init and final
+        return sum(sum(st.kernel_counts.values()) + len(st.kernel_counts) for st in self.vstages) + 3
 
     def step(self, watchdog_secs=120.0):
         for st in self.vstages:
             st.zero_grads()
         events, t0s = self.group.run_iteration(watchdog_secs)
         self.last_events = (events, min(t0s))
+        self.check_tp()
         if self.stage.last:
             return self.stage.loss.sum() / (self.stage.cfg.seq * self.stage.M)
         return None
@@ -321,7 +324,15 @@ class DistPipeline:
     def wait(self, watchdog_secs=120.0):
         events, t0s = self.group.wait(watchdog_secs)
         self.last_events = (events, min(t0s))
+        self.check_tp()
         return events
+
+    def check_tp(self):
+        """Raise if this rank's TP all-reduce timed out on a peer (csrc/tp.cu
+        only sets a sticky error word on the device)."""
+        if self.comm is not None and self.comm.error():
+            raise RuntimeError(f"TP all-reduce of stage {self.rank} rank {self.tp_rank} timed out "
+                               "waiting for a peer: this iteration's results are invalid")
 
     def close(self):
         self.group.close()

@@ -45,27 +45,33 @@ def nominal_workload(cfg: GPTConfig, n_stages: int, n_mb: int, decompose: bool,
                     latency=lat, decompose_backward=decompose)
 
 
-def lognormal_floor_tables(n_stages, n_mb, nominal_us, sigma, seed, stages=None):
+def lognormal_floor_tables(n_stages, n_mb, nominal_us, sigma, seed, stages=None, n_chunks=1):
     """Per-task duration floors (µs) for injected lognormal compute jitter
     (SURVEY.md 8d, config 5): X ~ LogNormal(0, sigma) drawn on the host per
-    (stage, mb, direction) from the (seed, "cjitter", ...) stream; the device
-    pads the task until start + nominal * X.  W shares B's draw so a
+    (stage, mb, chunk, direction) from the (seed, "cjitter", ...) stream; the
+    device pads the task until start + nominal * X.  W shares B's draw so a
     decomposed (BFW) and a fused (1F1B / BF) backward see the same
-    perturbation.  Returns {stage: float64[3, KEYS]} (dir rows B=0, F=1, W=2).
-    """
+    perturbation.  Returns {stage: float64[3, KEYS]} (dir rows B=0, F=1, W=2)
+    indexed like every lane table, KEYS = C * 32*MW, key = chunk * 32*MW + mb
+    (tables.key_of)."""
     import numpy as np
     from .rng import substream
-    keys = ((n_mb + 31) // 32) * 32
+    from .tables import key_of
+    mw = (n_mb + 31) // 32
+    keys = n_chunks * mw * 32
     out = {}
     for s in (stages if stages is not None else range(n_stages)):
         t = np.zeros((3, keys))
         if sigma > 0:
-            for mb in range(n_mb):
-                for d, row in (("F", 1), ("B", 0)):
-                    x = float(np.exp(substream(seed, "cjitter", s, mb, d).normal(0.0, sigma)))
-                    t[row, mb] = nominal_us[s][d] * x
-                    if d == "B" and nominal_us[s].get("W"):
-                        t[2, mb] = nominal_us[s]["W"] * x
+            for c in range(n_chunks):
+                for mb in range(n_mb):
+                    k = key_of(mb, c, mw)
+                    for d, row in (("F", 1), ("B", 0)):
+                        labels = (s, mb, d) if n_chunks == 1 else (s, mb, c, d)
+                        x = float(np.exp(substream(seed, "cjitter", *labels).normal(0.0, sigma)))
+                        t[row, k] = nominal_us[s][d] * x
+                        if d == "B" and nominal_us[s].get("W"):
+                            t[2, k] = nominal_us[s]["W"] * x
         out[s] = t
     return out
 
@@ -146,6 +152,7 @@ class GpuPipeline:
             if len(set(devices)) != 1 or R != 1:
                 raise ValueError("green partitions emulate a pipeline on ONE device without TP")
             arr = (ctypes.c_void_p * (2 * N))()
+            self._green_raw = arr
             sms = ctypes.c_int()
             n_sm = torch.cuda.get_device_properties(devices[0]).multi_processor_count
             _lib.check(_lib.lib().rrfp_green_streams(devices[0], N, max(2, (n_sm // N) & ~1), arr,
@@ -219,6 +226,7 @@ class GpuPipeline:
                     st.zero_grads()
         events, t0s = self.group.run_iteration(watchdog_secs)
         self.last_events = (events, min(t0s))
+        self.check_tp()
         last = self.stages[-1]
         return last.loss.sum() / (last.cfg.seq * self.M)
 
@@ -233,6 +241,7 @@ class GpuPipeline:
     def wait(self, watchdog_secs: float = 120.0):
         events, t0s = self.group.wait(watchdog_secs)
         self.last_events = (events, min(t0s))
+        self.check_tp()
         return events
 
     def nominal_us(self):
@@ -259,22 +268,31 @@ class GpuPipeline:
             tr, _ = self.trace()
             nominal_us = measured_nominal(tr, self.N)
         self.nominal_table = nominal_us
-        floors = lognormal_floor_tables(self.N, self.M, nominal_us, sigma, seed)
+        floors = lognormal_floor_tables(self.N, self.M, nominal_us, sigma, seed, n_chunks=self.C)
         self.group.set_floor_us(floors)
 
     def kernel_launches_per_step(self):
-        """Our kernels launched per iteration: every task body (captured counts)
-        plus the lane's dispatch + complete kernels per task and init/final."""
+        """Our kernels launched per iteration: every task body (captured counts),
+        one dispatcher step kernel per task plus the exiting step, and the
+        lane's init / final kernels."""
         n = 0
         for row in self.grid:
             for st in row:
-                n += sum(st.kernel_counts.values())
-                n += 2 * len(st.kernel_counts) + 2
-        return n
+                n += sum(st.kernel_counts.values()) + len(st.kernel_counts)
+        return n + 3 * self.N * self.R
 
     def trace(self):
         ev, t0 = self.last_events
         return wall_trace(self.workload, ev, t0)
+
+    def check_tp(self):
+        """A timed-out TP all-reduce only sets a sticky error word on the
+        device (csrc/tp.cu): surface it as an exception after every step."""
+        for s, comms in self.comms.items():
+            for c in comms:
+                if c.error():
+                    raise RuntimeError(f"TP all-reduce of stage {s} rank {c.rank} timed out "
+                                       "waiting for a peer: this iteration's results are invalid")
 
     def close(self):
         self.group.close()
@@ -286,3 +304,10 @@ class GpuPipeline:
             for st in row:
                 st.release()
         self.grid = self.stages = None
+        raw = getattr(self, "_green_raw", None)
+        if raw is not None:     # the SM partitions of the single-GPU emulation
+            from . import _lib
+            torch.cuda.synchronize()
+            self.green_streams = {}
+            _lib.check(_lib.lib().rrfp_green_destroy(raw, len(raw) // 2))
+            self._green_raw = None

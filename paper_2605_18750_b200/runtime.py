@@ -147,8 +147,7 @@ class LaneGroup:
                             for t in order[s]]
             floor = None
             if floor_table_us is not None:
-                floor = np.ascontiguousarray(np.rint(np.asarray(floor_table_us[s], np.float64)
-                                                     * 1000.0 * time_scale).astype(np.int64))
+                floor = self._floor_ns(floor_table_us[s], keys, time_scale)
             self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
                                                       _ptr(fixed), _ptr(floor) if floor is not None
@@ -162,13 +161,21 @@ class LaneGroup:
         if len(self.local) == n * r and not defer_bodies:
             self.connect_local()
 
+    @staticmethod
+    def _floor_ns(table_us, keys, scale):
+        """[3, KEYS] µs floor table -> contiguous int64 ns; the C side copies
+        exactly 3*KEYS entries, so the shape is checked here."""
+        a = np.asarray(table_us, np.float64)
+        if a.shape != (3, keys):
+            raise ValueError(f"floor table must be [3, {keys}] (dir x key), got {a.shape}")
+        return np.ascontiguousarray(np.rint(a * 1000.0 * scale).astype(np.int64))
+
     def set_floor_us(self, floor_by_stage):
         """Replace the lognormal-jitter floor tables (µs, [3, KEYS] per stage)
         between iterations."""
         for (s, k), h in self.lanes.items():
             dur, comm, dskew, fixed, _ = self._tables[(s, k)]
-            floor = np.ascontiguousarray(np.rint(np.asarray(floor_by_stage[s], np.float64)
-                                                 * 1000.0 * self.scale).astype(np.int64))
+            floor = self._floor_ns(floor_by_stage[s], self.tables.keys, self.scale)
             self._tables[(s, k)] = (dur, comm, dskew, fixed, floor)
             _lib.check(self.L.rrfp_runtime_load_tables(h, _ptr(dur), _ptr(comm), _ptr(dskew),
                                                       _ptr(fixed), _ptr(floor)))

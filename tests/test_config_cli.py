@@ -95,6 +95,26 @@ def test_cli_exit_codes(tmp_path, capsys):
     assert main(["simulate-rrfp", "--hint", f"file:{ext}", "--out", str(tmp_path)]) == 3
 
 
+def test_cli_reference_spelling_and_errors(tmp_path, capsys):
+    """`--config PATH` (the reference's documented form, cli.py:277) works; a
+    missing or malformed config exits 2 (cli.py:329-331); a deadlock exits 3
+    and writes <out>/deadlock_dump.txt (cli.py:332-338)."""
+    cfgp = tmp_path / "example.json"
+    cfgp.write_text(json.dumps(EXAMPLE))
+    assert main(["simulate-rrfp", "--config", str(cfgp), "--out", str(tmp_path / "o")]) == 0
+    assert "makespan=2158" in capsys.readouterr().out
+    assert main(["simulate-rrfp", "--config", str(tmp_path / "missing.json")]) == 2
+    bad = tmp_path / "bad.json"
+    bad.write_text("{not json")
+    assert main(["simulate-1f1b", "--config", str(bad)]) == 2
+    ext = tmp_path / "hint.json"
+    ext.write_text(json.dumps({"order": [["F", "asc"]]}))
+    out = tmp_path / "dl"
+    assert main(["simulate-rrfp", "--hint", f"file:{ext}", "--out", str(out)]) == 3
+    dump = (out / "deadlock_dump.txt").read_text()
+    assert "remaining" in dump
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["free", "fixed", "replay"])
 def test_cli_gpu_hook(tmp_path, capsys, mode):
