@@ -94,6 +94,11 @@ typedef struct {
  * __host__ __device__ code runs inside the device dispatcher. */
 int rrfp_arbitrate(const rrfp_stage_state* st, const rrfp_hint* hint, rrfp_decision* out);
 
+/* next_by_priority, arbitration.py:119-129: the first key of a chunk-major
+ * set (C*MW words) in forward order min(chunk, mb) (forward = 1) or backward
+ * order min(-chunk, mb) (forward = 0); kind RRFP_WAIT if the set is empty. */
+int rrfp_next_by_priority(const uint32_t* words, int32_t C, int32_t MW, int32_t forward, rrfp_decision* out);
+
 /* update_backpressure, arbitration.py:188-215.  In/out on mode/focus. */
 int rrfp_update_backpressure(rrfp_stage_state* st, int32_t limit, int32_t n_f, int32_t n_b);
 

@@ -76,7 +76,7 @@ EVENT_KINDS = {0: "exec", 1: "send", 2: "recv", 3: "coord", 4: "coord"}
 
 # exported symbols declared in include/rrfp_b200.h (checked by the CPU test-suite)
 EXPORTS = [
-    "rrfp_arbitrate", "rrfp_update_backpressure", "rrfp_replay_workspace_bytes",
+    "rrfp_arbitrate", "rrfp_next_by_priority", "rrfp_update_backpressure", "rrfp_replay_workspace_bytes",
     "rrfp_replay_event_capacity", "rrfp_replay_host", "rrfp_replay_device",
     "rrfp_runtime_create", "rrfp_runtime_destroy", "rrfp_runtime_inbox", "rrfp_runtime_inbox_ipc",
     "rrfp_ipc_open", "rrfp_ipc_close", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",

@@ -75,6 +75,15 @@ extern "C" int rrfp_arbitrate(const rrfp_stage_state* st, const rrfp_hint* hint,
   return RRFP_OK;
 }
 
+extern "C" int rrfp_next_by_priority(const uint32_t* words, int32_t C, int32_t MW, int32_t forward,
+                                     rrfp_decision* out) {
+  if (!words || !out) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  if (C < 1 || MW < 1 || C * MW > RRFP_MAX_WORDS) return rrfp_fail(RRFP_E_INVALID, "bad set shape");
+  int k = forward ? first_asc(words, C, MW) : first_desc(words, C, MW);
+  *out = mk_dec(k < 0 ? RRFP_WAIT : (forward ? RRFP_DIR_F : RRFP_DIR_B), k, MW);
+  return RRFP_OK;
+}
+
 extern "C" int rrfp_update_backpressure(rrfp_stage_state* st, int32_t limit, int32_t n_f, int32_t n_b) {
   if (!st) return rrfp_fail(RRFP_E_INVALID, "null argument");
   rrfp_bp_update(&st->mode, &st->focus, limit, n_f, n_b, st->doneF, st->doneB, st->M, st->C, st->MW);
