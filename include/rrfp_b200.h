@@ -178,6 +178,20 @@ typedef struct {
   double time_scale;               /* live.run_live time_scale */
   int64_t coord_cost_ns;
   rrfp_hint hint;
+  /* virtual_clock = 1: replay mode.  The lane makes EVERY decision itself
+   * (rrfp_arbitrate_core + the K4 TP round) at the reference engine's
+   * virtual times (engine.py:298-367): messages carry their virtual arrival
+   * time (end + comm delay + rank skew, engine.py:211-221), each lane
+   * publishes a lower bound on the virtual time of its future sends, and a
+   * lane processes tick T only when every in-neighbour's bound exceeds T
+   * (conservative parallel discrete-event simulation).  Tables are then in
+   * integer microseconds (virtual), trace records carry virtual times.
+   * v_dmin = the stage's smallest task duration, v_la = the smallest
+   * comm delay + skew of the lane's sends (v_dmin + v_la >= 1 for progress),
+   * v_horizon = an upper bound of the makespan (beyond it: deadlock). */
+  int32_t virtual_clock;
+  int32_t declog_cap;              /* > 0: log every arbitration (inputs + decision), records */
+  int64_t v_dmin, v_la, v_horizon;
 } rrfp_lane_desc;
 
 int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** out);
@@ -263,6 +277,17 @@ int rrfp_runtime_launch(rrfp_runtime* rt, int64_t epoch, void* stream);
 int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_event* events, int32_t cap,
                       int32_t* n_events, int64_t* t0_ns);
 int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap);
+/* Decision log of the last iteration (desc.declog_cap > 0): one record per
+ * arbitration the lane evaluated, uint32 words, stride = 16 + 5*nwords:
+ *   [0] stage [1] rank [2] n_f [3] n_b [4] bp mode before update_backpressure
+ *   [5] focus before [6] mode after [7] focus after [8] phase (-1/B/F)
+ *   [9] admission (-1) [10] decision kind [11] mb [12] chunk [13] nwords
+ *   [14..15] time (virtual us, or %globaltimer ns in free mode)
+ *   then fready, bready, wpend, doneF, doneB (nwords each, chunk-major keys).
+ * The inputs are exactly what rrfp_arbitrate_core saw, so the host can
+ * re-evaluate each decision with the reference's arbitrate (tests/). */
+int rrfp_runtime_declog(rrfp_runtime* rt, uint32_t* out, int32_t cap_words, int32_t* n_records,
+                        int32_t* stride_words);
 
 /* ---- stage-compute kernel entry points (unit-test surface) ------------- */
 

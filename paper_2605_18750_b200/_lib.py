@@ -69,7 +69,9 @@ class LaneDesc(C.Structure):
                 ("fixed_mode", C.c_int32), ("per_stage", C.c_int32), ("stage", C.c_int32),
                 ("rank", C.c_int32), ("device", C.c_int32), ("compute_kind", C.c_int32),
                 ("trace_cap", C.c_int32), ("time_scale", C.c_double),
-                ("coord_cost_ns", C.c_int64), ("hint", Hint)]
+                ("coord_cost_ns", C.c_int64), ("hint", Hint),
+                ("virtual_clock", C.c_int32), ("declog_cap", C.c_int32),
+                ("v_dmin", C.c_int64), ("v_la", C.c_int64), ("v_horizon", C.c_int64)]
 
 
 EVENT_KINDS = {0: "exec", 1: "send", 2: "recv", 3: "coord", 4: "coord"}
@@ -80,7 +82,7 @@ EXPORTS = [
     "rrfp_replay_event_capacity", "rrfp_replay_host", "rrfp_replay_device",
     "rrfp_runtime_create", "rrfp_runtime_destroy", "rrfp_runtime_inbox", "rrfp_runtime_inbox_ipc",
     "rrfp_ipc_open", "rrfp_ipc_close", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
-    "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status",
+    "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status", "rrfp_runtime_declog",
     "rrfp_spin", "rrfp_last_error", "rrfp_abi_version", "rrfp_gemm_bf16", "rrfp_gemm_set_variant", "rrfp_set_pdl",
     "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_gemm_set_tail_split", "rrfp_gemm_set_multicast", "rrfp_gemm_max_clusters", "rrfp_gemm_set_bk", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_embedding_fwd",
     "rrfp_embedding_bwd", "rrfp_bias_grad", "rrfp_copy_rows", "rrfp_xent_fwd", "rrfp_xent_bwd",

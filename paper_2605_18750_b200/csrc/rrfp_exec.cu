@@ -51,7 +51,13 @@ struct lane_inbox {
   uint32_t view_count;                          // monotone count of visible arrivals
   uint32_t done_epoch;                          // iteration barrier
   uint32_t pad[2];
+  // replay (virtual-clock) mode: (epoch << 44) | lower bound of the virtual
+  // time of any message this lane has not sent yet (conservative PDES)
+  unsigned long long vsafe;
 };
+
+#define V_TBITS 44
+#define V_INF ((1LL << V_TBITS) - 1)
 
 struct lane_state {
   rrfp_lane_desc d;
@@ -82,6 +88,16 @@ struct lane_state {
   uint32_t doneF[RRFP_MAX_WORDS], doneB[RRFP_MAX_WORDS], wpend[RRFP_MAX_WORDS];
   uint32_t fdisp[RRFP_MAX_WORDS], bdisp[RRFP_MAX_WORDS];
   uint32_t recvF[RRFP_MAX_WORDS], recvB[RRFP_MAX_WORDS];
+  // ---- replay (virtual-clock) mode: engine._Stage of this lane (engine.py:70-90)
+  long long v_now, v_busy_until, v_coord_until, v_coord_end, v_touch, v_start, v_end, v_H;
+  int32_t v_await, v_nin;
+  lane_inbox* v_in[2 * RRFP_MAX_RANKS];          // in-neighbour lanes (their vsafe words)
+  uint32_t vF[RRFP_MAX_WORDS], vB[RRFP_MAX_WORDS], vP[RRFP_MAX_WORDS];   // own view + pending grads
+  uint32_t procF[RRFP_MAX_RANKS][RRFP_MAX_WORDS], procB[RRFP_MAX_RANKS][RRFP_MAX_WORDS];
+  // ---- decision log (desc.declog_cap records)
+  uint32_t* declog;
+  int32_t declog_n;
+  uint32_t declog_sig;     // free mode: inputs of the last logged WAIT (re-polls are not logged)
 };
 
 // ------------------------------------------------------------ primitives
@@ -147,6 +163,11 @@ __global__ void lane_init_kernel(lane_state* L) {
     L->remaining = L->d.per_stage;
     L->fixed_head = 0; L->status = 0; L->cur_kind = LANE_NONE;
     L->ring_n = 0;
+    L->declog_n = 0;
+    L->declog_sig = 0xFFFFFFFFu;
+    L->v_now = 0; L->v_busy_until = 0; L->v_coord_until = 0; L->v_coord_end = -1;
+    L->v_touch = 0;       // engine.run dispatches every stage at t = 0 (engine.py:345-346)
+    L->v_start = L->v_end = 0; L->v_H = 0; L->v_await = 0;
     L->t_iter0 = gtimer();
     L->mon[0] = 1; L->mon[2] = L->remaining; L->mon[3] = (int32_t)L->epoch;
   }
@@ -154,6 +175,8 @@ __global__ void lane_init_kernel(lane_state* L) {
     L->doneF[i] = L->doneB[i] = L->wpend[i] = 0;
     L->fdisp[i] = L->bdisp[i] = 0;
     L->recvF[i] = L->recvB[i] = 0;
+    L->vF[i] = L->vB[i] = L->vP[i] = 0;
+    for (int r = 0; r < RRFP_MAX_RANKS; ++r) L->procF[r][i] = L->procB[r][i] = 0;
   }
 }
 
@@ -208,14 +231,49 @@ __device__ void build_view(lane_state* L, uint32_t* sF, uint32_t* sB, unsigned l
   __syncwarp();
 }
 
-__device__ rrfp_decision lane_arbitrate(lane_state* L, const uint32_t* sF, const uint32_t* sB) {
+// One record per evaluated arbitration: the exact inputs of rrfp_bp_update +
+// rrfp_arbitrate_core and the result (layout: include/rrfp_b200.h,
+// rrfp_runtime_declog).  Thread 0 only.
+__device__ void declog_put(lane_state* L, long long t, int mode_in, int focus_in, const uint32_t* fr,
+                           const uint32_t* br, const rrfp_decision& dec) {
+  if (!L->declog) return;
+  const int nw = L->nwords;
+  if (L->declog_n < L->d.declog_cap) {
+    uint32_t* r = L->declog + (size_t)L->declog_n * (16 + 5 * nw);
+    r[0] = L->d.stage; r[1] = L->d.rank; r[2] = L->n_f; r[3] = L->n_b;
+    r[4] = mode_in; r[5] = (uint32_t)focus_in; r[6] = L->mode; r[7] = (uint32_t)L->focus;
+    r[8] = (uint32_t)L->phase; r[9] = (uint32_t)L->next_adm;
+    r[10] = dec.kind; r[11] = (uint32_t)dec.mb; r[12] = (uint32_t)dec.chunk; r[13] = nw;
+    r[14] = (uint32_t)(unsigned long long)t; r[15] = (uint32_t)((unsigned long long)t >> 32);
+    for (int w = 0; w < nw; ++w) {
+      r[16 + w] = fr[w]; r[16 + nw + w] = br[w]; r[16 + 2 * nw + w] = L->wpend[w];
+      r[16 + 3 * nw + w] = L->doneF[w]; r[16 + 4 * nw + w] = L->doneB[w];
+    }
+  }
+  L->declog_n += 1;   // counts past the capacity: the host reports an overflow
+}
+
+__device__ rrfp_decision lane_arbitrate(lane_state* L, const uint32_t* sF, const uint32_t* sB,
+                                        long long t) {
   const rrfp_lane_desc& d = L->d;
+  const int mode_in = L->mode, focus_in = L->focus;
   rrfp_bp_update(&L->mode, &L->focus, d.buffer_limit, L->n_f, L->n_b, L->doneF, L->doneB, d.M,
                  d.C, d.MW);
   rrfp_view_ref v;
   v.fready = sF; v.bready = sB; v.wpend = L->wpend; v.doneF = L->doneF; v.doneB = L->doneB;
   v.admission = L->next_adm;
-  return rrfp_arbitrate_core(v, d.hint, L->mode, L->focus, L->phase, d.M, d.C, d.MW, d.decompose);
+  rrfp_decision dec =
+      rrfp_arbitrate_core(v, d.hint, L->mode, L->focus, L->phase, d.M, d.C, d.MW, d.decompose);
+  if (L->declog) {
+    // a WAIT is re-evaluated on every poll: log it once per distinct input
+    // (inputs only grow between dispatches, so the ready-bit count + the
+    // remaining-task count identify them)
+    uint32_t sig = (uint32_t)L->remaining << 20;
+    for (int w = 0; w < L->nwords; ++w) sig += __popc(sF[w]) + __popc(sB[w]) + __popc(L->wpend[w]);
+    if (dec.kind != RRFP_WAIT || sig != L->declog_sig) declog_put(L, t, mode_in, focus_in, sF, sB, dec);
+    L->declog_sig = dec.kind == RRFP_WAIT ? sig : 0xFFFFFFFFu;
+  }
+  return dec;
 }
 
 __device__ rrfp_decision lane_fixed_head(lane_state* L, const uint32_t* sF, const uint32_t* sB) {
@@ -256,6 +314,36 @@ __device__ __forceinline__ uint32_t dec_code(const rrfp_decision& d) {
   return (uint32_t)d.kind | ((uint32_t)(d.mb & 1023) << 2) | ((uint32_t)(d.chunk & 15) << 12);
 }
 
+// K4: one TP agreement round over the group's boards (arbitration.py:323-334,
+// live._resolve_round 246-277): publish this rank's proposal into every
+// peer's board, gather all R (the same vector on every rank).  Returns the
+// sum of the proposers' arrival counts (free mode's retry snapshot).
+__device__ uint32_t tp_exchange(lane_state* L, const rrfp_decision& dec, rrfp_decision* ds) {
+  const rrfp_lane_desc& d = L->d;
+  const int R = d.R;
+  unsigned long long round = ++L->tp_round;
+  unsigned long long word = (round << 32) | dec_code(dec);
+  uint32_t mycnt = L->inbox->view_count;
+  const int par = (int)(round & 1);
+  for (int r = 0; r < R; ++r) {
+    L->tp_peer[r]->tp_cnt[par][d.rank] = mycnt;
+    __threadfence_system();
+    st_release_sys64(&L->tp_peer[r]->tp_prop[par][d.rank], word);
+  }
+  uint32_t snap = 0;
+  for (int r = 0; r < R; ++r) {
+    unsigned long long w;
+    while (((w = ld_acquire_sys64(&L->inbox->tp_prop[par][r])) >> 32) != round) {
+      if (*L->abort_flag) break;
+      __nanosleep(32);
+    }
+    uint32_t code = (uint32_t)w;
+    ds[r].kind = code & 3; ds[r].mb = (code >> 2) & 1023; ds[r].chunk = (code >> 12) & 15;
+    snap += L->inbox->tp_cnt[par][r];
+  }
+  return snap;
+}
+
 __device__ void lane_dispatch(lane_state* L) {
   __shared__ uint32_t sF[RRFP_MAX_WORDS], sB[RRFP_MAX_WORDS];
   __shared__ int s_kind, s_exit;
@@ -280,7 +368,8 @@ __device__ void lane_dispatch(lane_state* L) {
     unsigned long long now = gtimer();
     build_view(L, sF, sB, now);
     if (lane == 0) {
-      rrfp_decision dec = d.fixed_mode ? lane_fixed_head(L, sF, sB) : lane_arbitrate(L, sF, sB);
+      rrfp_decision dec =
+          d.fixed_mode ? lane_fixed_head(L, sF, sB) : lane_arbitrate(L, sF, sB, (long long)now);
       s_kind = RRFP_WAIT;
       if (R == 1) {
         if (dec.kind == RRFP_WAIT) {
@@ -292,27 +381,8 @@ __device__ void lane_dispatch(lane_state* L) {
       } else {
         // K4: TP agreement round over the group's boards (arbitration.py:323-334,
         // live._resolve_round 246-277): publish, gather all R, same verdict everywhere.
-        unsigned long long round = ++L->tp_round;
-        unsigned long long word = (round << 32) | dec_code(dec);
-        uint32_t mycnt = L->inbox->view_count;
-        const int par = (int)(round & 1);
-        for (int r = 0; r < R; ++r) {
-          L->tp_peer[r]->tp_cnt[par][d.rank] = mycnt;
-          __threadfence_system();
-          st_release_sys64(&L->tp_peer[r]->tp_prop[par][d.rank], word);
-        }
         rrfp_decision ds[RRFP_MAX_RANKS];
-        uint32_t snap = 0;
-        for (int r = 0; r < R; ++r) {
-          unsigned long long w;
-          while (((w = ld_acquire_sys64(&L->inbox->tp_prop[par][r])) >> 32) != round) {
-            if (*L->abort_flag) break;
-            __nanosleep(32);
-          }
-          uint32_t code = (uint32_t)w;
-          ds[r].kind = code & 3; ds[r].mb = (code >> 2) & 1023; ds[r].chunk = (code >> 12) & 15;
-          snap += L->inbox->tp_cnt[par][r];
-        }
+        uint32_t snap = tp_exchange(L, dec, ds);
         bool all_wait = true, all_w = true;
         for (int r = 0; r < R; ++r) {
           all_wait = all_wait && ds[r].kind == RRFP_WAIT;
@@ -379,6 +449,306 @@ __device__ void lane_dispatch(lane_state* L) {
   }
 }
 
+// ======================================================== replay (virtual clock)
+// The lane runs the reference engine's per-stage semantics itself
+// (engine.py:181-340) at virtual times, and makes every decision with the
+// same rrfp_arbitrate_core + K4 round as free mode.  Cross-lane knowledge is
+// only what physically arrived: a message carries its virtual arrival time
+// (vt = end + comm delay + rank skew, engine.py:211-221) in the inbox's
+// visible-at stamp; each lane publishes vsafe = a lower bound of the vt of
+// anything it has not sent yet; a lane processes tick T only when every
+// in-neighbour's vsafe exceeds T, so every arrival with vt <= T has landed
+// (Chandy-Misra-Bryant conservative PDES, lookahead = min task duration +
+// min comm delay).  Within a tick the engine applies all events, then
+// dispatches (engine.py:347-362); a stage's arrivals and its own completion
+// commute (no dispatch happens while it is busy), so a lane applies its
+// completion as soon as the body has run and its arrivals tick by tick.
+
+__device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end);
+
+__device__ __forceinline__ long long v_min(long long a, long long b) { return a < b ? a : b; }
+__device__ __forceinline__ long long v_max(long long a, long long b) { return a > b ? a : b; }
+
+__device__ void v_publish(lane_state* L, long long h) {   // thread 0; monotone
+  if (h > V_INF) h = V_INF;
+  if (h <= L->v_H) return;
+  L->v_H = h;
+  unsigned long long w = ((unsigned long long)(L->epoch & 0xFFFFFu) << V_TBITS) | (unsigned long long)h;
+  __threadfence_system();            // every message sent so far is visible before the bound
+  st_release_sys64(&L->inbox->vsafe, w);
+}
+
+// min over the in-neighbours' bounds (V_INF without in-neighbours)
+__device__ long long v_safe(lane_state* L) {
+  long long S = V_INF;
+  for (int i = 0; i < L->v_nin; ++i) {
+    unsigned long long w = ld_acquire_sys64(&L->v_in[i]->vsafe);
+    long long h = ((w >> V_TBITS) == (L->epoch & 0xFFFFFu)) ? (long long)(w & (unsigned long long)V_INF) : 0;
+    S = v_min(S, h);
+  }
+  return S;
+}
+
+__device__ __forceinline__ long long warp_min64(long long v) {
+  for (int o = 16; o; o >>= 1) v = v_min(v, (long long)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, o));
+  return v;
+}
+
+// Earliest vt of a landed, unprocessed arrival at ANY rank of this stage (the
+// stage is touched by every rank's arrivals, engine.py:225-238).  Warp.
+__device__ long long v_scan(lane_state* L) {
+  const int lane = threadIdx.x;
+  const rrfp_lane_desc& d = L->d;
+  const uint32_t ep = L->epoch;
+  long long best = V_INF;
+  for (int q = 0; q < d.R; ++q) {
+    const lane_inbox* in = L->tp_peer[q];
+    for (int w = 0; w < L->nwords; ++w) {
+      int key = w * 32 + lane;
+      if (rrfp_key_mb(key, d.MW) >= d.M) continue;
+      if (!((L->procF[q][w] >> lane) & 1u) && ld_acquire_sys(&in->fflag[key]) == ep)
+        best = v_min(best, (long long)ld_volatile64(&in->fvis[key]));
+      if (!((L->procB[q][w] >> lane) & 1u) && ld_acquire_sys(&in->bflag[key]) == ep)
+        best = v_min(best, (long long)ld_volatile64(&in->bvis[key]));
+    }
+  }
+  return warp_min64(best);
+}
+
+// Apply every landed arrival with vt == T (engine._apply_arrival): own rank's
+// into the view (B gated on the local F, else pending), all ranks' marked
+// processed.  Returns whether any rank had one (stage touched).  Warp.
+__device__ bool v_arrivals(lane_state* L, long long T) {
+  const int lane = threadIdx.x;
+  const rrfp_lane_desc& d = L->d;
+  const uint32_t ep = L->epoch;
+  bool any = false;
+  for (int q = 0; q < d.R; ++q) {
+    const lane_inbox* in = L->tp_peer[q];
+    for (int w = 0; w < L->nwords; ++w) {
+      int key = w * 32 + lane;
+      int mb = rrfp_key_mb(key, d.MW), c = rrfp_key_chunk(key, d.MW);
+      bool valid = mb < d.M;
+      bool af = valid && !((L->procF[q][w] >> lane) & 1u) && ld_acquire_sys(&in->fflag[key]) == ep &&
+                (long long)ld_volatile64(&in->fvis[key]) == T;
+      bool ab = valid && !((L->procB[q][w] >> lane) & 1u) && ld_acquire_sys(&in->bflag[key]) == ep &&
+                (long long)ld_volatile64(&in->bvis[key]) == T;
+      uint32_t mF = __ballot_sync(0xffffffffu, af);
+      uint32_t mB = __ballot_sync(0xffffffffu, ab);
+      if (q == d.rank) {
+        if (af) ring_emit(L, 2, T, T, d.rank, rrfp_make_task(RRFP_DIR_F, d.stage, mb, c));
+        if (ab) ring_emit(L, 2, T, T, d.rank, rrfp_make_task(RRFP_DIR_B, d.stage, mb, c));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        L->procF[q][w] |= mF;
+        L->procB[q][w] |= mB;
+        if (q == d.rank) {
+          L->vF[w] |= mF;
+          L->vB[w] |= mB & L->doneF[w];
+          L->vP[w] |= mB & ~L->doneF[w];
+        }
+      }
+      any = any || mF || mB;
+      __syncwarp();
+    }
+  }
+  return any;
+}
+
+// engine._apply_complete (engine.py:240-266) for the task whose body just ran.
+__device__ void v_complete(lane_state* L) {
+  const rrfp_lane_desc& d = L->d;
+  const int kind = L->cur_kind;
+  rrfp_task_t t = L->cur_task;
+  int mb = rrfp_task_mb(t), c = rrfp_task_chunk(t);
+  int k = rrfp_key(mb, c, d.MW);
+  const long long end = L->v_end;
+  L->remaining -= 1;
+  L->mon[0] = 3;
+  L->mon[2] = L->remaining;
+  if (kind == RRFP_DIR_F) {
+    bit_set(L->doneF, k);
+    L->n_f += 1;
+    if (bit_get(L->vP, k)) { bit_clr(L->vP, k); bit_set(L->vB, k); }
+    if (d.stage == d.N - 1 && c == d.C - 1) bit_set(L->vB, k);   // turn-around (engine.py:193-199)
+    else lane_send(L, kind, mb, c, (unsigned long long)end);
+  } else if (kind == RRFP_DIR_B) {
+    bit_set(L->doneB, k);
+    L->n_b += 1;
+    if (d.decompose) bit_set(L->wpend, k);
+    lane_send(L, kind, mb, c, (unsigned long long)end);
+  } else {
+    L->n_w += 1;
+  }
+  L->cur_kind = LANE_NONE;
+  L->v_touch = end;                  // the completion touches the stage at `end`
+  // next send: after a task that starts >= end
+  v_publish(L, end + d.v_dmin + d.v_la);
+}
+
+// engine._commit (engine.py:270-296): virtual start/end, exec record per rank.
+__device__ void v_commit(lane_state* L, const rrfp_decision& dec, long long start) {
+  const rrfp_lane_desc& d = L->d;
+  int k = rrfp_key(dec.mb, dec.chunk, d.MW);
+  long long dur = L->dur_ns[(size_t)dec.kind * L->KEYS + k];     // integer us in replay mode
+  if (dec.kind == RRFP_DIR_F) {
+    if (d.stage == 0 && dec.chunk == 0) L->next_adm = (L->next_adm + 1 < d.M) ? L->next_adm + 1 : -1;
+    else bit_clr(L->vF, k);
+  } else if (dec.kind == RRFP_DIR_B) {
+    bit_clr(L->vB, k);
+  } else {
+    bit_clr(L->wpend, k);
+  }
+  if (d.fixed_mode) L->fixed_head += 1;
+  else rrfp_advance_phase(&L->phase, d.hint, dec.kind);
+  rrfp_task_t task = rrfp_make_task(dec.kind, d.stage, dec.mb, dec.chunk);
+  L->v_start = start;
+  L->v_end = start + dur;
+  L->v_busy_until = start + dur;
+  ring_emit(L, 0, (unsigned long long)start, (unsigned long long)(start + dur), d.R > 1 ? d.rank : -1, task);
+  L->cur_kind = dec.kind;
+  L->cur_task = task;
+  v_publish(L, start + dur + d.v_la);
+}
+
+// engine._dispatch (engine.py:298-340) / the FIXED head rule (baselines.py:121-143)
+// at virtual time T; returns the committed kind or RRFP_WAIT.  Thread 0.
+__device__ int v_dispatch(lane_state* L, long long T) {
+  const rrfp_lane_desc& d = L->d;
+  rrfp_decision dec;
+  if (d.fixed_mode) {
+    if (L->fixed_head >= d.per_stage) return RRFP_WAIT;
+    rrfp_task_t t = L->fixed[L->fixed_head];
+    int dir = rrfp_task_dir(t), mb = rrfp_task_mb(t), c = rrfp_task_chunk(t);
+    int k = rrfp_key(mb, c, d.MW);
+    bool ready = dir == RRFP_DIR_F ? ((d.stage == 0 && c == 0) || bit_get(L->vF, k))
+               : dir == RRFP_DIR_B ? bit_get(L->vB, k) : bit_get(L->wpend, k);
+    if (!ready) return RRFP_WAIT;
+    dec.kind = dir; dec.mb = mb; dec.chunk = c;
+    v_commit(L, dec, T);
+    return dir;
+  }
+  const int mode_in = L->mode, focus_in = L->focus;
+  rrfp_bp_update(&L->mode, &L->focus, d.buffer_limit, L->n_f, L->n_b, L->doneF, L->doneB, d.M, d.C, d.MW);
+  rrfp_view_ref v;
+  v.fready = L->vF; v.bready = L->vB; v.wpend = L->wpend; v.doneF = L->doneF; v.doneB = L->doneB;
+  v.admission = L->next_adm;
+  dec = rrfp_arbitrate_core(v, d.hint, L->mode, L->focus, L->phase, d.M, d.C, d.MW, d.decompose);
+  declog_put(L, T, mode_in, focus_in, L->vF, L->vB, dec);
+  if (d.R == 1) {
+    if (dec.kind == RRFP_WAIT) { L->phase = -1; return RRFP_WAIT; }
+    v_commit(L, dec, T);
+    return dec.kind;
+  }
+  // a blocking round: nothing this lane sends can precede T + dmin (+ la)
+  v_publish(L, T + d.v_dmin + d.v_la);
+  rrfp_decision ds[RRFP_MAX_RANKS];
+  tp_exchange(L, dec, ds);
+  bool all_wait = true, all_w = true;
+  for (int r = 0; r < d.R; ++r) {
+    all_wait = all_wait && ds[r].kind == RRFP_WAIT;
+    all_w = all_w && ds[r].kind == RRFP_DIR_W;
+  }
+  if (all_wait) { L->phase = -1; return RRFP_WAIT; }
+  if (all_w) { v_commit(L, ds[0], T); return RRFP_DIR_W; }
+  if (L->v_await) return RRFP_WAIT;             // a deferred round retries after an arrival
+  bool agreed = ds[0].kind == RRFP_DIR_F || ds[0].kind == RRFP_DIR_B;
+  for (int r = 1; r < d.R && agreed; ++r)
+    agreed = ds[r].kind == ds[0].kind && ds[r].mb == ds[0].mb && ds[r].chunk == ds[0].chunk;
+  const long long cost = d.coord_cost_ns;        // integer us in replay mode
+  if (d.rank == 0)
+    ring_emit(L, agreed ? 3 : 4, (unsigned long long)T, (unsigned long long)(T + cost), -1,
+              agreed ? rrfp_make_task(ds[0].kind, d.stage, ds[0].mb, ds[0].chunk) : RRFP_NO_TASK);
+  if (agreed) { v_commit(L, ds[0], T + cost); return ds[0].kind; }
+  L->v_coord_until = T + cost;
+  L->v_coord_end = T + cost;
+  L->v_await = 1;
+  L->phase = -1;
+  return RRFP_WAIT;
+}
+
+// The replay-mode step: complete the body that just ran, then advance the
+// virtual clock tick by tick until this lane commits its next task (SWITCH
+// branch set) or finishes (WHILE ends).
+__device__ void lane_virtual(lane_state* L) {
+  __shared__ long long s_T;
+  __shared__ int s_state;           // 0 wait, 1 process s_T, 2 exit
+  __shared__ int s_kind;
+  const int lane = threadIdx.x;
+  const rrfp_lane_desc& d = L->d;
+  if (lane == 0 && L->cur_kind != LANE_NONE) v_complete(L);
+  __syncwarp();
+  __shared__ long long s_S;
+  while (true) {
+    // the bound first, then the inbox: every message with vt < S was written
+    // before its sender published S (release / acquire, then __syncwarp)
+    if (lane == 0) s_S = v_safe(L);
+    __syncwarp();
+    long long amin = v_scan(L);
+    if (lane == 0) {
+      s_state = 0;
+      if (*L->abort_flag) {
+        L->status = RRFP_E_WATCHDOG; s_state = 2;
+      } else if (L->remaining == 0) {
+        s_state = 2;
+      } else {
+        const long long S = s_S;
+        long long T = amin;
+        if (L->v_touch >= 0) T = v_min(T, L->v_touch);
+        if (L->v_coord_end >= 0) T = v_min(T, L->v_coord_end);
+        if (T < S && T < V_INF) {
+          s_T = T; s_state = 1;
+        } else {
+          long long base = v_max(L->v_now, v_min(T, S));
+          if (base > d.v_horizon) {            // quiescent with unfinished tasks (engine.py:363-367)
+            L->status = RRFP_E_DEADLOCK; s_state = 2;
+          } else {
+            v_publish(L, base + d.v_dmin + d.v_la);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const int st = s_state;
+    if (st == 2) {
+      if (lane == 0) {
+        v_publish(L, V_INF);
+        L->cur_kind = LANE_NONE;
+        cudaGraphSetConditional(L->h_switch, 0xFFFFFFFFu);
+        cudaGraphSetConditional(L->h_while, 0);
+      }
+      return;
+    }
+    if (st == 0) { __nanosleep(64); continue; }
+    const long long T = s_T;
+    bool any = v_arrivals(L, T);
+    if (lane == 0) {
+      bool touched = any;
+      if (any) L->v_await = 0;
+      if (L->v_coord_end == T) { L->v_coord_end = -1; touched = true; }
+      if (L->v_touch == T) { L->v_touch = -1; touched = true; }
+      L->v_now = T;
+      s_kind = RRFP_WAIT;
+      if (touched && T >= L->v_busy_until && T >= L->v_coord_until && L->remaining > 0) {
+        L->mon[0] = 1;
+        s_kind = v_dispatch(L, T);
+      }
+      if (s_kind != RRFP_WAIT) {
+        L->mon[0] = 2;
+        L->mon[1] = (int32_t)L->cur_task;
+        L->t_start = gtimer();
+        unsigned branch = (unsigned)s_kind;
+        if (d.compute_kind == 1)
+          branch = (unsigned)(s_kind * d.M * d.C + rrfp_task_chunk(L->cur_task) * d.M + rrfp_task_mb(L->cur_task));
+        cudaGraphSetConditional(L->h_switch, branch);
+      }
+    }
+    __syncwarp();
+    if (s_kind != RRFP_WAIT) return;
+  }
+}
+
 // ---------------------------------------------------------------- bodies
 // Synthetic compute: spin the task's table duration (latency+jitter, scaled).
 __global__ void lane_spin_body_kernel(lane_state* L) {
@@ -386,6 +756,7 @@ __global__ void lane_spin_body_kernel(lane_state* L) {
     rrfp_task_t t = L->cur_task;
     int k = rrfp_key(rrfp_task_mb(t), rrfp_task_chunk(t), L->d.MW);
     long long ns = L->dur_ns[(size_t)rrfp_task_dir(t) * L->KEYS + k];
+    if (L->d.virtual_clock) ns = (long long)((double)ns * 1000.0 * L->d.time_scale);
     spin_until(L->t_start + (unsigned long long)ns);
   }
 }
@@ -475,6 +846,10 @@ __device__ void lane_complete(lane_state* L) {
 // task instead of a dispatch and a completion kernel: ~1 device-side launch
 // less per decision (tools/dispatch_bench.py).
 __global__ void __launch_bounds__(32, 1) lane_step_kernel(lane_state* L) {
+  if (L->d.virtual_clock) {
+    lane_virtual(L);
+    return;
+  }
   if (threadIdx.x == 0) lane_complete(L);
   __syncwarp();
   lane_dispatch(L);
@@ -495,6 +870,7 @@ struct rrfp_runtime {
   int32_t* mon_dev;
   cudaGraph_t graph;
   cudaGraphExec_t exec;
+  uint32_t* declog;         // device, desc.declog_cap records
   std::vector<cudaGraph_t> bodies;   // [3 * M] per-(kind, mb) compute graphs
   bool built;
   cudaEvent_t done_ev;
@@ -513,6 +889,14 @@ static int lane_check_desc(const rrfp_lane_desc* d) {
     return rrfp_fail(RRFP_E_INVALID, "stage/rank out of range");
   if (d->buffer_limit < 1) return rrfp_fail(RRFP_E_INVALID, "buffer_limit must be >= 1");
   if (d->trace_cap < 16) return rrfp_fail(RRFP_E_INVALID, "trace_cap too small");
+  if (d->declog_cap < 0) return rrfp_fail(RRFP_E_INVALID, "declog_cap must be >= 0");
+  if (d->virtual_clock) {
+    if (d->fixed_mode && d->R > 1)
+      return rrfp_fail(RRFP_E_INVALID, "replay of a fixed schedule is rank-agnostic (R must be 1)");
+    if (d->v_dmin + d->v_la < 1)
+      return rrfp_fail(RRFP_E_INVALID, "replay mode needs a positive lookahead (min task + comm delay >= 1 us)");
+    if (d->v_horizon < 1 || d->v_horizon >= V_INF) return rrfp_fail(RRFP_E_INVALID, "bad replay horizon");
+  }
   return RRFP_OK;
 }
 
@@ -536,6 +920,10 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   RRFP_CUDA_TRY(cudaMemset(rt->tables, 0, tbytes));
   RRFP_CUDA_TRY(cudaMalloc(&rt->fixed, sizeof(rrfp_task_t) * (size_t)(desc->per_stage + 1)));
   RRFP_CUDA_TRY(cudaMalloc(&rt->ring, sizeof(rrfp_event) * (size_t)desc->trace_cap));
+  rt->declog = nullptr;
+  if (desc->declog_cap > 0)
+    RRFP_CUDA_TRY(cudaMalloc(&rt->declog, sizeof(uint32_t) * (size_t)desc->declog_cap *
+                                              (16 + 5 * desc->C * desc->MW)));
   RRFP_CUDA_TRY(cudaHostAlloc(&rt->abort_host, sizeof(int32_t), cudaHostAllocMapped));
   *rt->abort_host = 0;
   RRFP_CUDA_TRY(cudaHostGetDevicePointer(&rt->abort_dev, rt->abort_host, 0));
@@ -560,6 +948,8 @@ extern "C" int rrfp_runtime_create(const rrfp_lane_desc* desc, rrfp_runtime** ou
   h.ring_cap = desc->trace_cap;
   h.abort_flag = rt->abort_dev;
   h.mon = rt->mon_dev;
+  h.declog = rt->declog;
+  h.v_nin = 0;
   h.n_lanes = 1;
   h.all[0] = rt->inbox;
   for (int r = 0; r < RRFP_MAX_RANKS; ++r) h.fwd_dst[r] = h.bwd_dst[r] = h.tp_peer[r] = rt->inbox;
@@ -576,6 +966,7 @@ extern "C" void rrfp_runtime_destroy(rrfp_runtime* rt) {
   for (void* p : rt->opened) cudaIpcCloseMemHandle(p);
   cudaFree(rt->L); cudaFree(rt->inbox); cudaFree(rt->tables); cudaFree(rt->fixed);
   cudaFree(rt->ring); cudaFreeHost(rt->abort_host); cudaFreeHost(rt->mon_host);
+  if (rt->declog) cudaFree(rt->declog);
   cudaEventDestroy(rt->done_ev);
   delete rt;
 }
@@ -652,6 +1043,19 @@ extern "C" int rrfp_runtime_connect(rrfp_runtime* rt, void* const* fwd_dst, void
   if (tp_peer) {
     h.n_lanes = NL;
     for (int i = 0; i < NL; ++i) h.all[i] = tp_peer[R + i] ? (lane_inbox*)tp_peer[R + i] : rt->inbox;
+  }
+  // replay mode: the lanes whose messages reach this stage (any rank) --
+  // F from the previous stage (from N-1 at stage 0 when C > 1: the chunk
+  // wrap), B from the next (from 0 at N-1 when C > 1); never itself.
+  {
+    const int s = rt->d.stage, N = rt->d.N, C = rt->d.C;
+    h.v_nin = 0;
+    if (s > 0 || C > 1)
+      for (int r = 0; r < R; ++r)
+        if (h.bwd_dst[r] != rt->inbox) h.v_in[h.v_nin++] = h.bwd_dst[r];
+    if (s < N - 1 || C > 1)
+      for (int r = 0; r < R; ++r)
+        if (h.fwd_dst[r] != rt->inbox) h.v_in[h.v_nin++] = h.fwd_dst[r];
   }
   RRFP_CUDA_TRY(cudaMemcpy(rt->L, &h, sizeof(h), cudaMemcpyHostToDevice));
   return RRFP_OK;
@@ -865,10 +1269,31 @@ extern "C" int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_ev
     RRFP_CUDA_TRY(cudaMemcpy(events, rt->ring, sizeof(rrfp_event) * n, cudaMemcpyDeviceToHost));
   if (n_events) *n_events = n;
   if (t0_ns) *t0_ns = (int64_t)h.t_iter0;
+  if (h.status == RRFP_E_DEADLOCK && !fired)
+    return rrfp_fail(RRFP_E_DEADLOCK, "replay: stage %d rank %d quiescent with %d unfinished tasks",
+                     rt->d.stage, rt->d.rank, h.remaining);
   if (fired || h.status == RRFP_E_WATCHDOG)
     return rrfp_fail(RRFP_E_WATCHDOG, "watchdog: stage %d rank %d remaining=%d n_f=%d n_b=%d",
                      rt->d.stage, rt->d.rank, h.remaining, h.n_f, h.n_b);
   if (h.ring_n > h.ring_cap) return rrfp_fail(RRFP_E_CAPACITY, "trace ring overflow");
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_declog(rrfp_runtime* rt, uint32_t* out, int32_t cap_words, int32_t* n_records,
+                                   int32_t* stride_words) {
+  if (!rt || !n_records) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  const int stride = 16 + 5 * rt->d.C * rt->d.MW;
+  if (stride_words) *stride_words = stride;
+  *n_records = 0;
+  if (!rt->declog) return RRFP_OK;
+  int32_t n = 0;
+  RRFP_CUDA_TRY(cudaMemcpy(&n, (char*)rt->L + offsetof(lane_state, declog_n), sizeof(n), cudaMemcpyDeviceToHost));
+  if (n > rt->d.declog_cap) return rrfp_fail(RRFP_E_CAPACITY, "decision log overflow (%d > %d)", n, rt->d.declog_cap);
+  if ((long long)n * stride > cap_words) return rrfp_fail(RRFP_E_CAPACITY, "output buffer too small");
+  if (n > 0 && out)
+    RRFP_CUDA_TRY(cudaMemcpy(out, rt->declog, sizeof(uint32_t) * (size_t)n * stride, cudaMemcpyDeviceToHost));
+  *n_records = n;
   return RRFP_OK;
 }
 

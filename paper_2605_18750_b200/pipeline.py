@@ -102,7 +102,7 @@ class GpuPipeline:
                  devices=None, stage_latency_us=None, model_seed: int = 1234, data_seed: int = 0,
                  schedule=None, comm_delay=None, tp_size: int = 1, tp: TpGroup | None = None,
                  n_chunks: int = 1, mm=None, head_cost: float = 0.0, gemm_sm_cap: int = 0, w_split: str = "fc",
-                 green: bool = False, split: str = "layer"):
+                 green: bool = False, split: str = "layer", declog_cap: int = 0):
         if mm is not None and (tp_size > 1 or n_chunks > 1):
             raise ValueError("the multimodal pipeline (config 4) runs with TP=1, C=1")
         if isinstance(hint, str):
@@ -214,7 +214,7 @@ class GpuPipeline:
         self.group = LaneGroup(w, hint, buffer_limit, 1.0, seed=seed, jitter=jitter, mode=mode,
                                tp=tp or (TpGroup(group_size=R) if R > 1 else None),
                                placement=[[d] * R for d in devices], bodies=bodies, compute_kind=1,
-                               schedule=schedule,
+                               schedule=schedule, declog_cap=declog_cap,
                                lane_streams={(s_, 0): self.green_streams[s_][0] for s_ in self.green_streams})
         self.last_events = None
 
@@ -282,8 +282,16 @@ class GpuPipeline:
         return n + 3 * self.N * self.R
 
     def trace(self):
+        """(Trace, Metrics) of the last iteration: wall clock, or the virtual
+        clock in replay mode (the lanes' own decisions at engine times)."""
         ev, t0 = self.last_events
-        return wall_trace(self.workload, ev, t0)
+        self.group.w = self.workload
+        return self.group.make_trace(ev, [t0])
+
+    def decisions(self):
+        """Every arbitration the lanes evaluated in the last iteration
+        (constructed with declog_cap > 0), for the per-decision oracle check."""
+        return self.group.decisions()
 
     def check_tp(self):
         """A timed-out TP all-reduce only sets a sticky error word on the

@@ -12,8 +12,15 @@ under torchrun) exchanges inbox addresses as CUDA IPC handles
 Modes
   free    lanes arbitrate on what physically arrived (the reference's live path)
   fixed   lanes follow a per-stage order list, head blocking (1F1B baseline)
-  replay  the replay kernel (engine.py) computes the virtual-clock dispatch
-          order first; lanes then execute exactly that order on the device
+  replay  every lane makes its own decisions (the same device arbiter + K4
+          round as free mode) at the reference engine's VIRTUAL times: a
+          message carries its virtual arrival time, each lane publishes a
+          lower bound on the virtual time of its future sends, and a lane
+          decides at tick T only once every in-neighbour's bound exceeds T
+          (conservative PDES; csrc/rrfp_exec.cu "replay").  Nothing is taken
+          from the oracle: the resulting trace (virtual times) is compared
+          with run_rrfp's event for event by the tests.  With ``schedule``:
+          FIXED heads under the same virtual clock (run_fixed semantics).
 """
 
 from __future__ import annotations
@@ -25,7 +32,7 @@ import numpy as np
 from . import _lib
 from .arbitration import HintOrder, TpGroup
 from .baselines import FixedSchedule, build_1f1b_schedule
-from .engine import gaps, replay_tables
+from .engine import EngineDeadlockError, build_trace_metrics, gaps, replay_tables
 from .jitter import JitterConfig
 from .tables import DIR_IDX, key_of, lower
 from .trace import Metrics, StageMetrics, Trace, TraceEvent
@@ -66,7 +73,7 @@ class LaneGroup:
                  tp: TpGroup | None = None, mode: str = "free", schedule: FixedSchedule | None = None,
                  placement=None, local=None, bodies=None, compute_kind: int = 0,
                  trace_cap: int | None = None, pad_table_us=None, defer_bodies: bool = False,
-                 floor_table_us=None, lane_streams=None):
+                 floor_table_us=None, lane_streams=None, declog_cap: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("run_gpu needs a CUDA device (B200)")
@@ -80,12 +87,11 @@ class LaneGroup:
         n, r = workload.num_stages, workload.tp_group_size
         self.n, self.r = n, r
         order = None
-        if mode == "fixed":
+        if mode == "fixed" or (mode == "replay" and schedule is not None):
             schedule = schedule or build_1f1b_schedule(workload)
             schedule.validate_for(workload)
             order = schedule.per_stage_order
-        elif mode == "replay":
-            order = replay_order(workload, hint, buffer_limit, seed, jitter, tp)
+        self.virtual = mode == "replay"
         tb = lower(workload, hint, buffer_limit, seed, jitter, tp)
         self.tables = tb
         self._seed, self._jitter, self._tp = seed, jitter, tp
@@ -98,6 +104,10 @@ class LaneGroup:
         per_stage = tb.desc.per_stage
         tpg = tp or TpGroup(group_size=r)
         cap = trace_cap or (16 * workload.num_microbatches * workload.num_chunks * (r + 2) + 256)
+        if self.virtual:   # deferred TP rounds: at most one per arrival tick
+            cap += 4 * workload.num_microbatches * workload.num_chunks * r
+        self.declog_cap = declog_cap
+        vh = self._virtual_bounds(tb, tpg) if self.virtual else None
         self.L = _lib.lib()
         self.lanes = {}
         self.streams = {}
@@ -108,6 +118,7 @@ class LaneGroup:
             d.decompose = int(workload.decompose_backward)
             d.buffer_limit = buffer_limit
             d.fixed_mode = int(order is not None)
+            self._fixed_order = order is not None
             d.per_stage = per_stage
             d.stage, d.rank = s, k
             d.device = placement[s][k]
@@ -116,14 +127,21 @@ class LaneGroup:
             d.time_scale = time_scale
             d.coord_cost_ns = int(round(tpg.coordination_round_cost * 1000 * time_scale))
             d.hint = _lib.make_hint(hint)
+            d.declog_cap = declog_cap
+            if self.virtual:
+                d.virtual_clock = 1
+                d.coord_cost_ns = int(tpg.coordination_round_cost)       # integer us
+                d.v_dmin, d.v_la, d.v_horizon = vh["dmin"][s], vh["la"][(s, k)], vh["horizon"]
             h = C.c_void_p()
             _lib.check(self.L.rrfp_runtime_create(C.byref(d), C.byref(h)))
             self.lanes[(s, k)] = h
             dev = torch.device("cuda", placement[s][k])
             # (lane_streams: e.g. a green-context partition's stream, see pipeline.py)
             self.streams[(s, k)] = (lane_streams or {}).get((s, k)) or torch.cuda.Stream(dev)
-            # tables (ns)
-            if compute_kind == 0:
+            # tables (ns; replay mode: integer virtual us, latency + injected)
+            if self.virtual:
+                dur = tb.dur[s].astype(np.float64)
+            elif compute_kind == 0:
                 dur = tb.dur[s].astype(np.float64) * 1000.0 * time_scale
             else:   # real bodies: the table only carries the jitter pad (K11)
                 dur = np.zeros((3, keys))
@@ -133,14 +151,15 @@ class LaneGroup:
                 if pad_table_us is not None:
                     dur += pad_table_us[s]
                 dur = dur * 1000.0 * time_scale
+            unit = 1.0 if self.virtual else 1000.0 * time_scale
             dur = np.ascontiguousarray(np.rint(dur).astype(np.int64))
-            comm = np.ascontiguousarray(np.rint(tb.comm[s] * 1000.0 * time_scale).astype(np.int64))
+            comm = np.ascontiguousarray(np.rint(tb.comm[s] * unit).astype(np.int64))
             f_dst = s + 1 if s + 1 < n else 0
             b_dst = s - 1 if s > 0 else n - 1
             dskew = np.zeros((2, keys, r), np.int64)
             dskew[DIR_IDX[FORWARD]] = tb.skew[f_dst, DIR_IDX[FORWARD]]
             dskew[DIR_IDX[BACKWARD]] = tb.skew[b_dst, DIR_IDX[BACKWARD]]
-            dskew = np.ascontiguousarray(np.rint(dskew * 1000.0 * time_scale).astype(np.int64))
+            dskew = np.ascontiguousarray(np.rint(dskew * unit).astype(np.int64))
             fixed = np.zeros(max(per_stage, 1), np.uint32)
             if order is not None:
                 fixed[:] = [_lib.task_code(t.direction, t.stage, t.microbatch, t.chunk)
@@ -160,6 +179,42 @@ class LaneGroup:
         self.epoch = 0
         if len(self.local) == n * r and not defer_bodies:
             self.connect_local()
+
+    @staticmethod
+    def _virtual_bounds(tb, tpg):
+        """Replay-mode constants per lane: the stage's smallest task duration
+        (v_dmin), the smallest comm delay + arrival skew of the lane's sends
+        (v_la) -- together the PDES lookahead -- and an upper bound of the
+        makespan (every instant of a live run has a task, a message or a TP
+        round in progress), past which a quiescent lane reports a deadlock."""
+        d = tb.desc
+        n, m, cc, r, mw = d.N, d.M, d.C, d.R, d.MW
+        keys = [key_of(mb, c, mw) for c in range(cc) for mb in range(m)]
+        dirs = (0, 1, 2) if d.decompose else (0, 1)
+        dmin = [int(min(tb.dur[s, di, k] for di in dirs for k in keys)) for s in range(n)]
+        la = {}
+        for s in range(n):
+            f_dst = s + 1 if s + 1 < n else 0
+            b_dst = s - 1 if s > 0 else n - 1
+            for q in range(r):
+                best = None
+                for c in range(cc):
+                    # (direction row, destination stage, destination chunk) of the
+                    # sends of chunk c (engine._send routing, engine.py:181-209)
+                    sends = []
+                    if s + 1 < n or c + 1 < cc:
+                        sends.append((DIR_IDX[FORWARD], f_dst, c if s + 1 < n else c + 1))
+                    if s > 0 or c > 0:
+                        sends.append((DIR_IDX[BACKWARD], b_dst, c if s > 0 else c - 1))
+                    for di, dst, dc in sends:
+                        for mb in range(m):
+                            v = int(tb.comm[s, di, key_of(mb, c, mw)] + tb.skew[dst, di, key_of(mb, dc, mw), q])
+                            best = v if best is None else min(best, v)
+                la[(s, q)] = best or 0
+        n_msgs = 2 * n * m * cc
+        horizon = (int(tb.dur.sum()) + int(tb.comm.sum()) + int(tb.skew.max(initial=0)) * n_msgs
+                   + int(tpg.coordination_round_cost) * (n * d.per_stage + n_msgs * r + n) + 16)
+        return {"dmin": dmin, "la": la, "horizon": horizon}
 
     @staticmethod
     def _floor_ns(table_us, keys, scale):
@@ -291,7 +346,7 @@ class LaneGroup:
 
     def wait(self, watchdog_secs: float = 30.0):
         """Block until every local lane finished; returns raw events and t0s."""
-        out, t0s, failures = [], [], []
+        out, t0s, failures, deadlocks = [], [], [], []
         for lane, h in self.lanes.items():
             ev = (_lib.Event * self.cap)()
             n_ev = C.c_int32()
@@ -300,6 +355,8 @@ class LaneGroup:
                                           C.byref(n_ev), C.byref(t0))
             if rc == -3:
                 failures.append(self.L.rrfp_last_error().decode())
+            elif rc == -2:
+                deadlocks.append(self.L.rrfp_last_error().decode())
             elif rc != 0:
                 _lib.check(rc)
             out.extend(ev[: n_ev.value])
@@ -312,7 +369,33 @@ class LaneGroup:
                 dump.append(buf.value.decode())
             raise LiveWatchdogError("device runtime watchdog fired: " + "; ".join(failures),
                                     "\n".join(dump))
+        if deadlocks:     # replay mode: the virtual clock quiesced (engine.py:363-367)
+            raise EngineDeadlockError("quiescent with unfinished tasks", "\n".join(deadlocks))
         return out, t0s
+
+    def decisions(self):
+        """The last iteration's decision log of every local lane (declog_cap > 0):
+        a list of dicts with the exact inputs of update_backpressure + arbitrate
+        and the decision the device made (include/rrfp_b200.h rrfp_runtime_declog)."""
+        out = []
+        for lane, h in self.lanes.items():
+            n, stride = C.c_int32(), C.c_int32()
+            _lib.check(self.L.rrfp_runtime_declog(h, None, 0, C.byref(n), C.byref(stride)))
+            if n.value == 0:
+                continue
+            buf = np.zeros(n.value * stride.value, np.uint32)
+            _lib.check(self.L.rrfp_runtime_declog(h, buf.ctypes.data_as(C.c_void_p), buf.size,
+                                                  C.byref(n), C.byref(stride)))
+            for rec in buf.reshape(n.value, stride.value):
+                out.append(parse_decision(rec, self.tables.desc.MW))
+        return out
+
+    def make_trace(self, events, t0s):
+        """(Trace, Metrics) of one iteration: virtual-clock (replay mode) or wall."""
+        if self.virtual:
+            return virtual_trace(self.w, events, fixed=self._fixed_order)
+        return wall_trace(self.w, events, min(t0s), self.scale)
+
 
     def run_iteration(self, watchdog_secs: float = 30.0):
         self.launch()
@@ -331,6 +414,76 @@ class LaneGroup:
             self.close()
         except Exception:
             pass
+
+
+def _i32(x):
+    x = int(x)
+    return x - (1 << 32) if x >= 1 << 31 else x
+
+
+def parse_decision(rec, mw):
+    """One rrfp_runtime_declog record -> dict of (mb, chunk) sets and scalars."""
+    nw = int(rec[13])
+
+    def keys(words):
+        out = set()
+        for w, v in enumerate(words):
+            v = int(v)
+            while v:
+                b = (v & -v).bit_length() - 1
+                k = w * 32 + b
+                out.add((k % (mw * 32), k // (mw * 32)))
+                v &= v - 1
+        return out
+    base = 16
+    blk = [rec[base + i * nw: base + (i + 1) * nw] for i in range(5)]
+    modes = {0: "normal", 1: "drain", 2: "focus"}
+    kind = {0: "B", 1: "F", 2: "W", 3: "wait"}[int(rec[10])]
+    return {"stage": int(rec[0]), "rank": int(rec[1]), "n_f": int(rec[2]), "n_b": int(rec[3]),
+            "mode_in": modes[int(rec[4])], "focus_in": _i32(rec[5]),
+            "mode": modes[int(rec[6])], "focus": _i32(rec[7]),
+            "phase": {-1: "", 0: "B", 1: "F"}[_i32(rec[8])], "admission": _i32(rec[9]),
+            "kind": kind, "task": None if kind == "wait" else (_i32(rec[11]), _i32(rec[12])),
+            "t": int(rec[14]) | (int(rec[15]) << 32),
+            "fready": keys(blk[0]), "bready": keys(blk[1]), "wpend": keys(blk[2]),
+            "doneF": keys(blk[3]), "doneB": keys(blk[4])}
+
+
+def virtual_trace(workload: Workload, events, fixed: bool = False):
+    """Replay-mode lane records (virtual us) -> (Trace, Metrics) exactly as
+    engine.run_rrfp / baselines.run_fixed build them (engine.py:381-449):
+    compute / coord per stage, agreed / deferred rounds, occupancy peaks
+    (through engine.build_trace_metrics), block gaps."""
+    from types import SimpleNamespace
+    n = workload.num_stages
+    comp, coord = [0] * n, [0] * n
+    nf, nb, nw = [0] * n, [0] * n, [0] * n
+    agreed = deferred = 0
+    makespan = 0
+    for e in events:
+        if e.kind == 0:
+            makespan = max(makespan, e.t1)
+            if e.rank <= 0:
+                d, st, _, _ = _lib.task_fields(e.task)
+                comp[st] += e.t1 - e.t0
+                if d == FORWARD:
+                    nf[st] += 1
+                elif d == BACKWARD:
+                    nb[st] += 1
+                else:
+                    nw[st] += 1
+        elif e.kind in (3, 4):
+            coord[e.stage] += e.t1 - e.t0
+            agreed += e.kind == 3
+            deferred += e.kind == 4
+    res = SimpleNamespace(makespan=makespan, agreed=agreed, deferred=deferred, compute=comp,
+                          coord=coord, n_f=nf, n_b=nb, n_w=nw)
+    evs = [e for e in events if e.kind == 0] if fixed else list(events)
+    tr, met = build_trace_metrics(workload, evs, res, fixed=fixed)
+    if fixed:
+        for sm in met.per_stage:
+            sm.n_w = 0
+    return tr, met
 
 
 def wall_trace(workload: Workload, events, t0_ns: int, time_scale: float = 1.0):
@@ -412,17 +565,25 @@ def dispatch_latency(trace, n_stages: int) -> dict:
 def run_gpu(workload: Workload, hint: HintOrder | str = "bf", buffer_limit: int = 32,
             time_scale: float = 1.0, *, seed: int = 0, jitter: JitterConfig | None = None,
             tp: TpGroup | None = None, watchdog_secs: float = 30.0, mode: str = "free",
-            schedule: FixedSchedule | None = None, placement=None):
+            schedule: FixedSchedule | None = None, placement=None, declog: list | None = None,
+            declog_cap: int | None = None):
     """One iteration on device lanes with synthetic (latency-table) compute.
 
     Drop-in for ``run_live``: same arguments plus ``mode`` / ``schedule`` /
     ``placement``.  Raises LiveWatchdogError (with a per-lane dump) if no
-    lane finishes within ``watchdog_secs``.
+    lane finishes within ``watchdog_secs``; in replay mode a virtual-clock
+    deadlock raises EngineDeadlockError like run_rrfp.  ``declog`` (a list)
+    receives every arbitration the lanes evaluated (LaneGroup.decisions).
+    mode="replay" returns the virtual-clock trace (clock "virtual").
     """
+    if declog_cap is None:
+        declog_cap = (8 * workload.task_count() // workload.num_stages + 64) if declog is not None else 0
     g = LaneGroup(workload, hint, buffer_limit, time_scale, seed=seed, jitter=jitter, tp=tp,
-                  mode=mode, schedule=schedule, placement=placement)
+                  mode=mode, schedule=schedule, placement=placement, declog_cap=declog_cap)
     try:
         events, t0s = g.run_iteration(watchdog_secs)
+        if declog is not None:
+            declog.extend(g.decisions())
+        return g.make_trace(events, t0s)
     finally:
         g.close()
-    return wall_trace(workload, events, min(t0s), time_scale)

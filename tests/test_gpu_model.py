@@ -182,3 +182,35 @@ def test_green_partition_pipeline_matches_fp32_reference():
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("hint", ["bf", "bfw"])
+def test_gpt_pp4_lane_decisions_match_oracle(hint):
+    """GPT PP=4 with real bodies: every free-running arbitration (logged on the
+    device) re-evaluates to the same decision under the reference's arbitrate;
+    in replay mode the lanes' own decisions give run_rrfp's trace exactly."""
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from decision_check import check_decisions
+    import paper_2605_18750_b200 as P
+    import rrfp_oracle as O
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, 4, 8, hint=hint, mode="free", declog_cap=1024)
+    try:
+        for _ in range(2):
+            pipe.step(watchdog_secs=60)
+        log = pipe.decisions()
+        assert sum(d["kind"] != "wait" for d in log) == pipe.workload.task_count()
+        assert not check_decisions(log, pipe.workload, P.HintOrder(hint), 32)
+    finally:
+        pipe.close()
+    pipe = GpuPipeline(cfg, 4, 8, hint=hint, mode="replay")
+    try:
+        pipe.step(watchdog_secs=60)
+        tr, met = pipe.trace()
+        ev, om = O.run_rrfp(O.from_workload_json(pipe.workload.to_json()), hint, 32, 0, "J0")
+        got = sorted((e.t_start, e.t_end, e.stage, e.microbatch, e.direction) for e in tr.execs())
+        want = sorted((a, b, s, mb, d) for (a, b, s, r, mb, c, d, k) in ev if k == "exec")
+        assert got == want
+        assert met.makespan == om["makespan"]
+    finally:
+        pipe.close()

