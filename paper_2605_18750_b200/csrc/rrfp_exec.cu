@@ -1290,7 +1290,7 @@ extern "C" int rrfp_runtime_declog(rrfp_runtime* rt, uint32_t* out, int32_t cap_
   int32_t n = 0;
   RRFP_CUDA_TRY(cudaMemcpy(&n, (char*)rt->L + offsetof(lane_state, declog_n), sizeof(n), cudaMemcpyDeviceToHost));
   if (n > rt->d.declog_cap) return rrfp_fail(RRFP_E_CAPACITY, "decision log overflow (%d > %d)", n, rt->d.declog_cap);
-  if ((long long)n * stride > cap_words) return rrfp_fail(RRFP_E_CAPACITY, "output buffer too small");
+  if (out && (long long)n * stride > cap_words) return rrfp_fail(RRFP_E_CAPACITY, "output buffer too small");
   if (n > 0 && out)
     RRFP_CUDA_TRY(cudaMemcpy(out, rt->declog, sizeof(uint32_t) * (size_t)n * stride, cudaMemcpyDeviceToHost));
   *n_records = n;
