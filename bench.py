@@ -4,8 +4,10 @@
                     [--hint bf|bfw|1f1b] [--mb 32] [--jitter J0..J3] [--layers 24]
 
 N=1 runs PP=1 (the single-GPU configuration of BASELINE.json configs[1]);
-under torchrun each rank is one pipeline stage (PP=N, one stage per GPU,
-mailboxes over CUDA IPC / NVLink).  A step = one training iteration over
+``--gpus N`` > 1 runs PP=N (N/tp stages x tp ranks), one process per GPU: under
+torchrun as launched by the driver, or -- started as plain ``python bench.py
+--gpus N`` -- by re-executing itself under ``torch.distributed.run`` with N
+ranks (mailboxes over CUDA IPC / NVLink).  A step = one training iteration over
 M=32 microbatches (F + B (+W) for every microbatch, fp32 weight-gradient
 accumulation), launched as ONE graph per stage whose device dispatcher picks
 every task.  Prints one JSON line (rank 0).
@@ -101,6 +103,13 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    if args.hint == "1f1b":
+        # the reference's only wall-clock executor (live.run_live) is readiness-
+        # driven; 1F1B exists only on its virtual clock (baselines.run_fixed)
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no wall-clock 1F1B "
+                          "executor (live.run_live arbitrates; 1F1B is baselines.run_fixed, virtual)"}),
+              flush=True)
+        return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import rrfp_oracle as O
     n = max(1, args.gpus // args.tp)
@@ -135,9 +144,13 @@ def run_reference(args):
             "tokens_per_s": round(v * args.mb * 2048, 1),
             "config": workload_config(args, n),
             "cpu_baseline": {"value": round(v, 4), "unit": "iter/s", "cores": cores, "kind": "port",
+                             "os_cpu_count": os.cpu_count(), "sched_affinity": len(os.sched_getaffinity(0)),
                              "sample": f"oracle.run_live: {3 * n} threads (GIL-bound; host has "
                                        f"{len(os.sched_getaffinity(0))} cores), {n}x{args.mb} tasks, "
-                                       f"task durations = B200-measured GPT-1.3B per-task times"},
+                                       f"task durations = B200-measured GPT-1.3B per-task times "
+                                       f"(profiles/task_times_gpt1p3b.json, this bench's kernels); what "
+                                       f"differs from our arm is the runtime: Python threads + queues vs "
+                                       f"device lanes"},
             "e2e": {"value": round(v, 4), "unit": "iter/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -214,7 +227,7 @@ def workload_config(args, n):
 
 # ------------------------------------------------------------------ our arm
 def roofline_gemm_calls(cfg):
-    """One layer's ten F/B/W GEMMs, shapes and epilogues exactly as the stage
+    """One layer's twelve F/B/W GEMMs, shapes and epilogues exactly as the stage
     bodies issue them: [(fn, flops), ...] (also used by tools/prof_gemm.py)."""
     import torch
     from paper_2605_18750_b200 import kernels as K
@@ -228,6 +241,7 @@ def roofline_gemm_calls(cfg):
     qkv, y, pre, act = (torch.empty(S, 3 * D, device=dev, dtype=bf), torch.empty(S, D, device=dev, dtype=bf),
                         torch.empty(S, Fd, device=dev, dtype=bf), torch.empty(S, Fd, device=dev, dtype=bf))
     gq, g1, g2 = torch.zeros(3 * D, D, device=dev), torch.zeros(Fd, D, device=dev), torch.zeros(D, Fd, device=dev)
+    go, dx = torch.zeros(D, D, device=dev), torch.empty(S, D, device=dev, dtype=bf)
     return [
         (lambda: K.gemm(x, w_qkv, qkv, bias=bias[:3 * D]), 2 * S * D * 3 * D),
         (lambda: K.gemm(x, w_o, y, epi=K.EPI_RESID, bias=bias[:D], r=x), 2 * S * D * D),
@@ -239,12 +253,16 @@ def roofline_gemm_calls(cfg):
         (lambda: K.gemm(x, act, g2, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * Fd),
         (lambda: K.gemm(pre, x, g1, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * Fd),
         (lambda: K.gemm(qkv, x, gq, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * 3 * D),
+        # attention out-projection backward: dgrad dY.W_o and wgrad dY^T.O (the 2048^3 shapes)
+        (lambda: K.gemm(y, w_o, dx, b_mn=True), 2 * S * D * D),
+        (lambda: K.gemm(y, x, go, epi=K.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True), 2 * S * D * D),
     ]
 
 
 def gemm_roofline(cfg, peak_tf):
     """Time the dominant kernel (the stage GEMMs) with CUDA events on its own
-    launch stream, shapes and epilogues exactly as one layer's F/B/W issue them."""
+    launch stream, shapes and epilogues exactly as one layer's F/B/W issue them.
+    Timed alone (10 back-to-back reps), so ``peak_tf`` is the BURST peak."""
     import torch
     calls = roofline_gemm_calls(cfg)
     st = torch.cuda.Stream()
@@ -264,6 +282,17 @@ def gemm_roofline(cfg, peak_tf):
     ms = e0.elapsed_time(e1) / (reps * len(calls))
     flops = sum(f for _, f in calls) / len(calls)
     achieved = flops / (ms * 1e-3) / 1e12
+    # per shape (each GEMM alone, same stream): the small 2048^3 ones are the weak spot
+    per = []
+    with torch.cuda.stream(st):
+        for fn, f in calls:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            for _ in range(5):
+                fn()
+            b.record(st)
+            st.synchronize()
+            per.append(round(f / (a.elapsed_time(b) / 5 * 1e-3) / 1e12, 1))
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
@@ -276,9 +305,10 @@ def gemm_roofline(cfg, peak_tf):
             "kernel": "gemm_bf16_sm100_pair (cta_group::2 tcgen05.mma 256x256x16; clusters of two CTA pairs "
                       "sharing A by TMA multicast; half-width last wave; TMA 6-stage ring, TMEM x2, "
                       "TMA-store / reduce-add epilogue)",
-            "per_launch": f"mean over one layer's 10 F/B/W GEMMs ({cfg.seq} tokens, d={cfg.d_model}, "
+            "per_launch": f"mean over one layer's 12 F/B/W GEMMs ({cfg.seq} tokens, d={cfg.d_model}, "
                           f"ffn={cfg.d_ff}); CUDA events on the launch stream, 10 reps, in this process "
-                          "after the timed region",
+                          "after the timed region (isolated: burst peak)",
+            "per_gemm_tflops": per,
             "share_of_step": "74.5% of device time (profiles/r01_bench_launches_summary_r1end.txt, ncu launch list)",
             "avg_launch_us": round(ms * 1e3, 1)}
 
@@ -380,9 +410,10 @@ def run_ours(args):
             xs = [e.t_end - e.t_start for e in execs if e.direction == d and e.stage == s_]
             per.append(round(sum(xs) / len(xs), 1) if xs else 0.0)
         task_us[d] = per
-    roof = gemm_roofline(cfg, peak_sus)
+    roof = gemm_roofline(cfg, peak_burst)
     _log("roofline done")
-    roof["peak_kind"] = f"bf16_tflops_sustained ({peak_kind})"
+    roof["peak_kind"] = f"bf16_tflops burst ({peak_kind}): the GEMMs are timed alone, back to back"
+    roof["frac_vs_sustained"] = round(roof["achieved"] / peak_sus, 3)
     it_flops = iteration_flops(args, cfg)
     n_dev = max(1, world)
     act = cfg.seq * cfg.d_model * 2
@@ -423,6 +454,8 @@ def run_ours(args):
             line["pipeline_model"] = pipeline_model(args, cfg, task_us, n)
         except Exception as e:   # a model table must never cost the measurement
             line["pipeline_model"] = {"error": repr(e)[:200]}
+    if dist:
+        line["p2p"] = p2p_block(pipe, cfg, args, dist, world, clock_cal)
     pipe.close()
     del pipe, stages, inputs
     import gc
@@ -564,14 +597,14 @@ def emulated_pp(args, cfg):
     from paper_2605_18750_b200.workload import CommDelay
     N = args.emulate_pp
     cap = (torch.cuda.get_device_properties(0).multi_processor_count // N) & ~1
-    sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
+    combos = jitter_combos(args)
     out = {"n_stages": N, "gemm_sm_cap": cap, "green_partitions": bool(args.green),
            "definition": emulated_pp.__doc__.split("\n\n")[0].replace("\n", " ").replace("    ", " "),
            "variants": {}}
     cur = torch.cuda.current_stream()
     for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
         t0 = time.perf_counter()
-        pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[args.compare_jitter],
+        pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[combos[0][0]],
                            head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split,
                            green=args.green, split=stage_split(args))
         out["gemm_sm_cap"] = getattr(pipe, "green_sms", cap) if args.green else cap
@@ -580,7 +613,8 @@ def emulated_pp(args, cfg):
             pipe.step()
         nominal = pipe.nominal_us()
         pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
-        for sigma in sigmas:
+        for jname, sigma in combos:
+            pipe.group.set_jitter(PRESETS[jname])
             comm = CommDelay()
             if sigma > 0:
                 comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
@@ -604,23 +638,23 @@ def emulated_pp(args, cfg):
             if args.trace_dir:
                 os.makedirs(args.trace_dir, exist_ok=True)
                 tr.dump_jsonl(os.path.join(args.trace_dir, f"pp{N}_{name}_sigma{sigma}.jsonl"))
-            out["variants"][f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
+            out["variants"][f"{name}@{jname}+sigma{sigma}"] = {
                 "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
                 "bubble_fraction": round(met.bubble_fraction(), 4), "build_s": round(build_s, 1),
                 "dispatch": dispatch_latency(tr, N),
                 # all N stages share this GPU's power budget: a schedule that keeps
                 # more stages busy runs at a lower SM clock than on N separate GPUs
                 "sm_mhz": clk.summary()["sm_mhz"]}
-            _log(f"emulated PP={N} {name} sigma={sigma}: {ms:.1f} ms")
+            _log(f"emulated PP={N} {name} {jname} sigma={sigma}: {ms:.1f} ms")
         pipe.close()
         del pipe
         gc.collect()
         torch.cuda.empty_cache()
     v = out["variants"]
-    for sigma in sigmas:
-        base = v.get(f"1f1b@{args.compare_jitter}+sigma{sigma}")
+    for jname, sigma in combos:
+        base = v.get(f"1f1b@{jname}+sigma{sigma}")
         for name in ("bf", "bfw"):
-            x = v.get(f"{name}@{args.compare_jitter}+sigma{sigma}")
+            x = v.get(f"{name}@{jname}+sigma{sigma}")
             if base and x:
                 x["speedup_vs_1f1b"] = round(base["ms"] / x["ms"], 4)
                 if base.get("sm_mhz") and x.get("sm_mhz"):
@@ -669,6 +703,18 @@ def timed_steps(pipe, steps, dist, barrier):
     return ms
 
 
+def jitter_combos(args):
+    """(J-preset, sigma) operating points of the comparison runs: the first
+    --compare-jitter preset at every --sigmas value (0 always included), each
+    further preset at the largest sigma (default: J0 x {0, 0.5} + J3 x 0.5,
+    the regime SURVEY 6.3 puts the >= 1.5x target in)."""
+    js = [j for j in args.compare_jitter.split(",") if j]
+    sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
+    out = [(js[0], sg) for sg in sigmas]
+    out += [(j, sigmas[-1]) for j in js[1:]]
+    return out
+
+
 def compare_variants(cfg, args, world, dist, barrier):
     """Same kernels, same box: fixed-order 1F1B vs RRFP (BF, BFW) under the
     J-preset jitter table (--compare-jitter) and injected lognormal compute +
@@ -682,8 +728,8 @@ def compare_variants(cfg, args, world, dist, barrier):
     from paper_2605_18750_b200.jitter import PRESETS
     from paper_2605_18750_b200.workload import CommDelay
     out = {}
-    sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
-    jit = PRESETS[args.compare_jitter]
+    combos = jitter_combos(args)
+    jit = PRESETS[combos[0][0]]
     for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
         if name == "1f1b" and args.chunks > 1:
             continue          # 1F1B is undefined for interleaved chunks (baselines.py:72-75)
@@ -696,7 +742,8 @@ def compare_variants(cfg, args, world, dist, barrier):
             pipe.step()
         nominal = pipe.nominal_us()
         pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
-        for sigma in sigmas:
+        for jname, sigma in combos:
+            pipe.group.set_jitter(PRESETS[jname])
             comm = CommDelay()
             if sigma > 0:
                 comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
@@ -706,26 +753,138 @@ def compare_variants(cfg, args, world, dist, barrier):
             pipe.step()
             ms = timed_steps(pipe, args.steps, dist, barrier)
             tr, met = gather_trace(pipe, dist, world)
-            out[f"{name}@{args.compare_jitter}+sigma{sigma}"] = {
-                "iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
-                "bubble_fraction": round(met.bubble_fraction(), 4)}
+            key = f"{name}@{jname}+sigma{sigma}"
+            out[key] = {"iter_s": round(1000.0 / ms, 4), "ms": round(ms, 2),
+                        "tokens_per_s": round(1000.0 / ms * args.mb * cfg.seq, 1),
+                        "bubble_fraction": round(met.bubble_fraction(), 4)}
             if not dist or dist.get_rank() == 0:   # (rank 0 holds the gathered trace)
                 from paper_2605_18750_b200.runtime import dispatch_latency
-                out[f"{name}@{args.compare_jitter}+sigma{sigma}"]["dispatch"] = \
-                    dispatch_latency(tr, pipe.workload.num_stages)
-            _log(f"variant {name} {args.compare_jitter} sigma={sigma}: {ms:.1f} ms")
+                out[key]["dispatch"] = dispatch_latency(tr, pipe.workload.num_stages)
+            _log(f"variant {name} {jname} sigma={sigma}: {ms:.1f} ms")
         pipe.close()
         del pipe, stages
         gc.collect()
         torch.cuda.empty_cache()
-    for sigma in sigmas:
-        base = out.get(f"1f1b@{args.compare_jitter}+sigma{sigma}")
+    for jname, sigma in combos:
+        base = out.get(f"1f1b@{jname}+sigma{sigma}")
         if base:
             for name in ("bf", "bfw"):
-                v = out.get(f"{name}@{args.compare_jitter}+sigma{sigma}")
+                v = out.get(f"{name}@{jname}+sigma{sigma}")
                 if v:
                     v["speedup_vs_1f1b"] = round(base["ms"] / v["ms"], 4)
     return out
+
+
+def p2p_block(pipe, cfg, args, dist, world, clock_cal):
+    """NVLink evidence of the N>1 run (rank 0 reports, every rank measures):
+    the mailbox store of one [S, D] bf16 activation (8 MiB at 1.3B) into the
+    NEXT stage's slot on the peer GPU vs into a local buffer (our copy kernel,
+    CUDA events, 20 reps), the FC2 GEMM with its epilogue writing the peer
+    mailbox vs a local output (the fused K1 path), the device flag round trip
+    (clock ping-pong), and the TP all-reduce (R-1 peer partials per call)."""
+    import ctypes as C
+    import torch
+    from paper_2605_18750_b200 import _lib
+    from paper_2605_18750_b200 import kernels as K
+    L = _lib.lib()
+    S, D, Fd = cfg.seq, cfg.d_model, cfg.d_ff
+    st = pipe.vstages[0]
+    out = {"rank": dist.get_rank()}
+    stream = torch.cuda.current_stream()
+    try:
+        _p2p_measure(out, pipe, st, L, K, S, D, Fd, stream, dist, clock_cal)
+    except Exception as e:       # a probe must never cost the run (or hang the gather)
+        out["error"] = repr(e)[:200]
+    allv = [None] * world
+    dist.all_gather_object(allv, out)
+    return allv
+
+
+def _p2p_measure(out, pipe, st, L, K, S, D, Fd, stream, dist, clock_cal):
+    import ctypes as C
+    import torch
+    from paper_2605_18750_b200 import _lib
+
+    def timeit(fn, reps=20):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e-3
+
+    if st.fwd_out is not None:
+        peer = st.fwd_out[0][0]
+        src = torch.randn(S, D, device="cuda").to(torch.bfloat16)
+        local = torch.empty_like(src)
+        nbytes = S * D * 2
+
+        def cp(dst):
+            return lambda: _lib.check(L.rrfp_copy_rows(C.c_void_p(dst.data_ptr()), C.c_longlong(D * 2),
+                                                       C.c_void_p(src.data_ptr()), C.c_longlong(D * 2), S,
+                                                       C.c_longlong(D * 2), C.c_void_p(stream.cuda_stream)))
+        tp_, tl = timeit(cp(peer)), timeit(cp(local))
+        out["mailbox_copy"] = {"bytes": nbytes, "peer_gbs": round(nbytes / tp_ / 1e9, 1),
+                               "local_gbs": round(nbytes / tl / 1e9, 1), "peer_us": round(tp_ * 1e6, 1)}
+        act = torch.randn(S, Fd, device="cuda").to(torch.bfloat16)
+        w2 = torch.randn(D, Fd, device="cuda").to(torch.bfloat16)
+        bias = torch.zeros(D, device="cuda").to(torch.bfloat16)
+        gp = timeit(lambda: K.gemm(act, w2, peer, epi=K.EPI_RESID, bias=bias, r=src), 10)
+        gl = timeit(lambda: K.gemm(act, w2, local, epi=K.EPI_RESID, bias=bias, r=src), 10)
+        out["fc2_epilogue_to_mailbox"] = {"peer_us": round(gp * 1e6, 1), "local_us": round(gl * 1e6, 1),
+                                          "tflops_peer": round(2 * S * D * Fd / gp / 1e12, 1)}
+    if clock_cal:
+        out["flag_round_trip_ns_best"] = clock_cal["best_rtt_ns"]
+    comm = getattr(pipe, "comm", None)
+    if comm is not None:
+        dst = torch.empty(S, D, device="cuda").to(torch.bfloat16)
+        dist.barrier()
+        t = timeit(lambda: comm.allreduce([dst]), 20)
+        moved = (comm.size - 1) * S * D * 2
+        out["tp_allreduce"] = {"us": round(t * 1e6, 1), "peer_read_gbs": round(moved / t / 1e9, 1),
+                               "bytes_peer_per_call": moved}
+
+
+def scheduler_baseline(task_us, n_meas, args, device="cuda"):
+    """SURVEY 8d CPU item (i): the reference's virtual-clock schedulers
+    (engine.run_rrfp, baselines.run_fixed -- the oracle's restatement, one
+    core) vs the device replay kernel on IDENTICAL tables built from this
+    run's measured per-task times, PP 4/8 x M 16/32; microseconds per task."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rrfp_oracle as O
+    import paper_2605_18750_b200 as P
+    f_tot = sum(task_us["F"])
+    b_tot = sum(task_us["B"])
+    out = []
+    for n in (4, 8):
+        for m in (16, 32):
+            lat = {}
+            for s_ in range(n):
+                for mb in range(m):
+                    lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(f_tot / n))
+                    lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(b_tot / n))
+            w = P.Workload(num_stages=n, num_microbatches=m, num_chunks=1, tp_group_size=1, latency=lat)
+            ow = O.from_workload_json(w.to_json())
+            tasks = w.task_count()
+            row = {"pp": n, "mb": m, "tasks": tasks}
+            for name, fn in (("run_rrfp_cpu", lambda: O.run_rrfp(ow, "bf", 32, 0, "J3")),
+                             ("run_fixed_cpu", lambda: O.run_fixed(O.one_f_one_b(ow), ow)),
+                             ("replay_kernel_gpu", lambda: P.run_rrfp(w, "bf", 32, 0,
+                                                                      jitter=P.JITTER_PRESETS["J3"],
+                                                                      device=device))):
+                fn()
+                k, t0 = 0, time.perf_counter()
+                while time.perf_counter() - t0 < 0.5 or k < 2:
+                    fn()
+                    k += 1
+                row[name + "_us_per_task"] = round((time.perf_counter() - t0) / k / tasks * 1e6, 2)
+            out.append(row)
+    return {"definition": scheduler_baseline.__doc__.split("\n\n")[0].strip().replace("\n", " "),
+            "note": "replay_kernel_gpu includes the table upload and the event read-back per call",
+            "rows": out}
 
 
 def cpu_baseline(args, n, task_us):
@@ -750,9 +909,46 @@ def cpu_baseline(args, n, task_us):
         O.run_live(w, hint, 32, 1.0, seed=0)
         k += 1
     dt = (time.perf_counter() - t0) / k
-    return {"value": round(1.0 / dt, 4), "unit": "iter/s", "cores": 3 * n, "kind": "port",
-            "sample": f"{k} iterations of oracle.run_live ({3 * n} threads, GIL-bound) on this run's "
-                      f"measured per-task times, PP={n}, M={args.mb}"}
+    out = {"value": round(1.0 / dt, 4), "unit": "iter/s", "cores": 3 * n, "kind": "port",
+           "os_cpu_count": os.cpu_count(), "sched_affinity": len(os.sched_getaffinity(0)),
+           "sample": f"{k} iterations of oracle.run_live ({3 * n} threads, GIL-bound) on this run's "
+                     f"measured per-task times, PP={n}, M={args.mb}"}
+    try:
+        out["scheduler"] = scheduler_baseline(task_us, n, args)
+    except Exception as e:     # never cost the measurement
+        out["scheduler"] = {"error": repr(e)[:200]}
+    return out
+
+
+def reexec_torchrun(n):
+    """``python bench.py --gpus N`` (no torchrun): one process per GPU, launched
+    the way the driver launches the N > 1 runs; returns the exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    _log(f"re-exec under torchrun: {n} ranks")
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args):
+    """The launch plan every rank resolved (rendezvous over gloo when N > 1)."""
+    rank, world, local = dist_env()
+    plan = {"n_gpus": world, "pp": world // args.tp if world > 1 else 1, "tp": args.tp,
+            "chunks": args.chunks, "impl": args.impl, "rank_to_stage":
+            [[r // args.tp, r % args.tp] for r in range(world)], "dry_run": True}
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        allp = [None] * world
+        dist.all_gather_object(allp, {"rank": rank, "local_rank": local})
+        plan["ranks"] = allp
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(plan), flush=True)
 
 
 def main():
@@ -779,8 +975,9 @@ def main():
     ap.add_argument("--sigmas", default="0.5",
                     help="comma list of lognormal compute+comm jitter sigmas of the comparison runs "
                          "(config 5 sweep: 0,0.1,0.2,0.3,0.4,0.5); sigma 0 is always included")
-    ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0",
-                    help="J-preset jitter table (jitter.py PRESETS) applied to every comparison variant")
+    ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0,J3",
+                    help="comma list of J-preset jitter tables (jitter.py PRESETS) for the comparison runs: "
+                         "the first at every --sigmas value, the others at the largest sigma")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)
     ap.add_argument("--w-split", dest="w_split", default="fc", choices=["fc", "all"],
                     help="BFW: weight gradients deferred to the W task (fc: FC1/FC2; all: all four)")
@@ -794,7 +991,19 @@ def main():
     ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "
                          "1F1B vs BF vs BFW at every --sigmas (default 8; 0 = off)")
+    ap.add_argument("--dry-run", dest="dry_run", action="store_true",
+                    help="resolve the launch (re-exec under torchrun for --gpus N > 1, rendezvous) and "
+                         "print the plan; no CUDA")
     args = ap.parse_args()
+    rank, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.emulate_only and \
+            (args.impl == "ours" or args.dry_run):
+        sys.exit(reexec_torchrun(args.gpus))
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; one process per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus})")
+    if args.dry_run:
+        return dry_run(args)
     if args.emulate_only:
         import torch
         torch.cuda.set_device(0)

@@ -250,6 +250,12 @@ class LaneGroup:
                                                       _ptr(floor) if floor is not None else None))
         self.w = w
 
+    def set_jitter(self, jitter: JitterConfig | None):
+        """Switch the J-preset injection table (jitter.py:97-118) between
+        iterations, keeping the current latencies (real-body lanes)."""
+        self._jitter = jitter
+        self.set_latency(self.w.latency)
+
     def set_latency(self, latency: dict):
         """Replace the workload's nominal per-task latencies (e.g. the measured
         task times of the real bodies) and re-derive the J-preset jitter pads

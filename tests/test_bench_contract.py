@@ -62,3 +62,46 @@ def test_dispatch_latency_from_trace():
     d = dispatch_latency(tr, 2)
     assert d["back_to_back_gap_us"]["n"] == 2 and d["back_to_back_gap_us"]["p50"] == 25
     assert d["arrival_to_start_us"] == {"p50": 10, "p90": 10, "n": 1}
+
+
+def _json_line(p):
+    return json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+
+
+def test_gpus_n_is_self_sufficient_on_cpu():
+    """`python bench.py --gpus 2` without torchrun: our arm re-executes itself
+    under torch.distributed.run with 2 ranks (dry run: rendezvous + plan, no
+    CUDA) and the reference arm runs PP=2 on rank 0."""
+    env = dict(os.environ, RRFP_SAME_DEVICE="1")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    plan = _json_line(p)
+    assert plan["n_gpus"] == 2 and plan["pp"] == 2 and len(plan["ranks"]) == 2
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0", "--mb", "4"], capture_output=True, text=True,
+                       timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = _json_line(p)
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "pp2"
+    assert line["cpu_baseline"]["os_cpu_count"] >= 1
+
+
+def test_world_size_mismatch_fails_loudly():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert p.returncode != 0 and "WORLD_SIZE=2" in p.stderr
+
+
+def test_reference_arm_refuses_1f1b():
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--hint", "1f1b",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0 and "unavailable" in _json_line(p)
+
+
+def test_jitter_combos_default_includes_j3():
+    sys.path.insert(0, ROOT)
+    import bench
+    args = argparse.Namespace(compare_jitter="J0,J3", sigmas="0.5")
+    assert bench.jitter_combos(args) == [("J0", 0.0), ("J0", 0.5), ("J3", 0.5)]
