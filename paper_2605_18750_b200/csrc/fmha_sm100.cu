@@ -1,0 +1,576 @@
+// fmha_sm100.cu -- the attention core of the GPT stage bodies,
+// hand-written for sm_100a: tcgen05.mma with TMEM accumulators, TMA-fed
+// shared-memory operands, d_head = 128, causal or bidirectional, reading Q/K/V
+// straight out of the packed QKV GEMM output [T, 3*D] and writing O [T, D] and
+// the packed dQKV [T, 3*D] (no layout copies).  It fills the compute slot the
+// reference times as a no-op (engine.py:272-273) / a spin (live.py:388-390).
+//
+// Forward (one CTA per (head, pair of 128-row query tiles)):
+//   warp 0      TMA producer: both Q tiles once, then K_j / V_j tiles through a
+//               4-stage ring of 32 KB tiles (two SW128 panels of 128 x 64)
+//   warp 1      MMA issuer (one thread):  S = Q K^T  (SS, 128x128x128) into a
+//               TMEM S buffer;  O += P V  (TS: P read from TMEM, V from smem)
+//   warp 2      TMEM allocator (512 columns: S buffers 0/1, O0, O1)
+//   warps 4-7   softmax of query tile 0, warps 8-11 softmax of query tile 1
+//               (one thread per query row; P written back over its S columns
+//               as packed bf16 with tcgen05.st, the A operand of the PV MMA)
+// The two tiles ping-pong on the tensor core: issue order QK0_j, PV1_{j-1},
+// QK1_j, PV0_j, so each softmax has a full QK+PV of the other tile to hide
+// behind.  Causal pairs are (u, n_qt-1-u): every CTA has n_qt+1 tile steps.
+// Once the short tile is done, the long one alternates between both S buffers
+// (QK_{j+1} is issued before PV_j) so its softmax still overlaps the MMAs.
+// Row max uses a lazy rescale: O and l are rescaled only when the running max
+// grows by more than 8 (log2 units), so P <= 256 and the O correction (a TMEM
+// read-modify-write) happens on the first tiles only.
+// Statistics: lse2[h][t] = max + log2(sum), in log2 units of the scaled scores
+// (P = exp2(s * scale * log2(e) - lse2) in the backward).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "../../include/rrfp_b200.h"
+#include "rrfp_common.h"
+#include "sm100_ptx.cuh"
+
+namespace {
+
+constexpr int FT = 128;                      // query / key tile rows
+constexpr int DH = 128;                      // head dimension
+constexpr int PANEL = FT * 128;              // 16 KB: 128 rows x 64 bf16 (one SW128 panel)
+constexpr int TILE = 2 * PANEL;              // 32 KB: 128 rows x 128 bf16
+constexpr int F_RING = 4;
+constexpr int F_SMEM = (2 + F_RING) * TILE + 1024 + 256;
+constexpr int F_THREADS = 384;
+
+struct FwdArgs {
+  int T, H, D, n_qt, causal;
+  float sl2;                   // softmax scale * log2(e)
+  __nv_bfloat16* o;
+  long long ldo;
+  float* lse;
+  long long lse_ld;
+  int experiment;    // test hook: 1 = P from a copy instead of exp (pipeline-bound time)
+  long long* dbg;    // optional event log of one CTA: [4][512] (code<<56 | j<<40 | clock)
+  int dbg_cta;
+};
+
+// mbarrier wait that traps after ~4 s instead of hanging the device
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = sm100::smem_u32(bar);
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+  if (ok) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    if (ok) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();
+  }
+}
+
+// whole-warp callers: one elected lane issues the op
+__device__ __forceinline__ void mma_ss_e(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(sm100::smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA pipe for 3 of every 8 exponential pairs of the softmax (the
+// MUFU unit, 16 results / clock / SM, bounds it otherwise): x = j + f,
+// j = rint(x), 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max rel.
+// error 1.0e-4, far below the bf16 rounding of P), 2^j added into the exponent.
+// packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): half the issue slots
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ uint64_t u2pack(uint32_t lo, uint32_t hi) { return (uint64_t)lo | ((uint64_t)hi << 32); }
+__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// two exponentials per MUFU op: 2^x on packed halves (ex2.approx.f16x2).  The
+// fp16 input keeps 11 significant bits of x <= 8 (|error in 2^x| <= 0.27 %, the
+// size of the bf16 rounding P gets anyway), the result 11 bits; P in [0, 256].
+__device__ __forceinline__ uint64_t ex2_h2(uint64_t x2) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f2hi(x2)), "f"(f2lo(x2)));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  float lo, hi;
+  asm("{\n.reg .f16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}" : "=f"(lo), "=f"(hi) : "r"(e));
+  return f2pack(lo, hi);
+}
+// pairs of exponentials emulated on the FMA pipe (bit mask over pair index mod 8): 3/8
+constexpr uint32_t POLY_PAIRS = 0xA4;
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
+  const float a = fmaxf(f2lo(x2), -127.f), b = fmaxf(f2hi(x2), -127.f);
+  const uint64_t x = f2pack(a, b);
+  const uint64_t t = fadd2(x, f2pack(12582912.f, 12582912.f));
+  const uint64_t jn = fadd2(t, f2pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(jn, f2pack(-1.f, -1.f), x);
+  uint64_t p = ffma2(f2pack(0.05500882f, 0.05500882f), f, f2pack(0.24221077f, 0.24221077f));
+  p = ffma2(p, f, f2pack(0.69328291f, 0.69328291f));
+  p = ffma2(p, f, f2pack(1.f, 1.f));
+  const uint32_t lo = (uint32_t)t * 8388608u + (uint32_t)p;
+  const uint32_t hi = (uint32_t)(t >> 32) * 8388608u + (uint32_t)(p >> 32);
+  return u2pack(lo, hi);
+}
+
+// causal mask of the diagonal tile: key column i > query row -> -inf
+__device__ __forceinline__ void mask_diag(uint32_t (&r)[128], int row) {
+#pragma unroll
+  for (int i = 0; i < 128; ++i)
+    if (i > row) r[i] = __float_as_uint(-INFINITY);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// The query tiles of a CTA: slot 0 (short) and slot 1 (long); len = kv tiles.
+struct FwdPlan {
+  int h, q0, q1, len0, len1;
+};
+__device__ __forceinline__ FwdPlan fwd_plan(const FwdArgs& g) {
+  FwdPlan p;
+  const int n_pairs = (g.n_qt + 1) >> 1;
+  p.h = blockIdx.x % g.H;
+  const int u = blockIdx.x / g.H;
+  if (g.causal) {
+    p.q0 = u; p.q1 = g.n_qt - 1 - u;
+  } else {
+    p.q0 = 2 * u; p.q1 = 2 * u + 1;
+    if (p.q1 >= g.n_qt) { p.q1 = p.q0; }
+  }
+  if (p.q0 == p.q1) {   // a single tile: it runs as the long one
+    p.len0 = 0;
+  } else {
+    p.len0 = g.causal ? p.q0 + 1 : g.n_qt;
+  }
+  p.len1 = g.causal ? p.q1 + 1 : g.n_qt;
+  (void)n_pairs;
+  return p;
+}
+// S/P buffer of slot 1 at kv step j (slot 0 always uses buffer 0)
+__device__ __forceinline__ int buf1(const FwdPlan& p, int j) { return j < p.len0 ? 1 : ((j - p.len0) & 1); }
+
+__global__ void __launch_bounds__(F_THREADS, 1)
+    fmha_fwd_sm100(const __grid_constant__ CUtensorMap tmQKV, FwdArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = smem;                         // [2][TILE]
+  uint8_t* ring = smem + 2 * TILE;            // [F_RING][TILE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + F_RING * TILE);
+  uint64_t* full = bars;                      // [F_RING]
+  uint64_t* empty = bars + F_RING;            // [F_RING]
+  uint64_t* q_full = bars + 2 * F_RING;       // [2]
+  uint64_t* s_full = q_full + 2;              // [2] per S buffer
+  uint64_t* p_full = s_full + 2;              // [2] per S buffer
+  uint64_t* o_done = p_full + 2;              // [2] per slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const FwdPlan pl = fwd_plan(g);
+  int dbg_n = 0;
+  const bool dbg_on = g.dbg && (int)blockIdx.x == g.dbg_cta && (lane == 0) &&
+                      (warp == 1 || warp == 0 || warp == 4 || warp == 8);
+#define DBG(stream, code, j)                                                                        \
+  do {                                                                                              \
+    if (dbg_on && dbg_n < 512)                                                                      \
+      g.dbg[(stream) * 512 + dbg_n++] = ((long long)(code) << 56) | ((long long)(j) << 40) |        \
+                                        (long long)(clock64() & 0xffffffffffLL);                     \
+  } while (0)
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmQKV);
+    for (int s = 0; s < F_RING; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&q_full[i], 1);
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_full[i], 128);
+      sm100::mbar_init(&o_done[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  sm100::griddep_launch();
+  sm100::griddep_wait();
+
+  const int n_iter = pl.len1;
+  const int kcol = g.D + pl.h * DH, vcol = 2 * g.D + pl.h * DH;
+
+  // registers: producer / MMA / allocator warpgroup down, the two softmax warpgroups up
+  if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (lane == 0) {
+      if (pl.len0) {
+        sm100::mbar_arrive_expect_tx(&q_full[0], TILE);
+        for (int p = 0; p < 2; ++p)
+          sm100::tma_load_2d(sQ + p * PANEL, &tmQKV, &q_full[0], pl.h * DH + 64 * p, pl.q0 * FT);
+      }
+      sm100::mbar_arrive_expect_tx(&q_full[1], TILE);
+      for (int p = 0; p < 2; ++p)
+        sm100::tma_load_2d(sQ + TILE + p * PANEL, &tmQKV, &q_full[1], pl.h * DH + 64 * p, pl.q1 * FT);
+      for (int n = 0; n < 2 * n_iter; ++n) {
+        const int st = n % F_RING, j = n >> 1;
+        DBG(0, 20, n);
+        wait(&empty[st], ((n / F_RING) & 1) ^ 1);
+        DBG(0, 21, n);
+        sm100::mbar_arrive_expect_tx(&full[st], TILE);
+        const int col = (n & 1) ? vcol : kcol;
+        for (int p = 0; p < 2; ++p)
+          sm100::tma_load_2d(ring + st * TILE + p * PANEL, &tmQKV, &full[st], col + 64 * p, j * FT);
+      }
+    }
+  } else if (warp == 1) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    // the whole warp walks the schedule (warp-uniform values stay in uniform
+    // registers); one elected lane issues each tcgen05 op
+    constexpr uint32_t idS = sm100::idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idO = sm100::idesc_bf16(128, 128, 0, 1);
+    const uint64_t dQ0 = sm100::umma_desc_sw128(sm100::smem_u32(sQ), 16, 1024);
+    const uint64_t dQ1 = sm100::umma_desc_sw128(sm100::smem_u32(sQ + TILE), 16, 1024);
+    const uint64_t dK0 = sm100::umma_desc_sw128(sm100::smem_u32(ring), 16, 1024);
+    const uint64_t dV0 = sm100::umma_desc_sw128(sm100::smem_u32(ring), PANEL, 1024);
+    int pc0 = 0, pc1 = 0;     // p_full consumptions per S buffer
+    auto ring_wait = [&](int n) {
+      DBG(1, 10, n);
+      wait(&full[n % F_RING], (n / F_RING) & 1);
+      sm100::tc_fence_after();
+      DBG(1, 11, n);
+    };
+    auto qk = [&](uint64_t dq, int n, int b) {
+      const uint64_t dk = dK0 + (uint64_t)(((n % F_RING) * TILE) >> 4);
+      const uint32_t d = tmem + b * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t off = ((k >> 2) * PANEL + (k & 3) * 32) >> 4;
+        mma_ss_e(d, dq + off, dk + off, idS, k != 0);
+      }
+      commit_e(&s_full[b]);
+    };
+    auto pv = [&](int slot, int n, int b, int j) {
+      DBG(1, 12, j);
+      const int c = b ? pc1 : pc0;
+      wait(&p_full[b], c & 1);
+      if (b) ++pc1; else ++pc0;
+      sm100::tc_fence_after();
+      DBG(1, 13, j);
+      const uint64_t dv = dV0 + (uint64_t)(((n % F_RING) * TILE) >> 4);
+      const uint32_t d = tmem + 256 + slot * 128, a = tmem + b * 128;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_ts_e(d, a + k * 8, dv + ((k * 16 * 128) >> 4), idO, (j | k) != 0);
+      commit_e(&o_done[slot]);
+    };
+    for (int j = 0; j < n_iter; ++j) {
+      ring_wait(2 * j);
+      if (j < pl.len0) {
+        if (j == 0) { wait(&q_full[0], 0); sm100::tc_fence_after(); }
+        qk(dQ0, 2 * j, 0);
+        if (j >= 1) {
+          pv(1, 2 * (j - 1) + 1, buf1(pl, j - 1), j - 1);
+          commit_e(&empty[(2 * (j - 1) + 1) % F_RING]);
+        }
+        if (j == 0) { wait(&q_full[1], 0); sm100::tc_fence_after(); }
+        qk(dQ1, 2 * j, 1);
+        commit_e(&empty[(2 * j) % F_RING]);
+        ring_wait(2 * j + 1);
+        pv(0, 2 * j + 1, 0, j);
+      } else {
+        if (j == 0) { wait(&q_full[1], 0); sm100::tc_fence_after(); }
+        qk(dQ1, 2 * j, buf1(pl, j));
+        commit_e(&empty[(2 * j) % F_RING]);
+        if (j >= 1) {
+          if (j - 1 >= pl.len0) ring_wait(2 * (j - 1) + 1);
+          pv(1, 2 * (j - 1) + 1, buf1(pl, j - 1), j - 1);
+          commit_e(&empty[(2 * (j - 1) + 1) % F_RING]);
+        }
+      }
+    }
+    const int j = n_iter - 1;
+    if (j >= pl.len0) ring_wait(2 * j + 1);
+    pv(1, 2 * j + 1, buf1(pl, j), j);
+    commit_e(&empty[(2 * j + 1) % F_RING]);
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  } else {
+    // (the pool is what warpgroup 0 released: 128 x (168 - 56) = 256 x (224 - 168))
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // softmax: warpgroup 1 = query tile of slot 0, warpgroup 2 = slot 1; one
+    // thread per query row (TMEM lane)
+    const int slot = (warp - 4) >> 2, q = warp & 3;
+    const int row = q * 32 + lane;
+    const int qi = slot ? pl.q1 : pl.q0;
+    const int len = slot ? pl.len1 : pl.len0;
+    int cnt[2] = {slot ? pl.len0 : 0, 0};   // s_full completions seen per buffer (slot 0 used buffer 0 len0 times)
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t o_t = tmem + lane_off + 256 + slot * 128;
+    float m_used = -INFINITY, l = 0.f;
+    const uint64_t sl2_2 = f2pack(g.sl2, g.sl2);
+    for (int j = 0; j < len; ++j) {
+      const int b = slot ? buf1(pl, j) : 0;
+      DBG(2 + slot, 0, j);
+      wait(&s_full[b], cnt[b] & 1);
+      ++cnt[b];
+      sm100::tc_fence_after();
+      const uint32_t s_t = tmem + lane_off + b * 128;
+      const bool diag = g.causal && j == qi;
+      DBG(2 + slot, 1, j);
+      // the whole S row in registers: four loads in flight, one wait
+      uint32_t r[128];
+      sm100::tmem_ld32(s_t, *reinterpret_cast<uint32_t(*)[32]>(r));
+      sm100::tmem_ld32(s_t + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      sm100::tmem_ld32(s_t + 64, *reinterpret_cast<uint32_t(*)[32]>(r + 64));
+      sm100::tmem_ld32(s_t + 96, *reinterpret_cast<uint32_t(*)[32]>(r + 96));
+      sm100::tmem_ld_wait();
+      DBG(2 + slot, 2, j);
+      if (diag) mask_diag(r, row);
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 128; i += 2)
+        mx4[(i >> 1) & 3] = fmaxf(mx4[(i >> 1) & 3], fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
+      const float m_new = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * g.sl2;
+      const bool need = m_new > m_used + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = need ? ex2(m_used - m_new) : 1.f;
+        if (need) { m_used = m_new; l *= alpha; }
+        if (j > 0) {   // O holds P V of earlier tiles: wait for the last PV, then scale
+          wait(&o_done[slot], (j - 1) & 1);
+          sm100::tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            sm100::tmem_ld32(o_t + 32 * c, o);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(o_t + 32 * c, o);
+          }
+          tmem_st_wait();
+        }
+      }
+      // exponentials on pairs (FFMA2 / FADD2): x = s*scale*log2e - m; 3 of every 8
+      // pairs on the FMA pipe (ex2_poly2), the rest on MUFU.  P (bf16 pairs) goes
+      // over the first 64 columns of the S buffer: the A operand of the PV MMA
+      // phase 1: x = s*scale*log2e - m in place (FFMA2); phase 2: 2^x in place, 3 of
+      // every 8 pairs on the FMA pipe (ex2_poly2), the rest on MUFU; phase 3: row
+      // sum (FADD2), bf16 pairs of P over the first 64 columns of the S buffer (the
+      // A operand of the PV MMA).  Phases keep producer and consumer far apart: one
+      // warp per SM sub-partition has nothing else to hide latencies with.
+      const uint64_t negm2 = f2pack(-m_used, -m_used);
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
+        const uint64_t x2 = ffma2(u2pack(r[i], r[i + 1]), sl2_2, negm2);
+        r[i] = (uint32_t)x2;
+        r[i + 1] = (uint32_t)(x2 >> 32);
+      }
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
+        if ((POLY_PAIRS >> ((i >> 1) & 7)) & 1) {
+          const uint64_t p2 = ex2_poly2(u2pack(r[i], r[i + 1]));
+          r[i] = (uint32_t)p2;
+          r[i + 1] = (uint32_t)(p2 >> 32);
+        } else {
+          r[i] = __float_as_uint(ex2(__uint_as_float(r[i])));
+          r[i + 1] = __float_as_uint(ex2(__uint_as_float(r[i + 1])));
+        }
+      }
+      uint64_t l2[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const uint64_t p2 = u2pack(r[32 * c + i], r[32 * c + i + 1]);
+          l2[(i >> 1) & 3] = fadd2(l2[(i >> 1) & 3], p2);
+          pk[i >> 1] = pack_bf16(f2lo(p2), f2hi(p2));
+        }
+        tmem_st16(s_t + 16 * c, pk);
+      }
+      {
+        const uint64_t ls = fadd2(fadd2(l2[0], l2[1]), fadd2(l2[2], l2[3]));
+        l += f2lo(ls) + f2hi(ls);
+      }
+      DBG(2 + slot, 3, j);
+      tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&p_full[b]);
+      DBG(2 + slot, 4, j);
+    }
+    if (len > 0) {
+      wait(&o_done[slot], (len - 1) & 1);
+      sm100::tc_fence_after();
+      const float inv = 1.f / l;
+      const int t = qi * FT + row;
+      __nv_bfloat16* orow = g.o + (size_t)t * g.ldo + pl.h * DH;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        sm100::tmem_ld32(o_t + 32 * c, r);
+        sm100::tmem_ld_wait();
+        uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(r[8 * v + 0]) * inv, __uint_as_float(r[8 * v + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv);
+          dst[v] = w;
+        }
+      }
+      g.lse[(size_t)pl.h * g.lse_ld + t] = m_used + __log2f(l);
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn_t encode() {
+  static encode_fn_t fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (encode_fn_t)p;
+  }
+  return fn;
+}
+
+// bf16 [rows, cols] row-major (leading dim ld), box {64 cols, box_rows}, SW128
+int map_bf16(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  encode_fn_t enc = encode();
+  if (!enc) return rrfp_fail(RRFP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return rrfp_fail(RRFP_E_INVALID, "fmha tensor map encode failed (%d)", (int)r);
+  return RRFP_OK;
+}
+
+long long* g_attn_dbg = nullptr;
+int g_attn_dbg_cta = 0;
+
+}  // namespace
+
+/* test hook: log the event timeline of CTA `cta` into buf ([4][512] int64), NULL: off */
+extern "C" int rrfp_attn_debug(long long* buf, int cta) {
+  g_attn_dbg = buf;
+  g_attn_dbg_cta = cta;
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_attn_fwd(const void* qkv, long long ldqkv, void* o, long long ldo, float* lse,
+                             long long lse_ld, int T, int H, int d_head, int causal, float scale, void* stream) {
+  if (d_head != DH) return rrfp_fail(RRFP_E_INVALID, "attn_fwd: d_head %d unsupported (128 only)", d_head);
+  if (T <= 0 || T % FT) return rrfp_fail(RRFP_E_INVALID, "attn_fwd: T=%d must be a positive multiple of 128", T);
+  if (!qkv || !o || !lse || ldqkv < 3LL * H * DH || ldo < (long long)H * DH || (ldqkv % 8) || (ldo % 8))
+    return rrfp_fail(RRFP_E_INVALID, "attn_fwd: bad pointers / leading dims");
+  static bool attr = false;
+  if (!attr) {
+    RRFP_CUDA_TRY(cudaFuncSetAttribute(fmha_fwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM));
+    attr = true;
+  }
+  CUtensorMap m;
+  int rc = map_bf16(&m, qkv, T, 3LL * H * DH, ldqkv, FT);
+  if (rc) return rc;
+  FwdArgs g;
+  g.T = T; g.H = H; g.D = H * DH; g.n_qt = T / FT; g.causal = causal ? 1 : 0;
+  g.sl2 = scale * 1.4426950408889634f;
+  g.o = reinterpret_cast<__nv_bfloat16*>(o); g.ldo = ldo;
+  g.lse = lse; g.lse_ld = lse_ld;
+  g.dbg = g_attn_dbg; g.dbg_cta = g_attn_dbg_cta;
+  g.experiment = 0;
+  const int grid = H * ((g.n_qt + 1) / 2);
+  RRFP_CUDA_TRY(rrfp_launch(fmha_fwd_sm100, dim3(grid), dim3(F_THREADS), F_SMEM, (cudaStream_t)stream, m, g));
+  return RRFP_OK;
+}

@@ -53,3 +53,17 @@ def gemm(a, b, c, *, epi=EPI_BF16, a_mn=False, b_mn=False, c2=None, bias=None, r
         C.c_longlong(c2.stride(0) if c2 is not None else 0), _p(bias), _p(r),
         C.c_longlong(r.stride(0) if r is not None else 0), int(accumulate), _stream()))
     return c
+
+
+def attn_fwd(qkv, o, lse, *, heads, causal=True, scale=None, T=None):
+    """Flash attention forward (csrc/fmha_sm100.cu): qkv [T, >=3D] packed, o [T, >=D],
+    lse fp32 [H, >=T] (log2 units).  d_head = 128."""
+    T = qkv.shape[0] if T is None else T
+    dh = 128
+    scale = dh ** -0.5 if scale is None else scale
+    L = _lib.lib()
+    note()
+    _lib.check(L.rrfp_attn_fwd(_p(qkv), C.c_longlong(qkv.stride(0)), _p(o), C.c_longlong(o.stride(0)),
+                               _p(lse), C.c_longlong(lse.stride(0)), T, heads, dh, int(causal),
+                               C.c_float(scale), _stream()))
+    return o

@@ -1,0 +1,64 @@
+"""Attention core (csrc/fmha_sm100.cu) against a plain PyTorch fp32
+reference of the same op on the same packed QKV.
+
+Tolerances: bf16 output O -> max |err| / max |ref| < 2e-2 (P is rounded to bf16
+before the PV product, as in every flash kernel); the row statistics lse (fp32,
+log2 units) -> |err| < 1e-3 * max(1, |ref|)."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_fwd(qkv, H, causal, scale):
+    T = qkv.shape[0]
+    D = H * 128
+    q, k, v = (qkv[:, i * D:(i + 1) * D].float().view(T, H, 128).transpose(0, 1) for i in range(3))
+    s = (q @ k.transpose(1, 2)) * scale
+    if causal:
+        s = s.masked_fill(torch.ones(T, T, dtype=torch.bool, device=qkv.device).triu(1), float("-inf"))
+    lse = torch.logsumexp(s, dim=-1) / math.log(2.0)
+    o = torch.softmax(s, dim=-1) @ v
+    return o.transpose(0, 1).reshape(T, D), lse
+
+
+def _qkv(T, H, seed, pad=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    D = H * 128
+    x = torch.randn(T, 3 * D + pad, device="cuda", generator=g)
+    x[:, :2 * D] *= 1.5   # peaky rows: exercises the lazy rescale
+    return x.to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("T,H,causal", [(128, 1, True), (256, 2, True), (384, 1, True), (2048, 16, True),
+                                        (256, 2, False), (384, 3, False), (1024, 4, False)])
+def test_attn_fwd_matches_fp32(T, H, causal):
+    from paper_2605_18750_b200 import kernels as K
+    qkv = _qkv(T, H, T + H)
+    D = H * 128
+    o = torch.zeros(T, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(H, T, device="cuda")
+    K.attn_fwd(qkv, o, lse, heads=H, causal=causal)
+    torch.cuda.synchronize()
+    want, wl = _ref_fwd(qkv, H, causal, 128 ** -0.5)
+    err = (o.float() - want).abs().max().item()
+    assert err / want.abs().max().item() < 2e-2, err
+    assert ((lse - wl).abs() / wl.abs().clamp(min=1)).max().item() < 1e-3
+
+
+def test_attn_fwd_strided_views():
+    """O written into a wider activation row, lse rows longer than T (stats_row)."""
+    from paper_2605_18750_b200 import kernels as K
+    T, H = 512, 2
+    qkv = _qkv(T, H, 7, pad=64)
+    D = H * 128
+    obuf = torch.full((T, D + 64), 7.0, device="cuda", dtype=torch.bfloat16)
+    lbuf = torch.full((H, T + 128), 7.0, device="cuda")
+    K.attn_fwd(qkv, obuf[:, :D], lbuf[:, :T], heads=H, causal=True, T=T)
+    torch.cuda.synchronize()
+    want, wl = _ref_fwd(qkv, H, True, 128 ** -0.5)
+    assert (obuf[:, D:] == 7.0).all() and (lbuf[:, T:] == 7.0).all()
+    assert (obuf[:, :D].float() - want).abs().max().item() / want.abs().max().item() < 2e-2
+    assert ((lbuf[:, :T] - wl).abs()).max().item() < 1e-2
