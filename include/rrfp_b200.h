@@ -342,8 +342,8 @@ int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, i
  * compute slot of engine.py:272-273 / live.py:388-390).  tcgen05 flash attention,
  * d_head = 128, T a multiple of 128.  qkv: packed [T, ldqkv] bf16 with Q, K, V of
  * head h at columns h*128, D + h*128, 2D + h*128 (D = H*128); o: [T, ldo] bf16
- * (head h at columns h*128); lse: fp32 [H, lse_ld], lse2 = max + log2(sum) of the
- * scores scaled by scale*log2(e). */
+ * (head h at columns h*128); lse: fp32 [H, lse_ld], the natural-log logsumexp of
+ * each row of scaled scores. */
 int rrfp_attn_fwd(const void* qkv, long long ldqkv, void* o, long long ldo, float* lse,
                   long long lse_ld, int T, int H, int d_head, int causal, float scale, void* stream);
 /* test hook: log the forward's event timeline of CTA `cta` ([4][512] int64), NULL: off */

@@ -22,8 +22,8 @@
 // Row max uses a lazy rescale: O and l are rescaled only when the running max
 // grows by more than 8 (log2 units), so P <= 256 and the O correction (a TMEM
 // read-modify-write) happens on the first tiles only.
-// Statistics: lse2[h][t] = max + log2(sum), in log2 units of the scaled scores
-// (P = exp2(s * scale * log2(e) - lse2) in the backward).
+// Statistics: lse[h][t] = logsumexp of the scaled scores of row t (natural log,
+// the softmax-stats layout cuDNN's SDPA backward also reads).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(F_THREADS, 1)
           dst[v] = w;
         }
       }
-      g.lse[(size_t)pl.h * g.lse_ld + t] = m_used + __log2f(l);
+      g.lse[(size_t)pl.h * g.lse_ld + t] = (m_used + __log2f(l)) * 0.6931471805599453f;
     }
   }
   sm100::tc_fence_before();

@@ -447,6 +447,10 @@ class StageCompute:
                 self._sdpa[T] = sdpa_graphs(T, self.Hl, cfg.d_head, cfg.causal, dev, S)
             ws = max(g.workspace_bytes for g in self._sdpa.values())
             self.attn_ws = torch.empty(max(ws, 16), device=dev, dtype=torch.uint8)
+        # forward attention core: our tcgen05 kernel (csrc/fmha_sm100.cu) for d_head 128
+        # (GPT-1.3B / 7B); its softmax statistics are the layout cuDNN's backward reads
+        self.own_attn_fwd = (bool(self._sdpa) and cfg.d_head == 128 and all(T % 128 == 0 for T in self.rows)
+                             and os.environ.get("RRFP_ATTN_FWD", "own") == "own")
         if self.last:
             self.hf, self.mf, self.rf = e(n_mb, S, D), f32(n_mb, S), f32(n_mb, S)
             self.logits = e(n_mb, S, V)
@@ -494,6 +498,11 @@ class StageCompute:
     # ------------------------------------------------------------ forward
     def _attn_fwd(self, qkv, mb, li):
         T, H, Dh, D = qkv.shape[0], self.Hl, self.cfg.d_head, self.Dl
+        if self.own_attn_fwd:
+            o = self.attn_o[mb, li, :T]
+            K.attn_fwd(qkv, o, self.attn_st[mb, li], heads=H, causal=self.cfg.causal, T=T)
+            self.o_view[mb][li] = o
+            return
         if self._sdpa:
             o = self.attn_o[mb, li, :T]
             self._sdpa[T].forward(qkv.data_ptr(), o.data_ptr(), self.attn_st[mb, li].data_ptr(),

@@ -214,3 +214,52 @@ def test_gpt_pp4_lane_decisions_match_oracle(hint):
         assert met.makespan == om["makespan"]
     finally:
         pipe.close()
+
+
+# ---------------------------------------------------------------------------
+# numerics at the benchmarked shapes: the GPT-1.3B layer
+# (d 2048, S 2048, 16 heads, ffn 8192, V 50304) and the 7B TP=2 layer (d 4096,
+# 32 heads, ffn 16384), two layers, two microbatches, same tolerances as above.
+GPT13B_SLICE = dict(n_layer=2, d_model=2048, n_head=16, d_ff=8192, vocab=50304, seq=2048)
+GPT7B_SLICE = dict(n_layer=2, d_model=4096, n_head=32, d_ff=16384, vocab=50304, seq=2048)
+
+
+@pytest.mark.parametrize("hint,mode", [("bf", "free"), ("bfw", "free"), ("bf", "fixed")])
+def test_gpt13b_slice_pp2_matches_fp32_reference(hint, mode):
+    """PP=2 with one 1.3B layer per stage; mode "fixed" + hint bf is the 1F1B run."""
+    from paper_2605_18750_b200.model import GPTConfig
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    cfg = GPTConfig(**GPT13B_SLICE)
+    pipe = GpuPipeline(cfg, 2, 2, hint=hint, mode=mode)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=120).item()
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
+    torch.cuda.empty_cache()
+
+
+def test_gpt7b_slice_tp2_matches_fp32_reference():
+    """Config 3's layer at TP=2 x PP=1 (two lanes on one GPU, peer-memory all-reduce)."""
+    from paper_2605_18750_b200.model import GPTConfig
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    from ref_gpt import device_grads_tp
+    cfg = GPTConfig(**GPT7B_SLICE)
+    pipe = GpuPipeline(cfg, 1, 2, hint="bf", mode="free", tp_size=2)
+    try:
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=120).item()
+        for row in pipe.grid:
+            for st in row:
+                assert st.tp.error() == 0
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads_tp(pipe.grid, cfg))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
+    torch.cuda.empty_cache()
