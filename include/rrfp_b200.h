@@ -346,6 +346,14 @@ int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, i
  * each row of scaled scores. */
 int rrfp_attn_fwd(const void* qkv, long long ldqkv, void* o, long long ldo, float* lse,
                   long long lse_ld, int T, int H, int d_head, int causal, float scale, void* stream);
+/* Attention backward (csrc/fmha_sm100.cu): dQ, dK, dV of the forward above written
+ * into the packed dqkv [T, lddqkv] (same column layout as qkv); o / dout [T, ld*] bf16,
+ * lse the forward's statistics; workspace of rrfp_attn_bwd_workspace_bytes(T, H)
+ * device bytes (fp32 dQ accumulator + per-row vectors), owned by the caller. */
+size_t rrfp_attn_bwd_workspace_bytes(int T, int H);
+int rrfp_attn_bwd(const void* qkv, long long ldqkv, const void* o, long long ldo, const void* dout,
+                  long long lddo, const float* lse, long long lse_ld, void* dqkv, long long lddqkv,
+                  void* workspace, int T, int H, int d_head, int causal, float scale, void* stream);
 /* test hook: log the forward's event timeline of CTA `cta` ([4][512] int64), NULL: off */
 int rrfp_attn_debug(long long* buf, int cta);
 

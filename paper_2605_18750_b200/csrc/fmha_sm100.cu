@@ -537,6 +537,381 @@ int map_bf16(CUtensorMap* m, const void* ptr, long long rows, long long cols, lo
   return RRFP_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Backward (FA2-style key/value-stationary): one CTA per (head, pair of 128-row
+// key tiles (u, n-1-u)), processed one after the other (every CTA does the same
+// number of steps under the causal mask).  For a key tile j the CTA walks the
+// 64-row query sub-tiles i it sees:
+//   S^T  = K Q_i^T,  dP^T = V dO_i^T          (SS, 128 x 64 x 128, TMEM)
+//   P^T  = exp2(S^T * scale*log2e - lse2_i),   dS^T = scale * P^T (dP^T - D_i)
+//          (elementwise warpgroups 1-2, one thread per key row, 32 query columns
+//           each; bf16 P^T / dS^T to shared memory, SW128 K-major)
+//   dV  += P^T dO_i,  dK += dS^T Q_i            (SS, 128 x 128 x 64, TMEM accumulators)
+//   dQ_i^T = K^T dS^T                          (SS, 128 x 64 x 128, double-buffered TMEM)
+//          -> warpgroup 3 reduces it into the fp32 dQ accumulator (TMA reduce-add)
+// TMEM: dV [0,128) dK [128,256) S^T [256,320) dP^T [320,384) dQ^T x2 [384,512).
+// MMA issue order per step: S^T_i, dP^T_i, dV_{i-1}, dK_{i-1}, dQ^T_{i-1}, so the
+// elementwise pass of step i overlaps the gradient MMAs of step i-1.
+// D_i = rowsum(dO * O) and lse2 = lse * log2(e) come from attn_bwd_prep_kernel;
+// attn_bwd_dq_kernel converts the fp32 dQ into the packed dQKV afterwards.
+constexpr int B_QT = 64;                        // query sub-tile rows
+constexpr int B_QTILE = B_QT * DH * 2;          // 16 KB
+constexpr int B_STAGES = 3;
+constexpr int B_STAGE = 2 * B_QTILE;            // Q_i, dO_i (1024-aligned SW128 tiles)
+constexpr int B_VEC = 512;                      // lse2_i[64], D_i[64] per stage
+constexpr int B_SMEM = 2 * TILE + B_STAGES * (B_STAGE + B_VEC) + 2 * (FT * B_QT * 2) + B_QT * DH * 4 + 1024 + 256;
+constexpr int B_THREADS = 512;
+
+struct BwdArgs {
+  int T, H, D, n_kt, causal;
+  float sl2, scale;
+  const float* lse2;    // [H][T]
+  const float* dsum;    // [H][T]  D = rowsum(dO * O)
+  __nv_bfloat16* dqkv;
+  long long lddqkv;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm100::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(sm100::smem_u32(bar))
+               : "memory");
+}
+
+// key tiles of a CTA and their query sub-tile ranges
+struct BwdPlan {
+  int h, n_units, kt[2];
+};
+__device__ __forceinline__ BwdPlan bwd_plan(const BwdArgs& g) {
+  BwdPlan p;
+  p.h = blockIdx.x % g.H;
+  const int u = blockIdx.x / g.H;
+  if (g.causal) { p.kt[0] = u; p.kt[1] = g.n_kt - 1 - u; }
+  else { p.kt[0] = 2 * u; p.kt[1] = 2 * u + 1; }
+  p.n_units = (p.kt[1] == p.kt[0] || p.kt[1] >= g.n_kt) ? 1 : 2;
+  return p;
+}
+// first query sub-tile of key tile kt, and the count
+__device__ __forceinline__ int bwd_i0(const BwdArgs& g, int kt) { return g.causal ? 2 * kt : 0; }
+__device__ __forceinline__ int bwd_ni(const BwdArgs& g, int kt) { return 2 * g.n_kt - bwd_i0(g, kt); }
+
+__global__ void __launch_bounds__(B_THREADS, 1)
+    fmha_bwd_sm100(const __grid_constant__ CUtensorMap tmKV,    // qkv, box {64, 128}
+                   const __grid_constant__ CUtensorMap tmQ,     // qkv, box {64, 64}
+                   const __grid_constant__ CUtensorMap tmDO,    // dO,  box {64, 64}
+                   const __grid_constant__ CUtensorMap tmDQ,    // fp32 dQ accumulator, box {128, 64}
+                   BwdArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE;
+  uint8_t* stg = smem + 2 * TILE;                       // [B_STAGES][Q | dO]
+  uint8_t* sP = stg + B_STAGES * B_STAGE;               // P^T  [128 keys x 64 q] bf16 SW128
+  uint8_t* sDS = sP + FT * B_QT * 2;                    // dS^T
+  float* sDQ = reinterpret_cast<float*>(sDS + FT * B_QT * 2);   // dQ staging [64 q][128 d]
+  uint8_t* svec = reinterpret_cast<uint8_t*>(sDQ) + B_QT * DH * 4;   // [B_STAGES][lse2 | D]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(svec + B_STAGES * B_VEC);
+  uint64_t* kv_full = bars;                 // K, V of the unit loaded
+  uint64_t* kv_free = bars + 1;             // the unit's MMAs are done with K, V
+  uint64_t* full = bars + 2;                // [B_STAGES]
+  uint64_t* empty = full + B_STAGES;        // [B_STAGES]
+  uint64_t* s_full = empty + B_STAGES;      // S^T, dP^T of the step in TMEM
+  uint64_t* sd_free = s_full + 1;           // ... loaded into registers (256 arrivals)
+  uint64_t* ds_full = sd_free + 1;          // P^T, dS^T in smem (256 arrivals)
+  uint64_t* pds_free = ds_full + 1;         // the MMAs reading P^T, dS^T are done
+  uint64_t* dq_full = pds_free + 1;         // [2] dQ^T in TMEM
+  uint64_t* dq_free = dq_full + 2;          // [2] ... read out (128 arrivals)
+  uint64_t* acc_full = dq_free + 2;         // dV, dK of the unit complete
+  uint64_t* acc_free = acc_full + 1;        // ... written out (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const BwdPlan pl = bwd_plan(g);
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmKV); sm100::tma_prefetch(&tmQ); sm100::tma_prefetch(&tmDO); sm100::tma_prefetch(&tmDQ);
+    sm100::mbar_init(kv_full, 1); sm100::mbar_init(kv_free, 1);
+    for (int s = 0; s < B_STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    sm100::mbar_init(s_full, 1); sm100::mbar_init(sd_free, 256); sm100::mbar_init(ds_full, 256);
+    sm100::mbar_init(pds_free, 1);
+    for (int b = 0; b < 2; ++b) { sm100::mbar_init(&dq_full[b], 1); sm100::mbar_init(&dq_free[b], 128); }
+    sm100::mbar_init(acc_full, 1); sm100::mbar_init(acc_free, 256);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  sm100::griddep_launch();
+  sm100::griddep_wait();
+  const int kcol = g.D + pl.h * DH, vcol = 2 * g.D + pl.h * DH, qcol = pl.h * DH;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int n = 0;
+      for (int un = 0; un < pl.n_units; ++un) {
+        const int kt = pl.kt[un];
+        if (un) wait(kv_free, (un - 1) & 1);
+        sm100::mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        for (int p = 0; p < 2; ++p) {
+          sm100::tma_load_2d(sK + p * PANEL, &tmKV, kv_full, kcol + 64 * p, kt * FT);
+          sm100::tma_load_2d(sV + p * PANEL, &tmKV, kv_full, vcol + 64 * p, kt * FT);
+        }
+        const int i0 = bwd_i0(g, kt), ni = bwd_ni(g, kt);
+        for (int ii = 0; ii < ni; ++ii, ++n) {
+          const int i = i0 + ii, st = n % B_STAGES;
+          wait(&empty[st], ((n / B_STAGES) & 1) ^ 1);
+          uint8_t* d = stg + st * B_STAGE;
+          sm100::mbar_arrive_expect_tx(&full[st], 2 * B_QTILE + B_VEC);
+          for (int p = 0; p < 2; ++p) {
+            sm100::tma_load_2d(d + p * (B_QTILE / 2), &tmQ, &full[st], qcol + 64 * p, i * B_QT);
+            sm100::tma_load_2d(d + B_QTILE + p * (B_QTILE / 2), &tmDO, &full[st], qcol + 64 * p, i * B_QT);
+          }
+          bulk_g2s(svec + st * B_VEC, g.lse2 + (size_t)pl.h * g.T + i * B_QT, 256, &full[st]);
+          bulk_g2s(svec + st * B_VEC + 256, g.dsum + (size_t)pl.h * g.T + i * B_QT, 256, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // S^T / dP^T: M=128 keys, N=64 queries, K=128 (A K-major keys/values, B K-major Q/dO)
+    constexpr uint32_t idSD = sm100::idesc_bf16(128, 64, 0, 0);
+    // dV / dK: M=128 keys, N=128 (d), K=64 queries (A = P^T / dS^T K-major, B = dO / Q MN-major)
+    constexpr uint32_t idVK = sm100::idesc_bf16(128, 128, 0, 1);
+    // dQ^T: M=128 (d), N=64 queries, K=128 keys (A = K MN-major, B = dS^T MN-major)
+    constexpr uint32_t idQ = sm100::idesc_bf16(128, 64, 1, 1);
+    const uint32_t tS = tmem + 256, tP = tmem + 320;
+    const uint64_t dK_k = sm100::umma_desc_sw128(sm100::smem_u32(sK), 16, 1024);
+    const uint64_t dV_k = sm100::umma_desc_sw128(sm100::smem_u32(sV), 16, 1024);
+    const uint64_t dK_mn = sm100::umma_desc_sw128(sm100::smem_u32(sK), PANEL, 1024);
+    const uint64_t dP_a = sm100::umma_desc_sw128(sm100::smem_u32(sP), 16, 1024);
+    const uint64_t dDS_a = sm100::umma_desc_sw128(sm100::smem_u32(sDS), 16, 1024);
+    const uint64_t dDS_b = sm100::umma_desc_sw128(sm100::smem_u32(sDS), PANEL, 1024);
+    const uint64_t dStg_k = sm100::umma_desc_sw128(sm100::smem_u32(stg), 16, 1024);
+    const uint64_t dStg_mn = sm100::umma_desc_sw128(sm100::smem_u32(stg), B_QTILE / 2, 1024);
+    int n = 0, step = 0;   // ring index, global step (sd/ds/pds/dq parities)
+    auto sd = [&](int st) {   // S^T, dP^T of a step into TMEM
+      const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
+        mma_ss_e(tS, dK_k + ka, dStg_k + so + kb, idSD, k != 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
+        mma_ss_e(tP, dV_k + ka, dStg_k + so + ((B_QTILE >> 4) + kb), idSD, k != 0);
+      }
+      commit_e(s_full);
+    };
+    auto grads = [&](int st, int first, int gstep) {   // dV, dK, dQ^T of a step
+      wait(ds_full, gstep & 1);
+      sm100::tc_fence_after();
+      const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)   // dV += P^T dO
+        mma_ss_e(tmem, dP_a + ((k * 32) >> 4), dStg_mn + so + ((B_QTILE + k * 2048) >> 4), idVK, !first || k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)   // dK += dS^T Q
+        mma_ss_e(tmem + 128, dDS_a + ((k * 32) >> 4), dStg_mn + so + ((k * 2048) >> 4), idVK, !first || k);
+      const int b = gstep & 1;
+      if (gstep >= 2) wait(&dq_free[b], ((gstep - 2) >> 1) & 1);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < 8; ++k)   // dQ^T = K^T dS^T
+        mma_ss_e(tmem + 384 + 64 * b, dK_mn + ((k * 2048) >> 4), dDS_b + ((k * 2048) >> 4), idQ, k != 0);
+      commit_e(pds_free);
+      commit_e(&dq_full[b]);
+      commit_e(&empty[st]);
+    };
+    for (int un = 0; un < pl.n_units; ++un) {
+      const int kt = pl.kt[un], ni = bwd_ni(g, kt);
+      wait(kv_full, un & 1);
+      if (un) wait(acc_free, (un - 1) & 1);   // the previous unit's dV / dK are written out
+      sm100::tc_fence_after();
+      int prev_st = -1;
+      for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
+        const int st = n % B_STAGES;
+        wait(&full[st], (n / B_STAGES) & 1);
+        if (step) wait(sd_free, (step - 1) & 1);   // the elementwise pass has S^T / dP^T of the last step
+        sm100::tc_fence_after();
+        sd(st);
+        if (ii) grads(prev_st, ii == 1, step - 1);
+        prev_st = st;
+      }
+      grads(prev_st, ni == 1, step - 1);
+      commit_e(acc_full);
+      commit_e(kv_free);
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // elementwise: thread = key row, 32 query columns of the sub-tile
+    const int wg = (warp - 4) >> 2, q4 = warp & 3, row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint64_t sl2_2 = f2pack(g.sl2, g.sl2);
+    int n = 0, step = 0;
+    for (int un = 0; un < pl.n_units; ++un) {
+      const int kt = pl.kt[un], i0 = bwd_i0(g, kt), ni = bwd_ni(g, kt);
+      const int key = kt * FT + row;
+      for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
+        const int st = n % B_STAGES, i = i0 + ii;
+        const float* vec = reinterpret_cast<const float*>(svec + st * B_VEC);
+        wait(&full[st], (n / B_STAGES) & 1);   // (the stage's lse2 / D vectors)
+        wait(s_full, step & 1);
+        sm100::tc_fence_after();
+        uint32_t s[32], dp[32];
+        sm100::tmem_ld32(tmem + lane_off + 256 + wg * 32, s);
+        sm100::tmem_ld32(tmem + lane_off + 320 + wg * 32, dp);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(sd_free);
+        const int qb = i * B_QT + wg * 32;
+        const bool mask = g.causal && qb < key;   // some query of this warp's columns precedes the key
+        uint32_t pw[16], dw[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const uint64_t l2 = *reinterpret_cast<const uint64_t*>(vec + wg * 32 + c);
+          const uint64_t d2 = *reinterpret_cast<const uint64_t*>(vec + 64 + wg * 32 + c);
+          const uint64_t x2 = ffma2(u2pack(s[c], s[c + 1]), sl2_2, l2 ^ 0x8000000080000000ull);
+          float p0 = ex2(f2lo(x2)), p1 = ex2(f2hi(x2));
+          if (mask) {
+            if (qb + c < key) p0 = 0.f;
+            if (qb + c + 1 < key) p1 = 0.f;
+          }
+          const uint64_t p2 = f2pack(p0, p1);
+          const uint64_t t2 = fadd2(u2pack(dp[c], dp[c + 1]), d2 ^ 0x8000000080000000ull);   // dP - D
+          const uint64_t ds2 = ffma2(p2, t2, 0);   // P (dP - D)
+          pw[c >> 1] = pack_bf16(p0, p1);
+          dw[c >> 1] = pack_bf16(f2lo(ds2) * g.scale, f2hi(ds2) * g.scale);
+        }
+        if (step) wait(pds_free, (step - 1) & 1);   // the last step's MMAs have read P^T / dS^T
+        // row `row` of the SW128 K-major tiles: 128 B = 8 chunks of 16 B, chunk c at c ^ (row & 7)
+        uint8_t* prow = sP + row * 128;
+        uint8_t* drow = sDS + row * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int ch = ((wg * 4 + c) ^ (row & 7)) * 16;
+          *reinterpret_cast<uint4*>(prow + ch) = make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+          *reinterpret_cast<uint4*>(drow + ch) = make_uint4(dw[4 * c], dw[4 * c + 1], dw[4 * c + 2], dw[4 * c + 3]);
+        }
+        sm100::fence_proxy_async_smem();
+        sm100::mbar_arrive(ds_full);
+      }
+      // unit epilogue: warpgroup 0 writes dV, warpgroup 1 dK (bf16 into the packed dQKV)
+      wait(acc_full, un & 1);
+      sm100::tc_fence_after();
+      __nv_bfloat16* dst = g.dqkv + (size_t)key * g.lddqkv + (wg ? kcol : vcol);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        sm100::tmem_ld32(tmem + lane_off + wg * 128 + 32 * c, r);
+        sm100::tmem_ld_wait();
+        uint4* o4 = reinterpret_cast<uint4*>(dst + 32 * c);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          o4[v] = make_uint4(pack_bf16(__uint_as_float(r[8 * v]), __uint_as_float(r[8 * v + 1])),
+                             pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
+                             pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
+                             pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(acc_free);
+    }
+  } else if (warp >= 12) {
+    // dQ^T read-out: thread = head-dim lane d, 64 query columns -> staging [q][d] ->
+    // TMA reduce-add into the fp32 dQ accumulator
+    const int q4 = warp & 3, d = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const bool issuer = warp == 12 && lane == 0;
+    int step = 0;
+    for (int un = 0; un < pl.n_units; ++un) {
+      const int kt = pl.kt[un], i0 = bwd_i0(g, kt), ni = bwd_ni(g, kt);
+      for (int ii = 0; ii < ni; ++ii, ++step) {
+        const int b = step & 1;
+        wait(&dq_full[b], (step >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t r[64];
+        sm100::tmem_ld32(tmem + lane_off + 384 + 64 * b, *reinterpret_cast<uint32_t(*)[32]>(r));
+        sm100::tmem_ld32(tmem + lane_off + 384 + 64 * b + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&dq_free[b]);
+        if (issuer) sm100::bulk_wait_read<0>();   // the last reduce has read the staging tile
+        named_bar(1, 128);
+#pragma unroll
+        for (int c = 0; c < 64; ++c) sDQ[c * DH + d] = __uint_as_float(r[c]);
+        sm100::fence_proxy_async_smem();
+        named_bar(1, 128);
+        if (issuer) {
+          sm100::tma_reduce_add_2d(&tmDQ, sDQ, pl.h * DH, (i0 + ii) * B_QT);
+          sm100::bulk_commit();
+        }
+      }
+    }
+    if (issuer) sm100::bulk_wait<0>();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+// D[h][t] = sum_d dO[t, h*128 + d] * O[t, h*128 + d];  lse2 = lse * log2(e).  One warp per (t, h).
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, long long ldo,
+                                     const __nv_bfloat16* __restrict__ dout, long long lddo,
+                                     const float* __restrict__ lse, long long lse_ld, float* __restrict__ lse2,
+                                     float* __restrict__ dsum, int T, int H) {
+  sm100::griddep_wait();
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= T * H) return;
+  const int t = w / H, h = w % H;
+  const uint2 a = *reinterpret_cast<const uint2*>(o + (size_t)t * ldo + h * DH + lane * 4);
+  const uint2 b = *reinterpret_cast<const uint2*>(dout + (size_t)t * lddo + h * DH + lane * 4);
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float2 x = __bfloat1622float2(a2[k]), y = __bfloat1622float2(b2[k]);
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    dsum[(size_t)h * T + t] = acc;
+    lse2[(size_t)h * T + t] = lse[(size_t)h * lse_ld + t] * 1.4426950408889634f;
+  }
+}
+
+// dQ (fp32 [T, D]) -> bf16 columns [0, D) of the packed dQKV
+__global__ void attn_bwd_dq_kernel(const float4* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv, long long ld,
+                                   int T, int D) {
+  sm100::griddep_wait();
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // 8 elements per thread
+  const long long n8 = (long long)T * D / 8;
+  if (i >= n8) return;
+  const long long e = i * 8;
+  const int t = (int)(e / D), c = (int)(e % D);
+  const float4 a = dq[2 * i], b = dq[2 * i + 1];
+  *reinterpret_cast<uint4*>(dqkv + (size_t)t * ld + c) =
+      make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+}
+
+int map_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols, int box_cols, int box_rows) {
+  encode_fn_t enc = encode();
+  if (!enc) return rrfp_fail(RRFP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return rrfp_fail(RRFP_E_INVALID, "fmha dq tensor map encode failed (%d)", (int)r);
+  return RRFP_OK;
+}
+
 long long* g_attn_dbg = nullptr;
 int g_attn_dbg_cta = 0;
 
@@ -572,5 +947,53 @@ extern "C" int rrfp_attn_fwd(const void* qkv, long long ldqkv, void* o, long lon
   g.experiment = 0;
   const int grid = H * ((g.n_qt + 1) / 2);
   RRFP_CUDA_TRY(rrfp_launch(fmha_fwd_sm100, dim3(grid), dim3(F_THREADS), F_SMEM, (cudaStream_t)stream, m, g));
+  return RRFP_OK;
+}
+
+/* workspace of rrfp_attn_bwd: fp32 dQ accumulator [T, H*128] + lse2 [H, T] + D [H, T] */
+extern "C" size_t rrfp_attn_bwd_workspace_bytes(int T, int H) {
+  return (size_t)T * H * DH * 4 + 2 * (size_t)H * T * 4;
+}
+
+extern "C" int rrfp_attn_bwd(const void* qkv, long long ldqkv, const void* o, long long ldo, const void* dout,
+                             long long lddo, const float* lse, long long lse_ld, void* dqkv, long long lddqkv,
+                             void* workspace, int T, int H, int d_head, int causal, float scale, void* stream) {
+  if (d_head != DH) return rrfp_fail(RRFP_E_INVALID, "attn_bwd: d_head %d unsupported (128 only)", d_head);
+  if (T <= 0 || T % FT) return rrfp_fail(RRFP_E_INVALID, "attn_bwd: T=%d must be a positive multiple of 128", T);
+  const long long D = (long long)H * DH;
+  if (!qkv || !o || !dout || !lse || !dqkv || !workspace || ldqkv < 3 * D || lddqkv < 3 * D || ldo < D ||
+      lddo < D || (ldqkv % 8) || (lddqkv % 8) || (ldo % 8) || (lddo % 8))
+    return rrfp_fail(RRFP_E_INVALID, "attn_bwd: bad pointers / leading dims");
+  static bool attr = false;
+  if (!attr) {
+    RRFP_CUDA_TRY(cudaFuncSetAttribute(fmha_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM));
+    attr = true;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  float* dq = reinterpret_cast<float*>(workspace);
+  float* lse2 = dq + (size_t)T * D;
+  float* dsum = lse2 + (size_t)H * T;
+  CUtensorMap mKV, mQ, mDO, mDQ;
+  int rc = map_bf16(&mKV, qkv, T, 3 * D, ldqkv, FT);
+  if (!rc) rc = map_bf16(&mQ, qkv, T, 3 * D, ldqkv, B_QT);
+  if (!rc) rc = map_bf16(&mDO, dout, T, D, lddo, B_QT);
+  if (!rc) rc = map_f32(&mDQ, dq, T, D, DH, B_QT);
+  if (rc) return rc;
+  RRFP_CUDA_TRY(cudaMemsetAsync(dq, 0, (size_t)T * D * 4, st));
+  const int warps = T * H;
+  RRFP_CUDA_TRY(rrfp_launch(attn_bwd_prep_kernel, dim3((warps + 7) / 8), dim3(256), 0, st,
+                            reinterpret_cast<const __nv_bfloat16*>(o), ldo,
+                            reinterpret_cast<const __nv_bfloat16*>(dout), lddo, lse, lse_ld, lse2, dsum, T, H));
+  BwdArgs g;
+  g.T = T; g.H = H; g.D = (int)D; g.n_kt = T / FT; g.causal = causal ? 1 : 0;
+  g.sl2 = scale * 1.4426950408889634f; g.scale = scale;
+  g.lse2 = lse2; g.dsum = dsum;
+  g.dqkv = reinterpret_cast<__nv_bfloat16*>(dqkv); g.lddqkv = lddqkv;
+  const int grid = H * ((g.n_kt + 1) / 2);
+  RRFP_CUDA_TRY(rrfp_launch(fmha_bwd_sm100, dim3(grid), dim3(B_THREADS), B_SMEM, st, mKV, mQ, mDO, mDQ, g));
+  const long long n8 = (long long)T * D / 8;
+  RRFP_CUDA_TRY(rrfp_launch(attn_bwd_dq_kernel, dim3((unsigned)((n8 + 255) / 256)), dim3(256), 0, st,
+                            reinterpret_cast<const float4*>(dq), reinterpret_cast<__nv_bfloat16*>(dqkv), lddqkv,
+                            T, (int)D));
   return RRFP_OK;
 }

@@ -67,3 +67,23 @@ def attn_fwd(qkv, o, lse, *, heads, causal=True, scale=None, T=None):
                                _p(lse), C.c_longlong(lse.stride(0)), T, heads, dh, int(causal),
                                C.c_float(scale), _stream()))
     return o
+
+
+def attn_bwd_workspace(T, heads, device="cuda"):
+    n = _lib.lib().rrfp_attn_bwd_workspace_bytes(T, heads)
+    return torch.empty(n, device=device, dtype=torch.uint8)
+
+
+def attn_bwd(qkv, o, do, lse, dqkv, ws, *, heads, causal=True, scale=None, T=None):
+    """Flash attention backward (csrc/fmha_sm100.cu): dQ, dK, dV into the packed dqkv
+    [T, >=3D]; lse = the forward's statistics [H, >=T]; ws from attn_bwd_workspace."""
+    T = qkv.shape[0] if T is None else T
+    dh = 128
+    scale = dh ** -0.5 if scale is None else scale
+    L = _lib.lib()
+    note(4)
+    _lib.check(L.rrfp_attn_bwd(_p(qkv), C.c_longlong(qkv.stride(0)), _p(o), C.c_longlong(o.stride(0)), _p(do),
+                               C.c_longlong(do.stride(0)), _p(lse), C.c_longlong(lse.stride(0)), _p(dqkv),
+                               C.c_longlong(dqkv.stride(0)), _p(ws), T, heads, dh, int(causal), C.c_float(scale),
+                               _stream()))
+    return dqkv

@@ -83,3 +83,38 @@ def test_attn_fwd_stats_match_cudnn():
     torch.cuda.synchronize()
     assert (lse - st).abs().max().item() < 1e-2
     assert (o.float() - oc.float()).abs().max().item() < 3e-2
+
+
+def _ref_bwd(qkv, do, H, causal, scale):
+    T = qkv.shape[0]
+    D = H * 128
+    x = qkv.float().requires_grad_(True)
+    q, k, v = (x[:, i * D:(i + 1) * D].view(T, H, 128).transpose(0, 1) for i in range(3))
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal, scale=scale)
+    o = o.transpose(0, 1).reshape(T, D)
+    o.backward(do.float())
+    return x.grad
+
+
+@pytest.mark.parametrize("T,H,causal", [(128, 1, True), (256, 2, True), (384, 1, True), (2048, 16, True),
+                                        (256, 2, False), (384, 3, False)])
+def test_attn_bwd_matches_fp32(T, H, causal):
+    """dQ, dK, dV (packed) against fp32 autograd: per block cosine >= 0.999, relative L2 <= 2e-2."""
+    from paper_2605_18750_b200 import kernels as K
+    qkv = _qkv(T, H, 3 * T + H)
+    D = H * 128
+    g = torch.Generator(device="cuda").manual_seed(T + 5)
+    do = torch.randn(T, D, device="cuda", generator=g).to(torch.bfloat16)
+    o = torch.zeros(T, D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(H, T, device="cuda")
+    K.attn_fwd(qkv, o, lse, heads=H, causal=causal)
+    dqkv = torch.full((T, 3 * D), 7.0, device="cuda", dtype=torch.bfloat16)
+    ws = K.attn_bwd_workspace(T, H)
+    K.attn_bwd(qkv, o, do, lse, dqkv, ws, heads=H, causal=causal)
+    torch.cuda.synchronize()
+    want = _ref_bwd(qkv, do, H, causal, 128 ** -0.5)
+    for i, name in enumerate("qkv"):
+        a, b = dqkv[:, i * D:(i + 1) * D].float(), want[:, i * D:(i + 1) * D]
+        cos = torch.nn.functional.cosine_similarity(a.flatten(), b.flatten(), dim=0).item()
+        rel = ((a - b).norm() / b.norm()).item()
+        assert cos >= 0.999 and rel <= 2e-2, (name, cos, rel)
