@@ -57,21 +57,23 @@ struct FwdArgs {
   int dbg_cta;
 };
 
-// mbarrier wait that traps after ~4 s instead of hanging the device
-__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = sm100::smem_u32(bar);
+// mbarrier wait that traps after ~4 s instead of hanging the device.  Plain
+// try_wait (no suspend-time hint): a hinted wait parks the thread in
+// NANOSLEEP.SYNCS and the hand-offs between the roles pick up its wake-up latency.
+__device__ __forceinline__ uint32_t try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\nselp.u32 %0, 1, 0, p;\n}\n"
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
-  if (ok) return;
+  return ok;
+}
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = sm100::smem_u32(bar);
+  if (try_wait(addr, parity)) return;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
-    if (ok) return;
+    if (try_wait(addr, parity)) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 4000000000ull) __trap();
@@ -132,6 +134,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -561,7 +571,10 @@ constexpr int B_STAGES = 3;
 constexpr int B_STAGE = 2 * B_QTILE;            // Q_i, dO_i (1024-aligned SW128 tiles)
 constexpr int B_VEC = 512;                      // lse2_i[64], D_i[64] per stage
 constexpr int B_SMEM = 2 * TILE + B_STAGES * (B_STAGE + B_VEC) + 2 * (FT * B_QT * 2) + B_QT * DH * 4 + 1024 + 256;
-constexpr int B_THREADS = 512;
+constexpr int B_EWG = 2;                        // elementwise warpgroups (query columns split B_EWG ways)
+constexpr int B_EWC = B_QT / B_EWG;             // query columns per elementwise thread
+constexpr int B_RD0 = 4 + 4 * B_EWG;            // first dQ read-out warp
+constexpr int B_THREADS = 32 * (B_RD0 + 4);
 
 struct BwdArgs {
   int T, H, D, n_kt, causal;
@@ -570,6 +583,8 @@ struct BwdArgs {
   const float* dsum;    // [H][T]  D = rowsum(dO * O)
   __nv_bfloat16* dqkv;
   long long lddqkv;
+  long long* dbg;    // optional event log of CTA dbg_cta: [4][512]
+  int dbg_cta;
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -628,14 +643,17 @@ __global__ void __launch_bounds__(B_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const BwdPlan pl = bwd_plan(g);
+  int dbg_n = 0;
+  const bool dbg_on = g.dbg && (int)blockIdx.x == g.dbg_cta && (lane == 0) &&
+                      (warp == 1 || warp == 0 || warp == 4 || warp == B_RD0);
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmKV); sm100::tma_prefetch(&tmQ); sm100::tma_prefetch(&tmDO); sm100::tma_prefetch(&tmDQ);
     sm100::mbar_init(kv_full, 1); sm100::mbar_init(kv_free, 1);
     for (int s = 0; s < B_STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    sm100::mbar_init(s_full, 1); sm100::mbar_init(sd_free, 256); sm100::mbar_init(ds_full, 256);
+    sm100::mbar_init(s_full, 1); sm100::mbar_init(sd_free, 128 * B_EWG); sm100::mbar_init(ds_full, 128 * B_EWG);
     sm100::mbar_init(pds_free, 1);
     for (int b = 0; b < 2; ++b) { sm100::mbar_init(&dq_full[b], 1); sm100::mbar_init(&dq_free[b], 128); }
-    sm100::mbar_init(acc_full, 1); sm100::mbar_init(acc_free, 256);
+    sm100::mbar_init(acc_full, 1); sm100::mbar_init(acc_free, 128 * B_EWG);
     sm100::fence_barrier_init();
   }
   if (warp == 2) sm100::tmem_alloc<512>(tmem_slot);
@@ -705,7 +723,9 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       commit_e(s_full);
     };
     auto grads = [&](int st, int first, int gstep) {   // dV, dK, dQ^T of a step
+      DBG(1, 14, gstep);
       wait(ds_full, gstep & 1);
+      DBG(1, 15, gstep);
       sm100::tc_fence_after();
       const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
 #pragma unroll
@@ -715,7 +735,9 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       for (int k = 0; k < 4; ++k)   // dK += dS^T Q
         mma_ss_e(tmem + 128, dDS_a + ((k * 32) >> 4), dStg_mn + so + ((k * 2048) >> 4), idVK, !first || k);
       const int b = gstep & 1;
+      DBG(1, 16, gstep);
       if (gstep >= 2) wait(&dq_free[b], ((gstep - 2) >> 1) & 1);
+      DBG(1, 17, gstep);
       sm100::tc_fence_after();
 #pragma unroll
       for (int k = 0; k < 8; ++k)   // dQ^T = K^T dS^T
@@ -723,6 +745,7 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       commit_e(pds_free);
       commit_e(&dq_full[b]);
       commit_e(&empty[st]);
+      DBG(1, 18, gstep);
     };
     for (int un = 0; un < pl.n_units; ++un) {
       const int kt = pl.kt[un], ni = bwd_ni(g, kt);
@@ -732,10 +755,14 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       int prev_st = -1;
       for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
         const int st = n % B_STAGES;
+        DBG(1, 10, step);
         wait(&full[st], (n / B_STAGES) & 1);
+        DBG(1, 11, step);
         if (step) wait(sd_free, (step - 1) & 1);   // the elementwise pass has S^T / dP^T of the last step
+        DBG(1, 12, step);
         sm100::tc_fence_after();
         sd(st);
+        DBG(1, 13, step);
         if (ii) grads(prev_st, ii == 1, step - 1);
         prev_st = st;
       }
@@ -743,8 +770,8 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       commit_e(acc_full);
       commit_e(kv_free);
     }
-  } else if (warp >= 4 && warp < 12) {
-    // elementwise: thread = key row, 32 query columns of the sub-tile
+  } else if (warp >= 4 && warp < B_RD0) {
+    // elementwise: thread = key row, B_EWC query columns of the sub-tile
     const int wg = (warp - 4) >> 2, q4 = warp & 3, row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint64_t sl2_2 = f2pack(g.sl2, g.sl2);
@@ -755,22 +782,30 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
         const int st = n % B_STAGES, i = i0 + ii;
         const float* vec = reinterpret_cast<const float*>(svec + st * B_VEC);
+        DBG(2, 0, step);
         wait(&full[st], (n / B_STAGES) & 1);   // (the stage's lse2 / D vectors)
         wait(s_full, step & 1);
+        DBG(2, 1, step);
         sm100::tc_fence_after();
-        uint32_t s[32], dp[32];
-        sm100::tmem_ld32(tmem + lane_off + 256 + wg * 32, s);
-        sm100::tmem_ld32(tmem + lane_off + 320 + wg * 32, dp);
+        uint32_t s[B_EWC], dp[B_EWC];
+        if (B_EWC == 32) {
+          sm100::tmem_ld32(tmem + lane_off + 256 + wg * B_EWC, *reinterpret_cast<uint32_t(*)[32]>(s));
+          sm100::tmem_ld32(tmem + lane_off + 320 + wg * B_EWC, *reinterpret_cast<uint32_t(*)[32]>(dp));
+        } else {
+          tmem_ld16(tmem + lane_off + 256 + wg * B_EWC, *reinterpret_cast<uint32_t(*)[16]>(s));
+          tmem_ld16(tmem + lane_off + 320 + wg * B_EWC, *reinterpret_cast<uint32_t(*)[16]>(dp));
+        }
         sm100::tmem_ld_wait();
         sm100::tc_fence_before();
         sm100::mbar_arrive(sd_free);
-        const int qb = i * B_QT + wg * 32;
+        DBG(2, 5, step);
+        const int qb = i * B_QT + wg * B_EWC;
         const bool mask = g.causal && qb < key;   // some query of this warp's columns precedes the key
-        uint32_t pw[16], dw[16];
+        uint32_t pw[B_EWC / 2], dw[B_EWC / 2];
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const uint64_t l2 = *reinterpret_cast<const uint64_t*>(vec + wg * 32 + c);
-          const uint64_t d2 = *reinterpret_cast<const uint64_t*>(vec + 64 + wg * 32 + c);
+        for (int c = 0; c < B_EWC; c += 2) {
+          const uint64_t l2 = *reinterpret_cast<const uint64_t*>(vec + wg * B_EWC + c);
+          const uint64_t d2 = *reinterpret_cast<const uint64_t*>(vec + 64 + wg * B_EWC + c);
           const uint64_t x2 = ffma2(u2pack(s[c], s[c + 1]), sl2_2, l2 ^ 0x8000000080000000ull);
           float p0 = ex2(f2lo(x2)), p1 = ex2(f2hi(x2));
           if (mask) {
@@ -779,31 +814,37 @@ __global__ void __launch_bounds__(B_THREADS, 1)
           }
           const uint64_t p2 = f2pack(p0, p1);
           const uint64_t t2 = fadd2(u2pack(dp[c], dp[c + 1]), d2 ^ 0x8000000080000000ull);   // dP - D
-          const uint64_t ds2 = ffma2(p2, t2, 0);   // P (dP - D)
+          const uint64_t ds2 = ffma2(ffma2(p2, t2, 0), f2pack(g.scale, g.scale), 0);   // scale * P (dP - D)
           pw[c >> 1] = pack_bf16(p0, p1);
-          dw[c >> 1] = pack_bf16(f2lo(ds2) * g.scale, f2hi(ds2) * g.scale);
+          dw[c >> 1] = pack_bf16(f2lo(ds2), f2hi(ds2));
         }
+        DBG(2, 2, step);
         if (step) wait(pds_free, (step - 1) & 1);   // the last step's MMAs have read P^T / dS^T
+        DBG(2, 3, step);
         // row `row` of the SW128 K-major tiles: 128 B = 8 chunks of 16 B, chunk c at c ^ (row & 7)
         uint8_t* prow = sP + row * 128;
         uint8_t* drow = sDS + row * 128;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int ch = ((wg * 4 + c) ^ (row & 7)) * 16;
+        for (int c = 0; c < B_EWC / 8; ++c) {
+          const int ch = ((wg * (B_EWC / 8) + c) ^ (row & 7)) * 16;
           *reinterpret_cast<uint4*>(prow + ch) = make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
           *reinterpret_cast<uint4*>(drow + ch) = make_uint4(dw[4 * c], dw[4 * c + 1], dw[4 * c + 2], dw[4 * c + 3]);
         }
         sm100::fence_proxy_async_smem();
         sm100::mbar_arrive(ds_full);
+        DBG(2, 4, step);
       }
-      // unit epilogue: warpgroup 0 writes dV, warpgroup 1 dK (bf16 into the packed dQKV)
+      // unit epilogue: the elementwise warpgroups write dV (TMEM columns [0,128)) and dK
+      // ([128,256)), 256 / B_EWG columns each, bf16 into the packed dQKV
       wait(acc_full, un & 1);
       sm100::tc_fence_after();
-      __nv_bfloat16* dst = g.dqkv + (size_t)key * g.lddqkv + (wg ? kcol : vcol);
+      constexpr int EC = 256 / B_EWG;
+      const int c0 = wg * EC;
+      __nv_bfloat16* dst = g.dqkv + (size_t)key * g.lddqkv + (c0 < 128 ? vcol + c0 : kcol + c0 - 128);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < EC / 32; ++c) {
         uint32_t r[32];
-        sm100::tmem_ld32(tmem + lane_off + wg * 128 + 32 * c, r);
+        sm100::tmem_ld32(tmem + lane_off + c0 + 32 * c, r);
         sm100::tmem_ld_wait();
         uint4* o4 = reinterpret_cast<uint4*>(dst + 32 * c);
 #pragma unroll
@@ -816,18 +857,20 @@ __global__ void __launch_bounds__(B_THREADS, 1)
       sm100::tc_fence_before();
       sm100::mbar_arrive(acc_free);
     }
-  } else if (warp >= 12) {
+  } else if (warp >= B_RD0) {
     // dQ^T read-out: thread = head-dim lane d, 64 query columns -> staging [q][d] ->
     // TMA reduce-add into the fp32 dQ accumulator
     const int q4 = warp & 3, d = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const bool issuer = warp == 12 && lane == 0;
+    const bool issuer = warp == B_RD0 && lane == 0;
     int step = 0;
     for (int un = 0; un < pl.n_units; ++un) {
       const int kt = pl.kt[un], i0 = bwd_i0(g, kt), ni = bwd_ni(g, kt);
       for (int ii = 0; ii < ni; ++ii, ++step) {
         const int b = step & 1;
+        DBG(3, 30, step);
         wait(&dq_full[b], (step >> 1) & 1);
+        DBG(3, 31, step);
         sm100::tc_fence_after();
         uint32_t r[64];
         sm100::tmem_ld32(tmem + lane_off + 384 + 64 * b, *reinterpret_cast<uint32_t(*)[32]>(r));
@@ -845,6 +888,7 @@ __global__ void __launch_bounds__(B_THREADS, 1)
           sm100::tma_reduce_add_2d(&tmDQ, sDQ, pl.h * DH, (i0 + ii) * B_QT);
           sm100::bulk_commit();
         }
+        DBG(3, 32, step);
       }
     }
     if (issuer) sm100::bulk_wait<0>();
@@ -913,12 +957,15 @@ int map_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols, int
 }
 
 long long* g_attn_dbg = nullptr;
+long long* g_attn_dbg_bwd = nullptr;
 int g_attn_dbg_cta = 0;
 
 }  // namespace
 
 /* test hook: log the event timeline of CTA `cta` into buf ([4][512] int64), NULL: off */
 extern "C" int rrfp_attn_debug(long long* buf, int cta) {
+  const char* e = getenv("RRFP_ATTN_DEBUG_BWD");
+  if (e && atoi(e)) { g_attn_dbg_bwd = buf; g_attn_dbg_cta = cta; return RRFP_OK; }
   g_attn_dbg = buf;
   g_attn_dbg_cta = cta;
   return RRFP_OK;
@@ -989,6 +1036,7 @@ extern "C" int rrfp_attn_bwd(const void* qkv, long long ldqkv, const void* o, lo
   g.sl2 = scale * 1.4426950408889634f; g.scale = scale;
   g.lse2 = lse2; g.dsum = dsum;
   g.dqkv = reinterpret_cast<__nv_bfloat16*>(dqkv); g.lddqkv = lddqkv;
+  g.dbg = g_attn_dbg_bwd; g.dbg_cta = g_attn_dbg_cta;
   const int grid = H * ((g.n_kt + 1) / 2);
   RRFP_CUDA_TRY(rrfp_launch(fmha_bwd_sm100, dim3(grid), dim3(B_THREADS), B_SMEM, st, mKV, mQ, mDO, mDQ, g));
   const long long n8 = (long long)T * D / 8;

@@ -263,3 +263,21 @@ def test_gpt7b_slice_tp2_matches_fp32_reference():
     finally:
         pipe.close()
     torch.cuda.empty_cache()
+
+
+def test_pipeline_with_own_attention_backward(monkeypatch):
+    """RRFP_ATTN_BWD=own: the tcgen05 attention backward inside the captured bodies."""
+    monkeypatch.setenv("RRFP_ATTN_BWD", "own")
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, 2, 4, hint="bfw", mode="free")
+    try:
+        assert all(st.own_attn_bwd for st in pipe.stages)
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()

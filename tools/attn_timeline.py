@@ -12,7 +12,11 @@ import torch
 NAMES = {0: "sm:wait_S", 1: "sm:S_ready", 2: "sm:S_loaded", 3: "sm:P_written", 4: "sm:P_arrived",
          5: "sm:max_done", 6: "sm:max_exchanged", 7: "sm:exp_chunk_done", 8: "sm:P_chunk_stored", 9: "sm:exp_start",
          10: "mma:wait_tile", 11: "mma:tile_ready", 12: "mma:wait_P", 13: "mma:P_ready",
-         20: "tma:wait_slot", 21: "tma:slot_free"}
+         20: "tma:wait_slot", 21: "tma:slot_free",
+         14: "mma:wait_dS", 15: "mma:dS_ready", 16: "mma:wait_dqbuf", 17: "mma:dqbuf_free", 18: "mma:grads_issued",
+         30: "rd:wait_dQ", 31: "rd:dQ_ready", 32: "rd:reduce_issued"}
+BWD_NAMES = {10: "mma:wait_stage", 11: "mma:stage_ready", 12: "mma:sd_free", 13: "mma:SD_issued",
+             0: "ew:wait_S", 1: "ew:S_ready", 2: "ew:computed", 3: "ew:pds_free", 4: "ew:dS_stored", 5: "ew:S_loaded"}
 
 
 def main():
@@ -20,6 +24,7 @@ def main():
     ap.add_argument("--cta", type=int, nargs="+", default=[0, 112])
     ap.add_argument("--T", type=int, default=2048)
     ap.add_argument("--H", type=int, default=16)
+    ap.add_argument("--bwd", action="store_true")
     a = ap.parse_args()
     from paper_2605_18750_b200 import _lib, kernels as K
     L = _lib.lib()
@@ -29,10 +34,21 @@ def main():
     lse = torch.empty(H, T, device="cuda")
     for _ in range(3):
         K.attn_fwd(qkv, o, lse, heads=H)
+    if a.bwd:
+        os.environ["RRFP_ATTN_DEBUG_BWD"] = "1"
+        NAMES.update(BWD_NAMES)
+        do = torch.randn(T, D, device="cuda").to(torch.bfloat16)
+        dqkv = torch.empty(T, 3 * D, device="cuda", dtype=torch.bfloat16)
+        ws = K.attn_bwd_workspace(T, H)
+        for _ in range(3):
+            K.attn_bwd(qkv, o, do, lse, dqkv, ws, heads=H)
     for cta in a.cta:
         buf = torch.zeros(4, 512, dtype=torch.int64, device="cuda")
         L.rrfp_attn_debug(C.c_void_p(buf.data_ptr()), cta)
-        K.attn_fwd(qkv, o, lse, heads=H)
+        if a.bwd:
+            K.attn_bwd(qkv, o, do, lse, dqkv, ws, heads=H)
+        else:
+            K.attn_fwd(qkv, o, lse, heads=H)
         torch.cuda.synchronize()
         L.rrfp_attn_debug(C.c_void_p(0), 0)
         ev = []
@@ -45,7 +61,8 @@ def main():
         t0 = ev[0][0]
         print(f"=== CTA {cta}: {len(ev)} events, span {ev[-1][0] - t0} cycles")
         for t, s, code, j in ev:
-            print(f"{t - t0:8d}  {'TMA MMA SM0 SM1'.split()[s]:4s} {NAMES.get(code, code):16s} {j}")
+            lab = ('TMA MMA EW RD' if a.bwd else 'TMA MMA SM0 SM1').split()[s]
+            print(f"{t - t0:8d}  {lab:4s} {NAMES.get(code, code):16s} {j}")
 
 
 if __name__ == "__main__":
