@@ -509,7 +509,8 @@ def build_pipe(cfg, args, hint, mode, world, jitter, comm_delay=None):
 B_IN_FRAC, W_FRAC = 0.714, 0.307
 
 
-def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8), device="cuda"):
+def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8), device="cuda", grid=True,
+                   grid_sigmas=(0.0, 0.1, 0.2, 0.3, 0.4, 0.5), grid_levels=("J0", "J1", "J2", "J3")):
     """Virtual-clock prediction of the PP sweep from THIS run's B200 task times
     (SURVEY 6.3 / 8d C5): per-layer F and B durations of the measured run,
     balanced layer split, LM head on the last stage, lognormal(0, sigma)
@@ -540,44 +541,100 @@ def pipeline_model(args, cfg, task_us, n_meas, sigmas=(0.0, 0.5), pps=(2, 4, 8),
         f_h, b_h = 1.6 * f_l, 1.27 * b_l
     out = {"definition": pipeline_model.__doc__.split("\n\n")[0].strip().replace("\n", " "),
            "per_layer_us": {"F": round(f_l, 1), "B": round(b_l, 1)}, "head_us": {"F": round(f_h, 1), "B": round(b_h, 1)}}
+    from paper_2605_18750_b200.jitter import PRESETS, build_injection_table
+
+    def point(n, lay, sigma, jname, seed=0):
+        res = {}
+        for name in ("1f1b", "bf", "bfw"):
+            dec = name == "bfw"
+            lat = {}
+            for s_ in range(n):
+                for mb in range(args.mb):
+                    x = float(np.exp(substream(11, "cjitter", s_, mb, "F").normal(0.0, sigma))) if sigma else 1.0
+                    y = float(np.exp(substream(11, "cjitter", s_, mb, "B").normal(0.0, sigma))) if sigma else 1.0
+                    fd = (f_l * lay[s_] + (f_h if s_ == n - 1 else 0)) * x
+                    bd = (b_l * lay[s_] + (b_h if s_ == n - 1 else 0)) * y
+                    lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(fd))
+                    if dec:
+                        # B-input / W as fractions of the fused B (captured bodies of
+                        # an interior stage, profiles/r01_task_times_ln_in_w.txt: 274 + 118 vs 384)
+                        lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(B_IN_FRAC * bd))
+                        lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(W_FRAC * bd))
+                    else:
+                        lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(bd))
+            comm = P.CommDelay()
+            if sigma:
+                comm = P.CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
+                                   hi=int(args.comm_us * 50), seed=17)
+            w = P.Workload(num_stages=n, num_microbatches=args.mb, num_chunks=1, tp_group_size=1,
+                           latency=lat, comm_delay=comm, decompose_backward=dec)
+            jc = PRESETS[jname]
+            if name == "1f1b":
+                inj = build_injection_table(w, jc, seed) if jc.enabled else None
+                tr, m = P.run_fixed(P.build_1f1b_schedule(w), w, injected_delays=inj, record_trace=False,
+                                    device=device)
+            else:
+                tr, m = P.run_rrfp(w, name, 32, seed, jitter=jc, record_trace=False, device=device)
+            res[name] = {"ms": round(m.makespan / 1e3, 2), "bubble": round(m.bubble_fraction(), 4)}
+        for name in ("bf", "bfw"):
+            res[name]["speedup_vs_1f1b"] = round(res["1f1b"]["ms"] / res[name]["ms"], 4)
+        return res
+
     for n in pps:
         lay = [round(layer_eq(n, s_), 2) for s_ in range(n)]
         row = {"layers": lay}
         for sigma in sigmas:
-            res = {}
-            for name in ("1f1b", "bf", "bfw"):
-                dec = name == "bfw"
-                lat = {}
-                for s_ in range(n):
-                    for mb in range(args.mb):
-                        x = float(np.exp(substream(11, "cjitter", s_, mb, "F").normal(0.0, sigma))) if sigma else 1.0
-                        y = float(np.exp(substream(11, "cjitter", s_, mb, "B").normal(0.0, sigma))) if sigma else 1.0
-                        fd = (f_l * lay[s_] + (f_h if s_ == n - 1 else 0)) * x
-                        bd = (b_l * lay[s_] + (b_h if s_ == n - 1 else 0)) * y
-                        lat[P.TaskId(s_, mb, 0, "F")] = max(1, int(fd))
-                        if dec:
-                            # B-input / W as fractions of the fused B (captured bodies of
-                            # an interior stage, profiles/r01_task_times_ln_in_w.txt: 274 + 118 vs 384)
-                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(B_IN_FRAC * bd))
-                            lat[P.TaskId(s_, mb, 0, "W")] = max(1, int(W_FRAC * bd))
-                        else:
-                            lat[P.TaskId(s_, mb, 0, "B")] = max(1, int(bd))
-                comm = P.CommDelay()
-                if sigma:
-                    comm = P.CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
-                                       hi=int(args.comm_us * 50), seed=17)
-                w = P.Workload(num_stages=n, num_microbatches=args.mb, num_chunks=1, tp_group_size=1,
-                               latency=lat, comm_delay=comm, decompose_backward=dec)
-                if name == "1f1b":
-                    tr, m = P.run_fixed(P.build_1f1b_schedule(w), w, device=device)
-                else:
-                    tr, m = P.run_rrfp(w, name, 32, 0, device=device)
-                res[name] = {"ms": round(m.makespan / 1e3, 2), "bubble": round(m.bubble_fraction(), 4)}
-            for name in ("bf", "bfw"):
-                res[name]["speedup_vs_1f1b"] = round(res["1f1b"]["ms"] / res[name]["ms"], 4)
-            row[f"sigma{sigma}"] = res
+            row[f"sigma{sigma}"] = point(n, lay, sigma, "J0")
         out[f"pp{n}"] = row
+    if grid and 8 in pps:
+        # the (sigma x J-preset) operating grid at PP=8 --
+        # where does BFW / 1F1B reach the north star's 1.5x with these kernels?
+        lay = out["pp8"]["layers"]
+        g = {"sigmas": list(grid_sigmas), "levels": list(grid_levels), "bfw_speedup": {}, "bf_speedup": {},
+             "bubble_1f1b": {}, "bubble_bfw": {}}
+        for jname in grid_levels:
+            for key in ("bfw_speedup", "bf_speedup", "bubble_1f1b", "bubble_bfw"):
+                g[key][jname] = []
+            for sigma in grid_sigmas:
+                r = point(8, lay, sigma, jname)
+                g["bfw_speedup"][jname].append(r["bfw"]["speedup_vs_1f1b"])
+                g["bf_speedup"][jname].append(r["bf"]["speedup_vs_1f1b"])
+                g["bubble_1f1b"][jname].append(r["1f1b"]["bubble"])
+                g["bubble_bfw"][jname].append(r["bfw"]["bubble"])
+        g["points_bfw_ge_1p5"] = [[j, sg] for j in grid_levels
+                                  for sg, v in zip(grid_sigmas, g["bfw_speedup"][j]) if v >= 1.5]
+        out["pp8_grid"] = g
     return out
+
+
+def replay_prediction(pipe, name, sigma, nominal, floor_seed=11):
+    """What the virtual-clock engine predicts for an emulated variant (ms):
+    the device replay kernel on the variant's own workload -- its measured
+    clean per-task means as latencies, the lanes' J-preset injection table and
+    per-edge comm delays -- with every task lasting max(nominal + pad, nominal
+    * X), the K11 rule (rrfp_exec.cu lane_complete) with the same lognormal
+    draws X (pipeline.lognormal_floor_tables).  Model vs measurement."""
+    import paper_2605_18750_b200 as P
+    from paper_2605_18750_b200.pipeline import lognormal_floor_tables
+    from paper_2605_18750_b200.tables import DIR_IDX, key_of
+    g = pipe.group
+    w = g.w
+    floors = lognormal_floor_tables(pipe.N, pipe.M, nominal, sigma, floor_seed, n_chunks=pipe.C)
+    mw = (w.num_microbatches + 31) // 32
+    inj = {}
+    for t, lat in w.latency.items():
+        pad = g.injected.get(t, 0)
+        fl = floors[t.stage][DIR_IDX[t.direction], key_of(t.microbatch, t.chunk, mw)] if sigma > 0 else 0.0
+        inj[t] = int(max(lat + pad, fl) - lat)
+    if name == "1f1b":
+        _, m = P.run_fixed(P.build_1f1b_schedule(w), w, injected_delays=inj, record_trace=False)
+    else:
+        from paper_2605_18750_b200.engine import build_trace_metrics, replay_tables
+        from paper_2605_18750_b200.tables import lower
+        tb = lower(w, g.hint, g.tables.desc.buffer_limit, g._seed, None, g._tp, injected=inj)
+        ev, res = replay_tables(tb)
+        _, m = build_trace_metrics(w, ev, res, record_trace=False)
+    return round(m.makespan / 1e3, 2)
 
 
 def emulated_pp(args, cfg):
@@ -591,20 +648,30 @@ def emulated_pp(args, cfg):
     import gc
     import math
     import torch
-    from paper_2605_18750_b200.jitter import PRESETS
+    from paper_2605_18750_b200.jitter import PRESETS, JitterConfig
     from paper_2605_18750_b200.pipeline import GpuPipeline
     from paper_2605_18750_b200.runtime import dispatch_latency
     from paper_2605_18750_b200.workload import CommDelay
     N = args.emulate_pp
     cap = (torch.cuda.get_device_properties(0).multi_processor_count // N) & ~1
     combos = jitter_combos(args)
+    # a stage on 148/N SMs runs ~N x slower than on its own GPU: the absolute-us
+    # parts of the jitter (J-preset base delay, jitter.py:55-60; the lognormal
+    # comm-delay median) are stretched by the same factor so the emulated pads
+    # relate to the task times as they would on N GPUs (1 = unscaled)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    jscale = args.emu_jitter_scale if args.emu_jitter_scale > 0 else n_sm / cap
+
+    def preset(jname):
+        j = PRESETS[jname]
+        return JitterConfig(j.probability, int(round(j.base_delay * jscale)), j.scale, j.level)
     out = {"n_stages": N, "gemm_sm_cap": cap, "green_partitions": bool(args.green),
            "definition": emulated_pp.__doc__.split("\n\n")[0].replace("\n", " ").replace("    ", " "),
-           "variants": {}}
+           "jitter_time_scale": round(jscale, 3), "variants": {}}
     cur = torch.cuda.current_stream()
     for name, hint, mode in (("1f1b", "bf", "fixed"), ("bf", "bf", "free"), ("bfw", "bfw", "free")):
         t0 = time.perf_counter()
-        pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=PRESETS[combos[0][0]],
+        pipe = GpuPipeline(cfg, N, args.mb, hint=hint, mode=mode, jitter=preset(combos[0][0]),
                            head_cost=args.head_cost, gemm_sm_cap=cap, w_split=args.w_split,
                            green=args.green, split=stage_split(args))
         out["gemm_sm_cap"] = getattr(pipe, "green_sms", cap) if args.green else cap
@@ -614,11 +681,12 @@ def emulated_pp(args, cfg):
         nominal = pipe.nominal_us()
         pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
         for jname, sigma in combos:
-            pipe.group.set_jitter(PRESETS[jname])
+            pipe.group.set_jitter(preset(jname))
             comm = CommDelay()
             if sigma > 0:
-                comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
-                                 hi=int(args.comm_us * 50), seed=17)
+                cu = args.comm_us * jscale
+                comm = CommDelay(kind="lognormal", mu=math.log(cu), sigma=sigma, lo=0,
+                                 hi=int(cu * 50), seed=17)
             pipe.group.set_comm_delay(comm)
             pipe.set_lognormal_jitter(sigma, seed=11, nominal_us=nominal)
             pipe.step()
@@ -645,6 +713,12 @@ def emulated_pp(args, cfg):
                 # all N stages share this GPU's power budget: a schedule that keeps
                 # more stages busy runs at a lower SM clock than on N separate GPUs
                 "sm_mhz": clk.summary()["sm_mhz"]}
+            try:
+                pred = replay_prediction(pipe, name, sigma, nominal)
+                out["variants"][f"{name}@{jname}+sigma{sigma}"]["model_ms"] = pred
+                out["variants"][f"{name}@{jname}+sigma{sigma}"]["model_err"] = round(ms / pred - 1.0, 4)
+            except Exception as exc:      # a model failure must not void the measurement
+                _log(f"replay prediction failed: {exc!r}")
             _log(f"emulated PP={N} {name} {jname} sigma={sigma}: {ms:.1f} ms")
         pipe.close()
         del pipe
@@ -706,7 +780,7 @@ def timed_steps(pipe, steps, dist, barrier):
 def jitter_combos(args):
     """(J-preset, sigma) operating points of the comparison runs: the first
     --compare-jitter preset at every --sigmas value (0 always included), each
-    further preset at the largest sigma (default: J0 x {0, 0.5} + J3 x 0.5,
+    further preset at the largest sigma (default: J0 x {0, 0.5} + J2, J3 x 0.5,
     the regime SURVEY 6.3 puts the >= 1.5x target in)."""
     js = [j for j in args.compare_jitter.split(",") if j]
     sigmas = sorted({0.0, *[float(x) for x in args.sigmas.split(",") if x]})
@@ -743,11 +817,12 @@ def compare_variants(cfg, args, world, dist, barrier):
         nominal = pipe.nominal_us()
         pipe.set_nominal_latency(nominal)      # J-preset pads scale with the measured task times
         for jname, sigma in combos:
-            pipe.group.set_jitter(PRESETS[jname])
+            pipe.group.set_jitter(preset(jname))
             comm = CommDelay()
             if sigma > 0:
-                comm = CommDelay(kind="lognormal", mu=math.log(args.comm_us), sigma=sigma, lo=0,
-                                 hi=int(args.comm_us * 50), seed=17)
+                cu = args.comm_us * jscale
+                comm = CommDelay(kind="lognormal", mu=math.log(cu), sigma=sigma, lo=0,
+                                 hi=int(cu * 50), seed=17)
             pipe.group.set_comm_delay(comm)
             pipe.set_lognormal_jitter(sigma, seed=11, nominal_us=nominal)
             pipe.step()
@@ -975,7 +1050,10 @@ def main():
     ap.add_argument("--sigmas", default="0.5",
                     help="comma list of lognormal compute+comm jitter sigmas of the comparison runs "
                          "(config 5 sweep: 0,0.1,0.2,0.3,0.4,0.5); sigma 0 is always included")
-    ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0,J3",
+    ap.add_argument("--emu-jitter-scale", dest="emu_jitter_scale", type=float, default=0.0,
+                    help="emulated PP: stretch the J-preset base delay and the comm-delay median by this "
+                         "factor (0 = auto: SMs of the GPU / SMs of a stage partition)")
+    ap.add_argument("--compare-jitter", dest="compare_jitter", default="J0,J2,J3",
                     help="comma list of J-preset jitter tables (jitter.py PRESETS) for the comparison runs: "
                          "the first at every --sigmas value, the others at the largest sigma")
     ap.add_argument("--comm-us", dest="comm_us", type=float, default=100.0)

@@ -319,6 +319,14 @@ int rrfp_gemm_set_multicast(int on);
 int rrfp_gemm_max_clusters(int mc);
 /* pair-kernel k-block depth: 64 (6-stage ring, default) or 128 (3 stages). */
 int rrfp_gemm_set_bk(int bk);
+/* GEMMs whose 256x256 tiles fill less than one wave of CTA pairs (bit mask,
+   default 0 -- both modes measured slower; env RRFP_GEMM_SMALL): 1 = f32-accumulate outputs stream-K over
+   every pair (each k-segment reduce-adds its partial tile), 2 = other outputs
+   as 256x128 halves. */
+int rrfp_gemm_set_small(int mode);
+/* 1 (default): the bf16 epilogues load R (residual / GELU pre-activation) one
+   32-column chunk ahead; 0: where used. */
+int rrfp_gemm_set_rpref(int on);
 /* LayerNorm / embedding / bias-grad / softmax cross-entropy (csrc/ops.cu). */
 int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
                        int rows, int D, float eps, void* stream);

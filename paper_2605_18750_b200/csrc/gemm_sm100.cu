@@ -80,6 +80,7 @@ struct GemmArgs {
   // a full one (256 tiles on 74 pairs: 3.5 tile times instead of 4).  -1: off.
   int half_rounds;
   int half_tail;
+  int rpref;   // 1: epilogue loads R one 32-column chunk ahead (env RRFP_GEMM_RPREF, default 1)
 };
 
 enum Role : int { ROLE_FULL = 0, ROLE_OWNER = 1, ROLE_PARTIAL = 2 };
@@ -116,7 +117,7 @@ __device__ __forceinline__ bool get_unit(const GemmArgs& g, int num_tiles, int k
   if (!g.sk_W) {
     if (g.half_rounds >= 0 && i >= g.half_rounds) {
       const int h = cid + (i - g.half_rounds) * C;
-      if (i > g.half_rounds || h >= 2 * g.half_tail) return false;
+      if (h >= 2 * g.half_tail) return false;   // (several rounds when every tile runs as halves)
       const int t = g.half_rounds * C + (h >> 1);
       u.tile = t; u.k0 = 0; u.k1 = kblocks; u.role = ROLE_FULL; u.tail = 0; u.first = 0;
       u.n0 = (t / g.tiles_m) * 256 + (h & 1) * 128; u.bn = 128;
@@ -275,6 +276,67 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& g, int row, int col0, 
           if (EPI == EPI_RESID) v[j] += x;
           else v[j] *= gelu_tanh_grad(x);
         }
+      }
+    }
+  }
+}
+
+// Residual / pre-activation operand of one 32-column chunk, loaded ahead of use
+// (the epilogue issues chunk c+1's loads before it works on chunk c, so the L2
+// latency of R is hidden behind the TMEM read-out and the stores instead of
+// being paid once per chunk: on a GEMM with one tile per CTA the whole
+// epilogue is exposed).  Rows / columns outside C load zeros.
+template <int EPI>
+__device__ __forceinline__ void epi_load_r(const GemmArgs& g, int row, int col0, uint4 (&q)[4]) {
+  if (EPI != EPI_RESID && EPI != EPI_GELU_BWD) return;
+  if (row < g.M && g.vec && col0 + 32 <= g.N) {
+    const __nv_bfloat16* rp = g.R + (size_t)row * g.ldr + col0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = __ldcg(reinterpret_cast<const uint4*>(rp + 8 * j));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// epi_apply with the R chunk already in registers (full vector chunks only;
+// ragged chunks take epi_apply's scalar path)
+template <int EPI>
+__device__ __forceinline__ void epi_apply_q(const GemmArgs& g, int row, int col0, float (&v)[32],
+                                            const uint4 (&q)[4]) {
+  if (EPI != EPI_RESID && EPI != EPI_GELU_BWD) { epi_apply<EPI>(g, row, col0, v); return; }
+  if (row >= g.M || col0 >= g.N) return;
+  if (!(g.vec && col0 + 32 <= g.N)) { epi_apply<EPI>(g, row, col0, v); return; }
+  if (g.bias && EPI != EPI_GELU_BWD) {
+    if (g.vec_bias) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 b = __ldg(reinterpret_cast<const uint4*>(g.bias + col0 + j));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float2 f = __bfloat1622float2(h[t]);
+          v[j + 2 * t] += f.x;
+          v[j + 2 * t + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += __bfloat162float(g.bias[col0 + j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 x = __bfloat1622float2(h[t]);
+      if (EPI == EPI_RESID) {
+        v[8 * j + 2 * t] += x.x;
+        v[8 * j + 2 * t + 1] += x.y;
+      } else {
+        v[8 * j + 2 * t] *= gelu_tanh_grad(x.x);
+        v[8 * j + 2 * t + 1] *= gelu_tanh_grad(x.y);
       }
     }
   }
@@ -729,6 +791,11 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
       const int row = row0 + lane;
       int* cnt = g.cnt ? g.cnt + u.tail * 8 + rank * 4 + ew : nullptr;
       if (u.role != ROLE_PARTIAL) epilogue_prefetch<EPI>(g, row, u.n0, u.bn);
+      uint4 qn[2][4];   // R of the next two 32-column chunks (EPI_RESID / EPI_GELU_BWD, TMA-store path)
+      if (g.rpref && g.tma_st && u.role != ROLE_PARTIAL) {
+        epi_load_r<EPI>(g, row, u.n0, qn[0]);
+        epi_load_r<EPI>(g, row, u.n0 + 32, qn[1]);
+      }
       sm100::mbar_wait(&tfull[acc], acc_phase);
       sm100::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * P_BN;
@@ -806,7 +873,9 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
           ++unit;
         }
       } else {
-        // 64 bf16 columns per box (two TMEM chunks); GELU also stages gelu(C) for C2
+        // 64 bf16 columns per box (two TMEM chunks); GELU also stages gelu(C) for C2.
+        // R (residual / pre-activation) runs one 32-column chunk ahead in qn[h]
+        // (its first chunk was requested before the accumulator wait, below).
 #pragma unroll 1
         for (int c = 0; c < u.bn; c += 64) {
           const int col = u.n0 + c;
@@ -822,7 +891,12 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
             if (u.role == ROLE_OWNER) ws_add(g, u, cluster_id, rank, (c >> 5) + h, ew, lane, v);
-            epi_apply<EPI>(g, row, col + 32 * h, v);
+            if (g.rpref) {
+              epi_apply_q<EPI>(g, row, col + 32 * h, v, qn[h]);
+              if (c + 64 < u.bn) epi_load_r<EPI>(g, row, col + 64 + 32 * h, qn[h]);
+            } else {
+              epi_apply<EPI>(g, row, col + 32 * h, v);
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               w[16 * h + j] = pack_bf16(v[2 * j], v[2 * j + 1]);
@@ -958,6 +1032,25 @@ std::map<std::pair<int, cudaStream_t>, SkWorkspace> g_ws;
 // traffic at 1.8 GHz), not by wave quantization, so idle SMs in the last round cost
 // little and the fix-up traffic of the split costs more (-10% on one layer).
 int g_tail_split = 1;   // half-width last wave (rrfp_gemm_set_tail_split)
+// Shapes whose tiles fill less than one wave of CTA pairs (2048^3: 64 tiles on
+// 74 pairs; rrfp_gemm_set_small, env RRFP_GEMM_SMALL, bit mask, default 0 --
+// both measured SLOWER than the two-pair multicast clusters on one B200,
+// profiles/r02_gemm_small_ab.txt: halves 17.8 -> 25.9 us on the 2048^3 dgrad
+// (a 256x128 half reads all of A for half the MMAs: L2 -> SM bound), stream-K
+// 18.5 -> 20.8 us on the 2048^3 wgrad (partial-tile reduce-add traffic)):
+//   1: f32-accumulate outputs (weight gradients) run stream-K over every pair;
+//      each k-segment TMA-reduce-adds its partial tile itself, no fix-up
+//   2: other outputs run as 256x128 halves (twice the units: the epilogue of
+//      a CTA's first half overlaps the MMAs of its second)
+int g_small = -1;
+int g_rpref = -1;   // R operand loaded one chunk ahead in the bf16 epilogues (rrfp_gemm_set_rpref)
+int small_mode() {
+  if (g_small < 0) {
+    const char* e = getenv("RRFP_GEMM_SMALL");
+    g_small = e ? atoi(e) : 0;
+  }
+  return g_small;
+}
 int g_mc = 1;           // 2-pair clusters with A multicast (rrfp_gemm_set_multicast)
 int g_streamk = -1;
 
@@ -1042,7 +1135,12 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   g.tiles_n = (g.N + P_BN - 1) / P_BN;
   // (not under an SM cap: a capped grid shares the GPU, possibly inside a green-context
   // partition, where 4-CTA clusters may not be placeable)
-  if (PBK == 64 && g_mc && g_reserve_sms == 0 && g.tiles_n > 1)
+  const bool direct_acc = EPI == EPI_ACC_F32 && g.accumulate && (g.tma_st || g.vec);
+  int all_pairs = (g_num_sms - g_reserve_sms) / 2;
+  const int tiles0 = g.tiles_m * g.tiles_n;
+  const bool small = g_reserve_sms == 0 && tiles0 < all_pairs &&
+                     (direct_acc ? (small_mode() & 1) : ((small_mode() & 2) && g_tail_split));
+  if (!small && PBK == 64 && g_mc && g_reserve_sms == 0 && g.tiles_n > 1)
     return launch_pair_mc<EPI, A_MN, B_MN, PBK>(ta, tb, tc, tc2, tbh, tah, g, st);
   auto kern = gemm_bf16_sm100_pair<EPI, A_MN, B_MN, PBK, 1>;
   static bool attr = false;
@@ -1061,6 +1159,22 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   g.half_rounds = -1; g.half_tail = 0;
   int grid = 2 * (tiles < pairs ? tiles : pairs);
   const int tail = tiles % pairs;
+  if (small && direct_acc) {
+    // every k-block of every tile split evenly over all pairs (reduce-add epilogue)
+    g.sk_full = 0;
+    g.sk_W = tiles * kblocks;
+    grid = 2 * pairs;
+    RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, tah, g));
+    return RRFP_OK;
+  }
+  if (small) {
+    // every tile as two 256x128 halves, rounds of `pairs` halves
+    g.half_rounds = 0;
+    g.half_tail = tiles;
+    grid = 2 * (2 * tiles < pairs ? 2 * tiles : pairs);
+    RRFP_CUDA_TRY(rrfp_launch(kern, dim3(grid), dim3(256), P_SMEM_BYTES, st, ta, tb, tc, tc2, tbh, tah, g));
+    return RRFP_OK;
+  }
   if (g_tail_split && tail != 0 && 2 * tail <= pairs) {
     // last partial wave as 256x128 halves: ceil(tiles / pairs) - 0.5 tile times
     g.half_rounds = tiles / pairs;
@@ -1156,6 +1270,11 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   g.bias = (const __nv_bfloat16*)bias;
   g.R = (const __nv_bfloat16*)R; g.ldr = ldr;
   g.accumulate = accumulate;
+  if (g_rpref < 0) {
+    const char* e = getenv("RRFP_GEMM_RPREF");
+    g_rpref = e ? atoi(e) : 1;
+  }
+  g.rpref = g_rpref;
   const int esz = (epi == EPI_ACC_F32 || epi == EPI_F32) ? 4 : 2;
   g.vec = ((uintptr_t)C % 16 == 0) && ((ldc * esz) % 16 == 0) &&
           (!C2 || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
@@ -1223,6 +1342,20 @@ extern "C" int rrfp_gemm_max_clusters(int mc) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES) != cudaSuccess)
       return rrfp_fail(RRFP_E_CUDA, "cudaFuncSetAttribute failed");
   return mc == 2 ? max_clusters(k2, 4) : max_clusters(k1, 2);
+}
+
+// sub-wave shapes (see g_small): bit 1 stream-K for f32 accumulate, bit 2 half tiles
+extern "C" int rrfp_gemm_set_small(int mode) {
+  g_small = mode < 0 ? 0 : mode;
+  return RRFP_OK;
+}
+
+// 1 (default) = residual / pre-activation loads run one 32-column chunk ahead
+// in the bf16 epilogues (first chunk before the accumulator wait), 0 = loaded
+// where used
+extern "C" int rrfp_gemm_set_rpref(int on) {
+  g_rpref = on ? 1 : 0;
+  return RRFP_OK;
 }
 
 // 1 = CTA-pair (cta_group::2) kernel, 0 = single-CTA kernel

@@ -400,7 +400,22 @@ class StageCompute:
             self.head = init_head_params(cfg, dev, seed) if self.last else None
             self.pe = init_mm_params(mm, dev, seed, "pe") if self.prologue == "patches" else None
             self.proj = init_mm_params(mm, dev, seed, "proj") if self.epilogue == "projector" else None
-        zeros = lambda d: {k: torch.zeros(v.shape, device=dev) for k, v in d.items()} if d else None
+        # every fp32 gradient is a view of ONE flat buffer (each view 1 KiB aligned for
+        # the TMA reduce-add epilogues), so zero_grads() is a single memset
+        groups = [*self.p, self.emb, self.head, self.pe, self.proj]
+        align = 256
+        total = sum((v.numel() + align - 1) // align * align for d in groups if d for v in d.values())
+        self.grad_flat = torch.zeros(max(total, 1), device=dev)
+        off = [0]
+
+        def zeros(d):
+            if not d:
+                return None
+            out = {}
+            for k, v in d.items():
+                out[k] = self.grad_flat[off[0]:off[0] + v.numel()].view(v.shape)
+                off[0] += (v.numel() + align - 1) // align * align
+            return out
         self.g = [zeros(p) for p in self.p]
         self.g_emb, self.g_head = zeros(self.emb), zeros(self.head)
         self.g_pe, self.g_proj = zeros(self.pe), zeros(self.proj)
@@ -935,10 +950,7 @@ class StageCompute:
                 setattr(self, k, None)
 
     def zero_grads(self):
-        extra = [d for d in (self.g_emb, self.g_head, self.g_pe, self.g_proj) if d]
-        for gd in self.g + extra:
-            for t in gd.values():
-                t.zero_()
+        self.grad_flat.zero_()
         if self.last:
             self.loss.zero_()
 

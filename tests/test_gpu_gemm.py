@@ -5,26 +5,31 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[(1, 1, 64, 0, 1), (1, 1, 128, 0, 1), (1, 2, 64, 0, 1), (1, 0, 64, 0, 1), (0, 0, 64, 0, 1),
-                        (1, 1, 64, 1, 1), (1, 2, 64, 1, 1), (1, 1, 64, 0, 0)],   # (pair, epilogue, bk, multicast, tail)
+@pytest.fixture(params=[(1, 1, 64, 0, 1, 3), (1, 1, 128, 0, 1, 3), (1, 2, 64, 0, 1, 3), (1, 0, 64, 0, 1, 3),
+                        (0, 0, 64, 0, 1, 3), (1, 1, 64, 1, 1, 3), (1, 2, 64, 1, 1, 3), (1, 1, 64, 0, 0, 3),
+                        (1, 1, 64, 1, 1, 0), (1, 2, 64, 1, 1, 0)],   # (small = 3: the measured-slower modes, kept tested)
+                # (pair, epilogue, bk, multicast, tail, small: sub-wave shapes as halves / stream-K)
                 ids=["pair-tma-store", "pair-bk128", "pair-staged-coalesced", "pair-st-global", "single",
-                     "pair-multicast", "pair-multicast-coalesced", "pair-full-last-wave"],
+                     "pair-multicast", "pair-multicast-coalesced", "pair-full-last-wave",
+                     "pair-multicast-default", "pair-multicast-coalesced-default"],
                 autouse=True)
 def variant(request):
     from paper_2605_18750_b200 import _lib
-    pair, tma, bk, mc, tail = request.param
+    pair, tma, bk, mc, tail, small = request.param
     L = _lib.lib()
     L.rrfp_gemm_set_variant(pair)
     L.rrfp_gemm_set_epilogue(tma)
     L.rrfp_gemm_set_bk(bk)
     L.rrfp_gemm_set_multicast(mc)
     L.rrfp_gemm_set_tail_split(tail)
+    L.rrfp_gemm_set_small(small)
     yield request.param
     L.rrfp_gemm_set_variant(1)
     L.rrfp_gemm_set_epilogue(1)
     L.rrfp_gemm_set_bk(64)
     L.rrfp_gemm_set_multicast(1)
     L.rrfp_gemm_set_tail_split(1)
+    L.rrfp_gemm_set_small(0)
 
 
 def _rand(*shape, scale=1.0):
@@ -174,3 +179,24 @@ def test_gemm_streamk_fixup_all_epilogues(pairs, variant):
     finally:
         L.rrfp_gemm_reserve_sms(0)
         L.rrfp_gemm_set_streamk(0)
+
+
+def test_gemm_out_projection_2048_cube():
+    """The three 2048^3 GEMMs of the attention out-projection (64 tiles: less
+    than one wave of CTA pairs): forward + bias + residual, dgrad, wgrad +=."""
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(7)
+    S = D = 2048
+    x, w, bias, res = _rand(S, D), _rand(D, D, scale=0.05), _rand(D), _rand(S, D)
+    y = torch.empty(S, D, device="cuda", dtype=torch.bfloat16)
+    Kn.gemm(x, w, y, epi=Kn.EPI_RESID, bias=bias, r=res)
+    dy = _rand(S, D)
+    dx = torch.empty(S, D, device="cuda", dtype=torch.bfloat16)
+    Kn.gemm(dy, w, dx, b_mn=True)
+    gw = torch.randn(D, D, device="cuda")
+    want_gw = gw + dy.float().t() @ x.float()
+    Kn.gemm(dy, x, gw, epi=Kn.EPI_ACC_F32, a_mn=True, b_mn=True, accumulate=True)
+    torch.cuda.synchronize()
+    _close(y, x.float() @ w.float().t() + bias.float() + res.float())
+    _close(dx, dy.float() @ w.float())
+    _close(gw, want_gw, 1e-2)
