@@ -447,6 +447,16 @@ def run_ours(args):
             "build_s": round(t_build, 1),
             "clock_calibration": clock_cal,
             "clocks": clk.summary()}
+    # dispatcher profile: one more (untimed) iteration with lane_step_kernel's own
+    # %globaltimer stamps (ncu cannot profile kernel nodes of conditional graphs)
+    try:
+        from paper_2605_18750_b200.runtime import dispatcher_profile
+        pipe.group.enable_profile(16384)
+        pipe.step()
+        line["dispatch"]["step_kernel"] = dispatcher_profile(pipe.group.profile())
+        pipe.group.enable_profile(0)
+    except Exception as e:     # a profile must never cost the measurement
+        line["dispatch"]["step_kernel"] = {"error": repr(e)[:200]}
     if rank == 0 and args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, task_us)
     if rank == 0 and args.model != "mm" and args.tp == 1 and args.chunks == 1:

@@ -289,6 +289,13 @@ int rrfp_runtime_status(rrfp_runtime* rt, char* dump, size_t cap);
 int rrfp_runtime_declog(rrfp_runtime* rt, uint32_t* out, int32_t cap_words, int32_t* n_records,
                         int32_t* stride_words);
 
+/* Dispatcher profile (free mode): cap > 0 records, for the next iterations,
+ * one record per lane_step_kernel run: uint64 {entry, completion done, decision
+ * made (%globaltimer ns), kind << 32 | view polls}; cap = 0 disables.  (ncu does
+ * not profile kernel nodes of graphs with conditional nodes.) */
+int rrfp_runtime_profile(rrfp_runtime* rt, int32_t cap);
+int rrfp_runtime_profile_read(rrfp_runtime* rt, uint64_t* out, int32_t cap, int32_t* n_records);
+
 /* ---- stage-compute kernel entry points (unit-test surface) ------------- */
 
 /* Stage GEMM (tcgen05/TMA, csrc/gemm_sm100.cu): C[M,N] = sum_k A(m,k) B(n,k),
@@ -334,6 +341,13 @@ int rrfp_layernorm_fwd(const void* x, const void* g, const void* b, void* y, flo
 int rrfp_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                        const void* g, const void* dres, void* dx, float* dg, float* db, int rows,
                        int D, void* stream);
+/* layernorm_bwd_fused: one pass over a slab of rows per CTA computing any of
+   dx (+ dres), the parameter gradients dg/db (+=) and the column sums
+   cs_res += sum_r dres, cs_dx += sum_r dx (the bias gradients of the linear
+   layers on either side of the residual); NULL skips an output.  D <= 4096. */
+int rrfp_layernorm_bwd_fused(const void* dy, const void* x, const float* mean, const float* rstd,
+                             const void* g, const void* dres, void* dx, float* dg, float* db,
+                             float* cs_res, float* cs_dx, int rows, int D, void* stream);
 int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x, int rows, int D,
                        void* stream);
 int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP, int rows, int D,
@@ -341,6 +355,12 @@ int rrfp_embedding_bwd(const int32_t* tok, const void* dx, float* dE, float* dP,
 int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows, int cols, void* stream);
 int rrfp_copy_rows(void* dst, long long ldd_bytes, const void* src, long long lds_bytes, int rows,
                    long long width_bytes, void* stream);
+/* Cross-entropy forward from the LM-head GEMM's softmax statistics (rrfp_gemm_bf16
+   epilogue 6, EPI_BF16_LSE: float2 (max, sum exp) per row and 128-column slot,
+   ldp float2 per row): lse[r], loss[r] = lse - logits[r, target[r]].  Replaces
+   rrfp_xent_fwd's pass over the logits. */
+int rrfp_xent_combine(const void* part, long long ldp, int slots, const void* logits, long long ld,
+                      const int32_t* target, int rows, float* loss, float* lse, void* stream);
 int rrfp_xent_fwd(const void* logits, long long ld, const int32_t* target, int rows, int V,
                   float* loss, float* lse, void* stream);
 int rrfp_xent_bwd(void* logits, long long ld, const int32_t* target, int rows, int V,

@@ -82,9 +82,9 @@ EXPORTS = [
     "rrfp_replay_event_capacity", "rrfp_replay_host", "rrfp_replay_device",
     "rrfp_runtime_create", "rrfp_runtime_destroy", "rrfp_runtime_inbox", "rrfp_runtime_inbox_ipc",
     "rrfp_ipc_open", "rrfp_ipc_close", "rrfp_ipc_alloc", "rrfp_ipc_handle", "rrfp_ipc_free", "rrfp_runtime_connect", "rrfp_runtime_load_tables", "rrfp_runtime_set_bodies",
-    "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status", "rrfp_runtime_declog",
+    "rrfp_runtime_task_ptr", "rrfp_runtime_prepare", "rrfp_runtime_launch", "rrfp_runtime_wait", "rrfp_runtime_status", "rrfp_runtime_declog", "rrfp_runtime_profile", "rrfp_runtime_profile_read",
     "rrfp_spin", "rrfp_last_error", "rrfp_abi_version", "rrfp_gemm_bf16", "rrfp_gemm_set_variant", "rrfp_set_pdl",
-    "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_gemm_set_tail_split", "rrfp_gemm_set_multicast", "rrfp_gemm_max_clusters", "rrfp_gemm_set_bk", "rrfp_gemm_set_small", "rrfp_gemm_set_rpref", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_embedding_fwd",
+    "rrfp_gemm_reserve_sms", "rrfp_gemm_set_epilogue", "rrfp_gemm_set_streamk", "rrfp_gemm_set_tail_split", "rrfp_gemm_set_multicast", "rrfp_gemm_max_clusters", "rrfp_gemm_set_bk", "rrfp_gemm_set_small", "rrfp_gemm_set_rpref", "rrfp_layernorm_fwd", "rrfp_layernorm_bwd", "rrfp_layernorm_bwd_fused", "rrfp_xent_combine", "rrfp_embedding_fwd",
     "rrfp_embedding_bwd", "rrfp_bias_grad", "rrfp_copy_rows", "rrfp_xent_fwd", "rrfp_xent_bwd", "rrfp_attn_fwd", "rrfp_attn_debug", "rrfp_attn_bwd", "rrfp_attn_bwd_workspace_bytes",
     "rrfp_tp_create", "rrfp_tp_buffers", "rrfp_tp_connect", "rrfp_tp_allreduce", "rrfp_tp_error",
     "rrfp_tp_destroy", "rrfp_clock_pingpong", "rrfp_enable_peer_access", "rrfp_green_streams", "rrfp_green_destroy",

@@ -46,6 +46,9 @@ enum Epi : int {
   EPI_ACC_F32 = 3,     // C (f32) (+)= acc                         -> f32
   EPI_GELU_BWD = 4,    // C = acc * gelu'(R)                       -> bf16
   EPI_F32 = 5,         // C = acc                                  -> f32
+  EPI_BF16_LSE = 6,    // C = acc (+ bias) -> bf16, and per row and 128-column slot the
+                       // online softmax statistics (max, sum exp) of the bf16 values:
+                       // float2 C2[row * ldc2 + col / 128] (LM head + cross-entropy)
 };
 
 struct GemmArgs {
@@ -876,6 +879,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
         // 64 bf16 columns per box (two TMEM chunks); GELU also stages gelu(C) for C2.
         // R (residual / pre-activation) runs one 32-column chunk ahead in qn[h]
         // (its first chunk was requested before the accumulator wait, below).
+        float lse_m = -INFINITY, lse_s = 0.f;   // EPI_BF16_LSE: this row's (max, sum exp) over the unit
 #pragma unroll 1
         for (int c = 0; c < u.bn; c += 64) {
           const int col = u.n0 + c;
@@ -901,6 +905,26 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
             for (int j = 0; j < 16; ++j) {
               w[16 * h + j] = pack_bf16(v[2 * j], v[2 * j + 1]);
               if (EPI == EPI_BIAS_GELU) w2[16 * h + j] = pack_bf16(gelu_tanh(v[2 * j]), gelu_tanh(v[2 * j + 1]));
+            }
+            if (EPI == EPI_BF16_LSE) {
+              // statistics of the values as stored (bf16), columns past N excluded
+              const int nv = g.N - (col + 32 * h);
+              float xr[32];
+              float cm = lse_m;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[16 * h + j]));
+                xr[2 * j] = 2 * j < nv ? f.x : -INFINITY;
+                xr[2 * j + 1] = 2 * j + 1 < nv ? f.y : -INFINITY;
+                cm = fmaxf(cm, fmaxf(xr[2 * j], xr[2 * j + 1]));
+              }
+              if (cm != -INFINITY) {
+                float acc = lse_s * __expf(lse_m - cm);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc += __expf(xr[j] - cm);
+                lse_s = acc;
+                lse_m = cm;
+              }
             }
           }
           uint8_t* box = wbuf + (EPI == EPI_BIAS_GELU ? 0 : (unit & 1) * 4096);
@@ -930,6 +954,11 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
             __syncwarp();
           }
           ++unit;
+        }
+        if (EPI == EPI_BF16_LSE && row < g.M && u.n0 < g.N) {
+          float2* part = reinterpret_cast<float2*>(g.C2) + (size_t)row * g.ldc2 + (u.n0 >> 7);
+          part[0] = make_float2(lse_m, lse_s);
+          if (u.bn == P_BN) part[1] = make_float2(-INFINITY, 0.f);
         }
       }
       if (u.role == ROLE_OWNER && lane == 0) *cnt = 0;   // ready for the next launch on this stream
@@ -1277,7 +1306,7 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   g.rpref = g_rpref;
   const int esz = (epi == EPI_ACC_F32 || epi == EPI_F32) ? 4 : 2;
   g.vec = ((uintptr_t)C % 16 == 0) && ((ldc * esz) % 16 == 0) &&
-          (!C2 || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
+          (!C2 || epi == EPI_BF16_LSE || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
           (!R || (((uintptr_t)R % 16 == 0) && (ldr * 2) % 16 == 0));
   g.vec_bias = ((uintptr_t)bias % 16) == 0;
   // TMA-store epilogue (pair kernel): C (and C2) must be valid TMA globals
@@ -1313,6 +1342,18 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
     case EPI_ACC_F32: return dispatch_majors<EPI_ACC_F32>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
     case EPI_GELU_BWD: return dispatch_majors<EPI_GELU_BWD>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
     case EPI_F32: return dispatch_majors<EPI_F32>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);
+    case EPI_BF16_LSE:
+      // pair kernel, TMA-store epilogue, K-major operands only (the LM head forward)
+      if (!use_pair() || g.tma_st != 1 || a_mn || b_mn || !C2 || ldc2 < 2 * ((N + 255) / 256))
+        return rrfp_fail(RRFP_E_INVALID, "EPI_BF16_LSE needs the pair kernel, a TMA-store C, K-major "
+                         "operands and C2 with >= 2 * ceil(N / 256) float2 slots per row");
+      if (!g_num_sms) {
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      if (pair_bk() == 128) return launch_pair<EPI_BF16_LSE, 0, 0, 128>(ta, tb, tc, tc2, tbh, tah, g, st);
+      return launch_pair<EPI_BF16_LSE, 0, 0, 64>(ta, tb, tc, tc2, tbh, tah, g, st);
   }
   return rrfp_fail(RRFP_E_INVALID, "unknown epilogue %d", epi);
 }

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/rrfp_b200.h"
 #include "rrfp_common.h"
@@ -190,6 +191,157 @@ __global__ void __launch_bounds__(256) ln_param_grad_kernel(
   }
 }
 
+// Fused LayerNorm backward over a slab of rows per CTA (D/8 threads, 8
+// consecutive columns each, G rows in flight per step):
+//   dx[r]   = rstd (dxh - xhat mean(dxh xhat) - mean(dxh)) + dres[r],  dxh = dy g
+//   dg     += sum_r dy xhat,   db += sum_r dy          (LN parameter gradients)
+//   cs_res += sum_r dres[r],   cs_dx += sum_r dx[r]    (bias gradients of the
+//             linear layers the residual gradients feed: b_2 from LN2's dres,
+//             b_o from LN1's dres)
+// One pass over dy / x / dres instead of three kernels (dx, parameter
+// gradients, bias-gradient column sums) each re-reading them; the column
+// partials stay in registers for the whole slab and leave with one vector
+// reduction (red.global.add.v4.f32) per 4 columns per CTA.  dx == NULL: the
+// reductions only (dres then only feeds cs_res).
+__device__ __forceinline__ void red_add8(float* p, const float* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]) : "memory");
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + 4), "f"(v[4]), "f"(v[5]), "f"(v[6]),
+               "f"(v[7]) : "memory");
+}
+
+__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// raw 16-byte loads of one row group (G rows of dy / x / dres + the row statistics):
+// kept packed in registers so the NEXT group's loads are in flight while the
+// current group is reduced (the block barrier of the row sums would otherwise
+// expose the full memory latency once per group)
+template <int G>
+struct LnGroup {
+  uint4 d[G], x[G], r[G];
+  float mu[G], rs[G];
+};
+
+template <int G>
+__device__ __forceinline__ void ln_group_load(LnGroup<G>& q, int rb, int r1, int D, int c,
+                                              const __nv_bfloat16* __restrict__ dy,
+                                              const __nv_bfloat16* __restrict__ x,
+                                              const __nv_bfloat16* __restrict__ dres,
+                                              const float* __restrict__ mean_in,
+                                              const float* __restrict__ rstd_in, bool want_x) {
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const int r = rb + i;
+    const size_t off = (size_t)r * D + c;
+    q.d[i] = q.x[i] = q.r[i] = make_uint4(0, 0, 0, 0);   // (bf16 zeros)
+    q.mu[i] = 0.f;
+    q.rs[i] = 0.f;
+    if (r < r1) {
+      q.d[i] = *reinterpret_cast<const uint4*>(dy + off);
+      if (want_x) {
+        q.x[i] = *reinterpret_cast<const uint4*>(x + off);
+        q.mu[i] = mean_in[r];
+        q.rs[i] = rstd_in[r];
+      }
+      if (dres) q.r[i] = *reinterpret_cast<const uint4*>(dres + off);
+    }
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(512, 1) ln_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+    const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ dres,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db,
+    float* __restrict__ cs_res, float* __restrict__ cs_dx, int rows, int D, int rows_per_cta) {
+  __shared__ float sh[2][16][2 * G];   // per-warp row partials, double-buffered by step parity
+  sm100::griddep_launch();
+  sm100::griddep_wait();
+  const int c = threadIdx.x * 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool want_x = dx || dg;
+  float gv[8];
+  if (dx) load8(g + c, gv);
+  float adg[8], adb[8], ares[8], adx[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { adg[j] = 0.f; adb[j] = 0.f; ares[j] = 0.f; adx[j] = 0.f; }
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int r1 = min(rows, r0 + rows_per_cta);
+  if (r0 >= r1) return;
+  LnGroup<G> nxt;
+  ln_group_load<G>(nxt, r0, r1, D, c, dy, x, dres, mean_in, rstd_in, want_x);
+  int parity = 0;
+  for (int rb = r0; rb < r1; rb += G, parity ^= 1) {
+    const LnGroup<G> cur = nxt;
+    if (rb + G < r1) ln_group_load<G>(nxt, rb + G, r1, D, c, dy, x, dres, mean_in, rstd_in, want_x);
+    float xv[G][8], dv[G][8], rv[G][8];
+    float s[2 * G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      unpack8(cur.d[i], dv[i]);
+      unpack8(cur.x[i], xv[i]);
+      unpack8(cur.r[i], rv[i]);
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xh = (xv[i][j] - cur.mu[i]) * cur.rs[i];
+        xv[i][j] = xh;
+        adg[j] += dv[i][j] * xh;
+        adb[j] += dv[i][j];
+        ares[j] += rv[i][j];
+        if (dx) {
+          const float d = dv[i][j] * gv[j];
+          dv[i][j] = d;
+          s1 += d * xh;
+          s2 += d;
+        }
+      }
+      s[2 * i] = s1;
+      s[2 * i + 1] = s2;
+    }
+    if (dx) {
+#pragma unroll
+      for (int k = 0; k < 2 * G; ++k) s[k] = warp_sum(s[k]);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 2 * G; ++k) sh[parity][warp][k] = s[k];
+      }
+      __syncthreads();   // (the other parity buffer is rewritten only after the next barrier)
+#pragma unroll
+      for (int k = 0; k < 2 * G; ++k) {
+        float t = 0.f;
+        for (int w = 0; w < nw; ++w) t += sh[parity][w][k];
+        s[k] = t * (1.f / D);
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const int r = rb + i;
+        if (r >= r1) break;
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o[j] = cur.rs[i] * (dv[i][j] - xv[i][j] * s[2 * i] - s[2 * i + 1]) + rv[i][j];
+          adx[j] += o[j];
+        }
+        store8(dx + (size_t)r * D + c, o);
+      }
+    }
+  }
+  if (dg) red_add8(dg + c, adg);
+  if (db) red_add8(db + c, adb);
+  if (cs_res) red_add8(cs_res + c, ares);
+  if (cs_dx) red_add8(cs_dx + c, adx);
+}
+
 // ------------------------------------------------------------- embedding
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
                                  const __nv_bfloat16* __restrict__ P, __nv_bfloat16* __restrict__ x,
@@ -363,6 +515,35 @@ __global__ void __launch_bounds__(XENT_FWD_THREADS) xent_fwd_kernel(
   }
 }
 
+// Cross-entropy forward from the LM-head GEMM's per-slot softmax statistics
+// (gemm EPI_BF16_LSE: float2 (max, sum exp) per row and 128-column slot): one
+// warp per row merges the slots -> lse, loss = lse - logit[target].  Reads
+// 8 B per slot instead of the 206 MB logits pass of xent_fwd_kernel.
+__global__ void __launch_bounds__(256) xent_combine_kernel(const float2* __restrict__ part, long long ldp,
+                                                           int slots, const __nv_bfloat16* __restrict__ logits,
+                                                           long long ld, const int32_t* __restrict__ target,
+                                                           int rows, float* __restrict__ loss,
+                                                           float* __restrict__ lse_out) {
+  sm100::griddep_launch();
+  sm100::griddep_wait();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float2* p = part + (size_t)row * ldp;
+  float m = -INFINITY, s = 0.f;
+  for (int i = lane; i < slots; i += 32) {
+    const float2 q = __ldcs(p + i);
+    lse_merge(m, s, q.x, q.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    lse_merge(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+  if (lane == 0) {
+    const float l = m + __logf(s);
+    lse_out[row] = l;
+    loss[row] = l - __bfloat162float(logits[(size_t)row * ld + target[row]]);
+  }
+}
+
 // dlogits = (softmax - onehot) * scale, written in place
 __global__ void __launch_bounds__(512) xent_bwd_kernel(__nv_bfloat16* __restrict__ logits, long long ld,
                                                        const int32_t* __restrict__ target, int V,
@@ -449,6 +630,47 @@ extern "C" int rrfp_layernorm_bwd(const void* dy, const void* x, const float* me
   return RRFP_OK;
 }
 
+// Fused LayerNorm backward (ln_bwd_fused_kernel): any of dx / dg / db / cs_res /
+// cs_dx may be NULL; the fp32 outputs are accumulated (+=).  Slabs of rows sized
+// so two CTAs per SM cover the rows in one wave.
+extern "C" int rrfp_layernorm_bwd_fused(const void* dy, const void* x, const float* mean, const float* rstd,
+                                        const void* g, const void* dres, void* dx, float* dg, float* db,
+                                        float* cs_res, float* cs_dx, int rows, int D, void* stream) {
+  if (int rc = ln_width_ok(D)) return rc;
+  if (D > 4096) return rrfp_fail(RRFP_E_INVALID, "layernorm_bwd_fused: width %d > 4096", D);
+  if (rows <= 0) return RRFP_OK;
+  if (dx && !g) return rrfp_fail(RRFP_E_INVALID, "layernorm_bwd_fused: dx needs gamma");
+  if ((dx || dg) && (!x || !mean || !rstd)) return rrfp_fail(RRFP_E_INVALID, "layernorm_bwd_fused: needs x/mean/rstd");
+  if (cs_res && !dres) return rrfp_fail(RRFP_E_INVALID, "layernorm_bwd_fused: cs_res needs dres");
+  if (!dx && cs_dx) return rrfp_fail(RRFP_E_INVALID, "layernorm_bwd_fused: cs_dx needs dx");
+  constexpr int G = 2;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int per_sm = D <= 2048 ? 2 : 1;
+  int rpc = (rows + per_sm * sms - 1) / (per_sm * sms);
+  // reductions only (no dx, no per-row barrier): taller slabs, fewer column partials
+  // to reduce-add (env RRFP_LN_RPC_MUL, default 2)
+  static int mul = -1;
+  if (mul < 0) {
+    const char* e = getenv("RRFP_LN_RPC_MUL");
+    mul = e ? atoi(e) : 2;
+    if (mul < 1) mul = 1;
+  }
+  if (!dx) rpc *= mul;
+  rpc = (rpc + G - 1) / G * G;
+  const int grid = (rows + rpc - 1) / rpc;
+  RRFP_CUDA_TRY(rrfp_launch(ln_bwd_fused_kernel<G>, dim3(grid), dim3(D / 8), 0, (cudaStream_t)stream,
+                            (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, mean, rstd,
+                            (const __nv_bfloat16*)g, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, dg, db,
+                            cs_res, cs_dx, rows, D, rpc));
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
 extern "C" int rrfp_embedding_fwd(const int32_t* tok, const void* E, const void* P, void* x, int rows,
                                   int D, void* stream) {
   if (D % 8) return rrfp_fail(RRFP_E_INVALID, "embedding width must be a multiple of 8");
@@ -470,6 +692,17 @@ extern "C" int rrfp_bias_grad(const void* dy, long long ld, float* db, int rows,
   const int rpb = 64;
   dim3 grid((cols + 255) / 256, (rows + rpb - 1) / rpb);
   RRFP_CUDA_TRY(rrfp_launch(colsum_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const __nv_bfloat16*)dy, ld, db, rows, cols, rpb));
+  RRFP_CUDA_TRY(cudaGetLastError());
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_xent_combine(const void* part, long long ldp, int slots, const void* logits, long long ld,
+                                 const int32_t* target, int rows, float* loss, float* lse, void* stream) {
+  if (slots <= 0 || ldp < slots) return rrfp_fail(RRFP_E_INVALID, "xent_combine: bad slot count");
+  if (rows <= 0) return RRFP_OK;
+  RRFP_CUDA_TRY(rrfp_launch(xent_combine_kernel, dim3((rows + 7) / 8), dim3(256), 0, (cudaStream_t)stream,
+                            (const float2*)part, ldp, slots, (const __nv_bfloat16*)logits, ld, target, rows, loss,
+                            lse));
   RRFP_CUDA_TRY(cudaGetLastError());
   return RRFP_OK;
 }

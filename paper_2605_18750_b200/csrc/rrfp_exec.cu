@@ -98,6 +98,10 @@ struct lane_state {
   uint32_t* declog;
   int32_t declog_n;
   uint32_t declog_sig;     // free mode: inputs of the last logged WAIT (re-polls are not logged)
+  // ---- dispatcher profile (rrfp_runtime_profile): per step kernel 4 x u64
+  //      {entry, completion done, decision made, kind << 32 | view polls}
+  unsigned long long* prof;
+  int32_t prof_n, prof_cap, polls;
 };
 
 // ------------------------------------------------------------ primitives
@@ -163,6 +167,7 @@ __global__ void lane_init_kernel(lane_state* L) {
     L->remaining = L->d.per_stage;
     L->fixed_head = 0; L->status = 0; L->cur_kind = LANE_NONE;
     L->ring_n = 0;
+    L->prof_n = 0;
     L->declog_n = 0;
     L->declog_sig = 0xFFFFFFFFu;
     L->v_now = 0; L->v_busy_until = 0; L->v_coord_until = 0; L->v_coord_end = -1;
@@ -350,8 +355,10 @@ __device__ void lane_dispatch(lane_state* L) {
   const int lane = threadIdx.x;
   const rrfp_lane_desc& d = L->d;
   const int R = d.R;
+  if (lane == 0) L->polls = 0;
   while (true) {
     if (lane == 0) {
+      L->polls += 1;
       s_exit = 0;
       if (*L->abort_flag) { L->status = RRFP_E_WATCHDOG; s_exit = 1; }
       else if (L->remaining == 0) s_exit = 1;
@@ -850,9 +857,19 @@ __global__ void __launch_bounds__(32, 1) lane_step_kernel(lane_state* L) {
     lane_virtual(L);
     return;
   }
+  const unsigned long long t_in = gtimer();
   if (threadIdx.x == 0) lane_complete(L);
+  const unsigned long long t_c = gtimer();
   __syncwarp();
   lane_dispatch(L);
+  if (L->prof && threadIdx.x == 0) {
+    const int i = L->prof_n++;
+    if (i < L->prof_cap) {
+      unsigned long long* p = L->prof + 4 * (size_t)i;
+      p[0] = t_in; p[1] = t_c; p[2] = gtimer();
+      p[3] = ((unsigned long long)(uint32_t)L->cur_kind << 32) | (uint32_t)L->polls;
+    }
+  }
 }
 
 // ================================================================ host side
@@ -964,6 +981,10 @@ extern "C" void rrfp_runtime_destroy(rrfp_runtime* rt) {
   if (rt->exec) cudaGraphExecDestroy(rt->exec);
   if (rt->graph) cudaGraphDestroy(rt->graph);
   for (void* p : rt->opened) cudaIpcCloseMemHandle(p);
+  unsigned long long* prof = nullptr;
+  if (cudaMemcpy(&prof, (char*)rt->L + offsetof(lane_state, prof), sizeof(prof), cudaMemcpyDeviceToHost) ==
+          cudaSuccess && prof)
+    cudaFree(prof);
   cudaFree(rt->L); cudaFree(rt->inbox); cudaFree(rt->tables); cudaFree(rt->fixed);
   cudaFree(rt->ring); cudaFreeHost(rt->abort_host); cudaFreeHost(rt->mon_host);
   if (rt->declog) cudaFree(rt->declog);
@@ -1276,6 +1297,36 @@ extern "C" int rrfp_runtime_wait(rrfp_runtime* rt, double watchdog_secs, rrfp_ev
     return rrfp_fail(RRFP_E_WATCHDOG, "watchdog: stage %d rank %d remaining=%d n_f=%d n_b=%d",
                      rt->d.stage, rt->d.rank, h.remaining, h.n_f, h.n_b);
   if (h.ring_n > h.ring_cap) return rrfp_fail(RRFP_E_CAPACITY, "trace ring overflow");
+  return RRFP_OK;
+}
+
+// Dispatcher profile: cap records of {step-kernel entry, completion done, decision
+// made, kind << 32 | view polls} (%globaltimer ns) per lane_step_kernel run of the
+// next iterations (cap = 0 disables).  Device-side stamps: ncu does not profile
+// the kernel nodes of a graph with conditional nodes.
+extern "C" int rrfp_runtime_profile(rrfp_runtime* rt, int32_t cap) {
+  if (!rt || cap < 0) return rrfp_fail(RRFP_E_INVALID, "bad argument");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  unsigned long long* buf = nullptr;
+  unsigned long long* old = nullptr;
+  RRFP_CUDA_TRY(cudaMemcpy(&old, (char*)rt->L + offsetof(lane_state, prof), sizeof(old), cudaMemcpyDeviceToHost));
+  if (old) RRFP_CUDA_TRY(cudaFree(old));
+  if (cap > 0) RRFP_CUDA_TRY(cudaMalloc(&buf, sizeof(unsigned long long) * 4 * (size_t)cap));
+  RRFP_CUDA_TRY(cudaMemcpy((char*)rt->L + offsetof(lane_state, prof), &buf, sizeof(buf), cudaMemcpyHostToDevice));
+  RRFP_CUDA_TRY(cudaMemcpy((char*)rt->L + offsetof(lane_state, prof_cap), &cap, sizeof(cap), cudaMemcpyHostToDevice));
+  return RRFP_OK;
+}
+
+extern "C" int rrfp_runtime_profile_read(rrfp_runtime* rt, uint64_t* out, int32_t cap, int32_t* n_records) {
+  if (!rt || !n_records) return rrfp_fail(RRFP_E_INVALID, "null argument");
+  RRFP_CUDA_TRY(cudaSetDevice(rt->dev));
+  lane_state h;
+  RRFP_CUDA_TRY(cudaMemcpy(&h, rt->L, sizeof(h), cudaMemcpyDeviceToHost));
+  int n = h.prof ? (h.prof_n < h.prof_cap ? h.prof_n : h.prof_cap) : 0;
+  if (n > cap) n = cap;
+  if (n > 0 && out)
+    RRFP_CUDA_TRY(cudaMemcpy(out, h.prof, sizeof(uint64_t) * 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  *n_records = n;
   return RRFP_OK;
 }
 

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 
-EPI_BF16, EPI_BIAS_GELU, EPI_RESID, EPI_ACC_F32, EPI_GELU_BWD, EPI_F32 = range(6)
+EPI_BF16, EPI_BIAS_GELU, EPI_RESID, EPI_ACC_F32, EPI_GELU_BWD, EPI_F32, EPI_BF16_LSE = range(7)
 
 # number of our own kernel launches issued through this module (graph bodies
 # count them at capture time; bench.py reports launches per step)
@@ -37,7 +37,7 @@ def _ld(t, mn_major=False):
 
 
 def gemm(a, b, c, *, epi=EPI_BF16, a_mn=False, b_mn=False, c2=None, bias=None, r=None,
-         accumulate=False, m=None, n=None, k=None):
+         accumulate=False, m=None, n=None, k=None, ldc2=None):
     """c = op(a) . op(b)^T with fused epilogue (see csrc/gemm_sm100.cu).
 
     a: [M, K] (or [K, M] if a_mn); b: [N, K] (or [K, N] if b_mn); row-major, unit inner stride.
@@ -50,7 +50,7 @@ def gemm(a, b, c, *, epi=EPI_BF16, a_mn=False, b_mn=False, c2=None, bias=None, r
     _lib.check(L.rrfp_gemm_bf16(
         epi, int(a_mn), int(b_mn), M, N, K, _p(a), C.c_longlong(a.stride(0)), _p(b),
         C.c_longlong(b.stride(0)), _p(c), C.c_longlong(c.stride(0)), _p(c2),
-        C.c_longlong(c2.stride(0) if c2 is not None else 0), _p(bias), _p(r),
+        C.c_longlong(ldc2 if ldc2 is not None else (c2.stride(0) if c2 is not None else 0)), _p(bias), _p(r),
         C.c_longlong(r.stride(0) if r is not None else 0), int(accumulate), _stream()))
     return c
 
@@ -87,3 +87,25 @@ def attn_bwd(qkv, o, do, lse, dqkv, ws, *, heads, causal=True, scale=None, T=Non
                                C.c_longlong(dqkv.stride(0)), _p(ws), T, heads, dh, int(causal), C.c_float(scale),
                                _stream()))
     return dqkv
+
+
+def lm_head_xent_fwd(hf, w_lm, logits, targets, loss, lse, part, *, rows=None):
+    """LM head + cross-entropy forward: logits = hf . w_lm^T (bf16,
+    tcgen05 GEMM) whose epilogue also emits each row's online-softmax
+    statistics per 128-column slot into `part` (fp32 [rows, slots, 2]); a
+    one-warp-per-row merge then gives lse and loss = lse - logit[target].  The
+    logits are written once and not re-read in the forward."""
+    rows = hf.shape[0] if rows is None else rows
+    V = w_lm.shape[0]
+    slots = part.shape[1]
+    gemm(hf, w_lm, logits, epi=EPI_BF16_LSE, c2=part, ldc2=part.stride(0) // 2, m=rows, n=V, k=hf.shape[1])
+    L = _lib.lib()
+    note()
+    _lib.check(L.rrfp_xent_combine(_p(part), C.c_longlong(part.stride(0) // 2), slots, _p(logits),
+                                   C.c_longlong(logits.stride(0)), _p(targets), rows, _p(loss), _p(lse),
+                                   _stream()))
+
+
+def lm_head_slots(vocab):
+    """float2 slots per row of lm_head_xent_fwd's statistics buffer."""
+    return 2 * ((vocab + 255) // 256)

@@ -302,6 +302,16 @@ def _ln_bwd(dy, x, mean, rstd, g, dres, dx, dg, db):
                                     x.shape[1], K._stream()))
 
 
+def _ln_bwd_fused(dy, x, mean, rstd, g, dres, dx, dg=None, db=None, cs_res=None, cs_dx=None):
+    """One-pass LayerNorm backward (csrc/ops.cu ln_bwd_fused_kernel): dx (+ dres),
+    the LN parameter gradients and the column sums of dres / dx (the bias
+    gradients of the adjacent linear layers) in one kernel."""
+    K.note()
+    _lib.check(_lib.lib().rrfp_layernorm_bwd_fused(
+        K._p(dy), K._p(x), K._p(mean), K._p(rstd), K._p(g), K._p(dres), K._p(dx), K._p(dg), K._p(db),
+        K._p(cs_res), K._p(cs_dx), dy.shape[0], dy.shape[1], K._stream()))
+
+
 def _copy_rows(dst, src, rows, cols):
     """bf16 [rows, cols] copy (e.g. into a peer stage's mailbox slot)."""
     K.note()
@@ -452,6 +462,11 @@ class StageCompute:
         # attention core: cuDNN SDPA through the frontend graph API (attention.py) reading
         # the packed QKV and writing O / stats / packed dQKV into our own slots;
         # RRFP_ATTN=torch selects the aten op (separate dQ/dK/dV, copied in)
+        # LayerNorm parameter gradients fused with the adjacent bias gradients (column
+        # sums of the residual gradients) in one side-stream pass (ops.cu
+        # ln_bwd_fused_kernel), the head's LN backward in one kernel; RRFP_LN_FUSED=0:
+        # separate kernels
+        self.ln_fused = os.environ.get("RRFP_LN_FUSED", "1") != "0" and D <= 4096
         self.attn_impl = os.environ.get("RRFP_ATTN", "cudnn_fe")
         self._sdpa = {}
         if self.attn_impl == "cudnn_fe" and nl:
@@ -476,6 +491,10 @@ class StageCompute:
             self.logits = e(n_mb, S, V)
             self.loss = torch.zeros(n_mb, S, device=dev)
             self.lse = f32(n_mb, S)
+            # LM head + cross-entropy forward fused (gemm EPI_BF16_LSE + xent_combine);
+            # RRFP_CE_FUSED=0: GEMM, then xent_fwd over the logits
+            self.ce_fused = os.environ.get("RRFP_CE_FUSED", "1") != "0" and V % 8 == 0
+            self.ce_part = f32(S, K.lm_head_slots(V), 2) if self.ce_fused else None   # shared scratch
         # scratch shared by all bodies of this stage (bodies never overlap on a lane)
         # two parity sets (layer li uses set li % 2) so the weight-gradient
         # GEMMs of layer li can run on the side stream while layer li-1's
@@ -604,11 +623,15 @@ class StageCompute:
         if self.last:
             h = self.head
             _ln_fwd(x, h["lnf_g"], h["lnf_b"], self.hf[mb], self.mf[mb], self.rf[mb], cfg.eps)
-            K.gemm(self.hf[mb], h["w_lm"], self.logits[mb])
-            K.note()
-            _lib.check(_lib.lib().rrfp_xent_fwd(
-                K._p(self.logits[mb]), C.c_longlong(cfg.vocab), K._p(self.targets[mb]), S,
-                cfg.vocab, K._p(self.loss[mb]), K._p(self.lse[mb]), K._stream()))
+            if self.ce_fused:   # softmax statistics from the GEMM epilogue (no pass over the logits)
+                K.lm_head_xent_fwd(self.hf[mb], h["w_lm"], self.logits[mb], self.targets[mb], self.loss[mb],
+                                   self.lse[mb], self.ce_part)
+            else:
+                K.gemm(self.hf[mb], h["w_lm"], self.logits[mb])
+                K.note()
+                _lib.check(_lib.lib().rrfp_xent_fwd(
+                    K._p(self.logits[mb]), C.c_longlong(cfg.vocab), K._p(self.targets[mb]), S,
+                    cfg.vocab, K._p(self.loss[mb]), K._p(self.lse[mb]), K._stream()))
         elif self.epilogue == "projector":   # [T_v, d_vit] -> [T_v, d_llm] rows of the LLM mailbox
             for dst in self.fwd_out[mb]:
                 K.gemm(x, self.proj["w_proj"], dst[:T], bias=self.proj["b_proj"])
@@ -689,8 +712,9 @@ class StageCompute:
                                              a_mn=True, b_mn=True, accumulate=True, m=V, n=D, k=S))
             K.gemm(self.logits[mb], h["w_lm"], self.d_head, b_mn=True, m=S, n=D, k=V)
             dy = dy_buf(nl - 1)
-            _ln_bwd(self.d_head, self.y[mb, nl - 1], self.mf[mb], self.rf[mb], h["lnf_g"], None, dy,
-                    gh["lnf_g"], gh["lnf_b"])
+            (_ln_bwd_fused if self.ln_fused else _ln_bwd)(
+                self.d_head, self.y[mb, nl - 1], self.mf[mb], self.rf[mb], h["lnf_g"], None, dy,
+                gh["lnf_g"], gh["lnf_b"])
         elif self.epilogue == "projector":
             # gradient of the projected visual rows -> ViT output gradient (+ projector grads)
             dyp, pj, gp = self.bwd_in[mb][:T], self.proj, self.g_proj
@@ -744,7 +768,7 @@ class StageCompute:
                     dyy = dy
                     on_side(ev(), lambda: (K.gemm(dyy, act, g["w_2"], epi=K.EPI_ACC_F32,
                                                   a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=T),
-                                           _bias_grad(dyy, g["b_2"])))
+                                           None if self.ln_fused else _bias_grad(dyy, g["b_2"])))   # (b_2: LN2 side pass)
                 # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
                 K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D)
                 if fused_w:
@@ -757,7 +781,12 @@ class StageCompute:
                 ln_dy = (self.gln2[mb, li] if dec else self.sd_ln2[q])[:T]
                 self._dgrad_reduce(d_pre, p["w_1"], Fl, T, out=ln_dy)
                 _ln_bwd(ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], p["ln2_g"], dy, d_x2, None, None)
-                if not dec:
+                if not dec and self.ln_fused:
+                    # side pass: LN2 parameter gradients + b_2's gradient (column sum of dy), one kernel
+                    on_side(ev(), lambda ln_dy=ln_dy, x2=x2, g=g, li=li, dyy=dy: _ln_bwd_fused(
+                        ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None, dyy, None,
+                        g["ln2_g"], g["ln2_b"], g["b_2"]))
+                elif not dec:
                     on_side(ev(), lambda ln_dy=ln_dy, x2=x2, g=g, li=li: _ln_bwd(
                         ln_dy, x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None, None, None,
                         g["ln2_g"], g["ln2_b"]))
@@ -771,7 +800,7 @@ class StageCompute:
                 dxx = d_x2
                 on_side(ev(), lambda: (K.gemm(dxx, ov, g["w_o"], epi=K.EPI_ACC_F32,
                                               a_mn=True, b_mn=True, accumulate=True, m=D, n=Dl, k=T),
-                                       _bias_grad(dxx, g["b_o"])))
+                                       None if self.ln_fused and not dec else _bias_grad(dxx, g["b_o"])))
             # out-proj dgrad -> attention backward -> QKV dgrad
             d_o = d_head if self.R == 1 else self.d_o
             K.gemm(d_x2, p["w_o"], d_o, b_mn=True, m=T, n=Dl, k=D)
@@ -792,7 +821,12 @@ class StageCompute:
             else:
                 dx, extra = stage_dx()
             _ln_bwd(ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], p["ln1_g"], d_x2, dx, None, None)
-            if not dec:
+            if not dec and self.ln_fused:
+                # side pass: LN1 parameter gradients + b_o's gradient (column sum of d_x2), one kernel
+                on_side(ev(), lambda ln_dy=ln_dy, x=x, g=g, li=li, dxx=d_x2: _ln_bwd_fused(
+                    ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], None, dxx, None,
+                    g["ln1_g"], g["ln1_b"], g["b_o"]))
+            elif not dec:
                 on_side(ev(), lambda ln_dy=ln_dy, x=x, g=g, li=li: _ln_bwd(
                     ln_dy, x, self.m1[mb, li, :T], self.r1[mb, li, :T], None, None, None,
                     g["ln1_g"], g["ln1_b"]))
@@ -903,17 +937,23 @@ class StageCompute:
             part = self.parts[li]
             with torch.cuda.stream(side if li % 2 else main):
                 # LayerNorm parameter gradients (memory-bound: they overlap the other stream's GEMMs)
+                lnb = _ln_bwd_fused if self.ln_fused else _ln_bwd
                 if part != "attn":
                     x2 = self._layer_input(mb, li) if part == "mlp" else self.x2[mb, li, :T]
-                    _ln_bwd(self.gln2[mb, li, :T], x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None,
-                            None, None, g["ln2_g"], g["ln2_b"])
+                    if self.ln_fused:   # + b_2's gradient (column sum of gy) in the same pass
+                        _ln_bwd_fused(self.gln2[mb, li, :T], x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None,
+                                      gy, None, g["ln2_g"], g["ln2_b"], g["b_2"])
+                    else:
+                        _ln_bwd(self.gln2[mb, li, :T], x2, self.m2[mb, li, :T], self.r2[mb, li, :T], None,
+                                None, None, g["ln2_g"], g["ln2_b"])
                 if part != "mlp":
-                    _ln_bwd(self.gln1[mb, li, :T], self._layer_input(mb, li), self.m1[mb, li, :T],
-                            self.r1[mb, li, :T], None, None, None, g["ln1_g"], g["ln1_b"])
+                    lnb(self.gln1[mb, li, :T], self._layer_input(mb, li), self.m1[mb, li, :T],
+                        self.r1[mb, li, :T], None, None, None, g["ln1_g"], g["ln1_b"])
                 if part != "attn":
                     K.gemm(gy, self.act[mb, li, :T], g["w_2"], epi=K.EPI_ACC_F32, a_mn=True,
                            b_mn=True, accumulate=True, m=D, n=Fd, k=T)
-                    _bias_grad(gy, g["b_2"])
+                    if not self.ln_fused:
+                        _bias_grad(gy, g["b_2"])
                     K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
                            b_mn=True, accumulate=True, m=Fd, n=D, k=T)
                     _bias_grad(gpre, g["b_1"])

@@ -396,6 +396,25 @@ class LaneGroup:
                 out.append(parse_decision(rec, self.tables.desc.MW))
         return out
 
+    def enable_profile(self, cap: int = 4096):
+        """Record every lane_step_kernel run of the following iterations
+        (include/rrfp_b200.h rrfp_runtime_profile); cap = 0 disables."""
+        for h in self.lanes.values():
+            _lib.check(self.L.rrfp_runtime_profile(h, cap))
+        self._prof_cap = cap
+
+    def profile(self):
+        """{lane: uint64[n, 4]} of the last iteration: step-kernel entry, completion
+        done, decision made (ns), kind << 32 | view polls."""
+        out = {}
+        cap = getattr(self, "_prof_cap", 0)
+        for lane, h in self.lanes.items():
+            buf = np.zeros((max(cap, 1), 4), np.uint64)
+            n = C.c_int32()
+            _lib.check(self.L.rrfp_runtime_profile_read(h, buf.ctypes.data_as(C.c_void_p), cap, C.byref(n)))
+            out[lane] = buf[:n.value].copy()
+        return out
+
     def make_trace(self, events, t0s):
         """(Trace, Metrics) of one iteration: virtual-clock (replay mode) or wall."""
         if self.virtual:
@@ -566,6 +585,40 @@ def dispatch_latency(trace, n_stages: int) -> dict:
         x = sorted(x)
         return {"p50": x[len(x) // 2], "p90": x[int(0.9 * (len(x) - 1))], "n": len(x)}
     return {"back_to_back_gap_us": q(gaps), "arrival_to_start_us": q(react)}
+
+
+def dispatcher_profile(records: dict, body_us: float | None = None) -> dict:
+    """Summary of LaneGroup.profile() records (device %globaltimer stamps inside
+    lane_step_kernel, ns): per decision the completion half (end stamp, jitter
+    pad, flag sends), the dispatch half when the next task was already ready
+    (one view poll: ballot + arbitrate + SWITCH select), and the time from one
+    decision to the next step kernel's entry (the SWITCH-launched body, then
+    the WHILE node relaunching the step kernel; minus body_us when the bodies
+    have a known length).  Microseconds, p50 / p90."""
+    comp, dec_ready, between = [], [], []
+    waited = 0
+    for recs in records.values():
+        if len(recs) == 0:
+            continue
+        r = recs[recs[:, 0].argsort()].astype(np.int64)
+        comp += list((r[:, 1] - r[:, 0]) / 1e3)
+        polls = r[:, 3] & 0xFFFFFFFF
+        kind = r[:, 3] >> 32
+        for i in range(len(r)):
+            if polls[i] == 1:
+                dec_ready.append((r[i, 2] - r[i, 1]) / 1e3)
+            else:
+                waited += 1
+            if i + 1 < len(r) and kind[i] in (0, 1, 2):    # a body ran between the two step kernels
+                between.append((r[i + 1, 0] - r[i, 2]) / 1e3 - (body_us or 0.0))
+
+    def q(x):
+        if not x:
+            return None
+        x = sorted(x)
+        return {"p50": round(x[len(x) // 2], 2), "p90": round(x[int(0.9 * (len(x) - 1))], 2), "n": len(x)}
+    return {"complete_us": q(comp), "decide_when_ready_us": q(dec_ready), "decisions_that_waited": waited,
+            ("graph_relaunch_us" if body_us is not None else "decision_to_next_step_us"): q(between)}
 
 
 def run_gpu(workload: Workload, hint: HintOrder | str = "bf", buffer_limit: int = 32,

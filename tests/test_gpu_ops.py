@@ -82,6 +82,49 @@ def test_layernorm_fwd_bwd(rows, D):
     torch.testing.assert_close(db, 2 * br.grad, rtol=1e-3, atol=1e-3)
 
 
+@pytest.mark.parametrize("rows,D", [(2048, 2048), (100, 1280), (2048, 4096), (33, 256), (3, 512)])
+def test_layernorm_bwd_fused(rows, D):
+    """One-pass LN backward: dx (+ dres), dg / db and the column sums of dres and
+    dx (adjacent bias gradients), each accumulated; every output optional."""
+    torch.manual_seed(D + rows)
+    bf = torch.bfloat16
+    x = torch.randn(rows, D, device="cuda").to(bf)
+    g = (1 + 0.1 * torch.randn(D, device="cuda")).to(bf)
+    mean = x.float().mean(1)
+    rstd = torch.rsqrt(x.float().var(1, unbiased=False) + 1e-5)
+    xr = x.float().requires_grad_(True)
+    gr = g.float().requires_grad_(True)
+    br = torch.zeros(D, device="cuda", requires_grad=True)
+    yr = torch.nn.functional.layer_norm(xr, (D,), gr, br, 1e-5)
+    dy = torch.randn(rows, D, device="cuda").to(bf)
+    dres = torch.randn(rows, D, device="cuda").to(bf)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    base = torch.randn(4, D, device="cuda")
+    dg, db, cr, cd = (base[i].clone() for i in range(4))
+    assert _L().rrfp_layernorm_bwd_fused(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), _p(dres), _p(dx), _p(dg),
+                                         _p(db), _p(cr), _p(cd), rows, D, _st()) == 0
+    torch.cuda.synchronize()
+    want_dx = xr.grad + dres.float()
+    _close(dx, want_dx)
+    torch.testing.assert_close(dg, base[0] + gr.grad, rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(db, base[1] + br.grad, rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(cr, base[2] + dres.float().sum(0), rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(cd, base[3] + want_dx.sum(0), rtol=1e-3, atol=0.05)
+    # reductions only: no dx, dres feeds only its column sum
+    dg2, cr2 = torch.zeros(D, device="cuda"), torch.zeros(D, device="cuda")
+    assert _L().rrfp_layernorm_bwd_fused(_p(dy), _p(x), _p(mean), _p(rstd), None, _p(dres), None, _p(dg2),
+                                         None, _p(cr2), None, rows, D, _st()) == 0
+    torch.cuda.synchronize()
+    torch.testing.assert_close(dg2, gr.grad, rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(cr2, dres.float().sum(0), rtol=1e-3, atol=2e-3)
+    # argument checks: cs_dx without dx, width > 4096
+    assert _L().rrfp_layernorm_bwd_fused(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), None, None, None,
+                                         None, None, _p(cd), rows, D, _st()) != 0
+    assert _L().rrfp_layernorm_bwd_fused(_p(dy), _p(x), _p(mean), _p(rstd), _p(g), None, _p(dx), None,
+                                         None, None, None, 1, 8192, _st()) != 0
+
+
 def test_layernorm_rejects_bad_width():
     x = torch.zeros(4, 300, device="cuda", dtype=torch.bfloat16)
     assert _L().rrfp_layernorm_fwd(_p(x), _p(x), _p(x), _p(x), _p(x), _p(x), 4, 300, C.c_float(1e-5), _st()) != 0
@@ -118,3 +161,31 @@ def test_embedding_fwd_bwd(rows, D, V):
     _close(x, E.float()[tok.long()] + P.float())
     torch.testing.assert_close(dE, wantE, rtol=1e-5, atol=1e-4)
     torch.testing.assert_close(dP, wantP, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("rows,D,V", [(2048, 2048, 50304), (256, 256, 1000), (200, 512, 4096)])
+def test_lm_head_xent_fused(rows, D, V):
+    """LM head GEMM with the softmax-statistics epilogue + xent_combine against
+    GEMM + xent_fwd (same bf16 logits, bit-identical) and an fp32 reference."""
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(V)
+    bf = torch.bfloat16
+    hf = torch.randn(rows, D, device="cuda").to(bf)
+    w = (torch.randn(V, D, device="cuda") * 0.05).to(bf)
+    tgt = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32)
+    logits = torch.empty(rows, V, device="cuda", dtype=bf)
+    loss, lse = torch.zeros(rows, device="cuda"), torch.zeros(rows, device="cuda")
+    part = torch.full((rows, Kn.lm_head_slots(V), 2), float("nan"), device="cuda")
+    Kn.lm_head_xent_fwd(hf, w, logits, tgt, loss, lse, part)
+    ref_logits = torch.empty_like(logits)
+    Kn.gemm(hf, w, ref_logits)
+    loss2, lse2 = torch.zeros(rows, device="cuda"), torch.zeros(rows, device="cuda")
+    assert _L().rrfp_xent_fwd(_p(ref_logits), C.c_longlong(V), _p(tgt), rows, V, _p(loss2), _p(lse2), _st()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(logits, ref_logits)
+    torch.testing.assert_close(lse, lse2, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(loss, loss2, rtol=1e-5, atol=1e-4)
+    lf = logits.float()
+    want = torch.logsumexp(lf, 1)
+    torch.testing.assert_close(lse, want, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(loss, want - lf[torch.arange(rows), tgt.long()], rtol=1e-5, atol=1e-4)

@@ -297,3 +297,32 @@ def test_replay_decisions_match_oracle():
             jitter=P.JITTER_PRESETS[case["jitter"]], tp=tp, mode="replay", declog=log)
     assert len(log) >= 750 * 0 + w.task_count()
     assert not check_decisions(log, w, hint, case["limit"])
+
+
+def test_dispatcher_profile_records_every_step():
+    """rrfp_runtime_profile: one record per lane_step_kernel run (every task's
+    decision plus the exiting step), stamps ordered entry <= completion done <=
+    decision, kinds of the dispatched tasks match the trace; disabling stops it."""
+    from paper_2605_18750_b200.runtime import LaneGroup, dispatcher_profile
+    w = P.generate_workload(_spec(n=2, m=8), 5)
+    g = LaneGroup(w, "bf", 32, 1.0, seed=5)
+    try:
+        g.run_iteration(30.0)
+        g.enable_profile(1024)
+        events, t0s = g.run_iteration(30.0)
+        prof = g.profile()
+        assert len(prof) == 2
+        for lane, r in prof.items():
+            assert len(r) == w.task_count() // 2 + 1
+            r = r.astype("int64")
+            assert (r[:, 0] <= r[:, 1]).all() and (r[:, 1] <= r[:, 2]).all()
+            kinds = sorted(int(k) for k in (r[:, 3] >> 32))
+            assert kinds.count(3) == 1                       # the exiting step
+            assert kinds.count(0) == kinds.count(1) == 8     # B and F of every microbatch
+        s = dispatcher_profile(prof)
+        assert s["complete_us"]["n"] == w.task_count() + 2
+        g.enable_profile(0)
+        g.run_iteration(30.0)
+        assert all(len(r) == 0 for r in g.profile().values())
+    finally:
+        g.close()
