@@ -44,7 +44,8 @@ enum Epi : int {
   EPI_BIAS_GELU = 1,   // C = acc + bias (pre-act), C2 = gelu(C)   -> bf16, bf16
   EPI_RESID = 2,       // C = acc (+ bias) + R                     -> bf16
   EPI_ACC_F32 = 3,     // C (f32) (+)= acc                         -> f32
-  EPI_GELU_BWD = 4,    // C = acc * gelu'(R)                       -> bf16
+  EPI_GELU_BWD = 4,    // C = acc * gelu'(R)                       -> bf16;  C2 (optional, f32 [N])
+                       //   += column sums of C as stored (the FC1 bias gradient)
   EPI_F32 = 5,         // C = acc                                  -> f32
   EPI_BF16_LSE = 6,    // C = acc (+ bias) -> bf16, and per row and 128-column slot the
                        // online softmax statistics (max, sum exp) of the bf16 values:
@@ -343,6 +344,22 @@ __device__ __forceinline__ void epi_apply_q(const GemmArgs& g, int row, int col0
       }
     }
   }
+}
+
+// Column sums of a warp's 32 rows x 32 columns (one row per lane, v[c] = column
+// c): 31 shuffles (halving exchange); lane l returns the sum of column l.
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int k = 16; k >= 1; k >>= 1) {
+    const bool upper = lane & k;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const float send = upper ? v[i] : v[i + k];
+      const float keep = upper ? v[i + k] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return v[0];
 }
 
 // Write one 128-byte row segment (8 x 16 B) of a SWIZZLE_128B staging box:
@@ -906,6 +923,19 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(256, 1)
               w[16 * h + j] = pack_bf16(v[2 * j], v[2 * j + 1]);
               if (EPI == EPI_BIAS_GELU) w2[16 * h + j] = pack_bf16(gelu_tanh(v[2 * j]), gelu_tanh(v[2 * j + 1]));
             }
+            if (EPI == EPI_GELU_BWD && g.C2) {
+              // FC1 bias gradient: column sums of d_pre as stored (bf16), rows past M excluded
+              float cv[32];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[16 * h + j]));
+                cv[2 * j] = row < g.M ? f.x : 0.f;
+                cv[2 * j + 1] = row < g.M ? f.y : 0.f;
+              }
+              const float cs = warp_colsum32(cv, lane);
+              const int cc = col + 32 * h + lane;
+              if (cc < g.N) atomicAdd(reinterpret_cast<float*>(g.C2) + cc, cs);
+            }
             if (EPI == EPI_BF16_LSE) {
               // statistics of the values as stored (bf16), columns past N excluded
               const int nv = g.N - (col + 32 * h);
@@ -1306,7 +1336,8 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
   g.rpref = g_rpref;
   const int esz = (epi == EPI_ACC_F32 || epi == EPI_F32) ? 4 : 2;
   g.vec = ((uintptr_t)C % 16 == 0) && ((ldc * esz) % 16 == 0) &&
-          (!C2 || epi == EPI_BF16_LSE || (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
+          (!C2 || epi == EPI_BF16_LSE || epi == EPI_GELU_BWD ||
+           (((uintptr_t)C2 % 16 == 0) && (ldc2 * 2) % 16 == 0)) &&
           (!R || (((uintptr_t)R % 16 == 0) && (ldr * 2) % 16 == 0));
   g.vec_bias = ((uintptr_t)bias % 16) == 0;
   // TMA-store epilogue (pair kernel): C (and C2) must be valid TMA globals
@@ -1334,6 +1365,8 @@ extern "C" int rrfp_gemm_bf16(int epi, int a_mn, int b_mn, int M, int N, int K, 
       g.tma_st = 2;
     }
   }
+  if (epi == EPI_GELU_BWD && C2 && !g.tma_st)
+    return rrfp_fail(RRFP_E_INVALID, "EPI_GELU_BWD column sums (C2) need the staged (TMA-store) epilogue");
   cudaStream_t st = (cudaStream_t)stream;
   switch (epi) {
     case EPI_BF16: return dispatch_majors<EPI_BF16>(a_mn, b_mn, ta, tb, tbh, tah, tc, tc2, g, st);

@@ -467,6 +467,8 @@ class StageCompute:
         # ln_bwd_fused_kernel), the head's LN backward in one kernel; RRFP_LN_FUSED=0:
         # separate kernels
         self.ln_fused = os.environ.get("RRFP_LN_FUSED", "1") != "0" and D <= 4096
+        # FC1 bias gradient reduced in the FC2-dgrad GEMM epilogue (EPI_GELU_BWD + C2)
+        self.colsum_epi = os.environ.get("RRFP_COLSUM_EPI", "1") != "0"
         self.attn_impl = os.environ.get("RRFP_ATTN", "cudnn_fe")
         self._sdpa = {}
         if self.attn_impl == "cudnn_fe" and nl:
@@ -770,11 +772,13 @@ class StageCompute:
                                                   a_mn=True, b_mn=True, accumulate=True, m=D, n=Fl, k=T),
                                            None if self.ln_fused else _bias_grad(dyy, g["b_2"])))   # (b_2: LN2 side pass)
                 # FC2 dgrad fused with GELU': d_pre = (dy . W2) * gelu'(pre)   (this rank's FFN columns)
-                K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D)
+                # (+ b_1's gradient, the column sums of d_pre, reduced in the same epilogue)
+                K.gemm(dy, p["w_2"], d_pre, epi=K.EPI_GELU_BWD, b_mn=True, r=pre, m=T, n=Fl, k=D,
+                       c2=g["b_1"] if self.colsum_epi else None)
                 if fused_w:
                     on_side(ev(), lambda: (K.gemm(d_pre, h2, g["w_1"], epi=K.EPI_ACC_F32,
                                                   a_mn=True, b_mn=True, accumulate=True, m=Fl, n=D, k=T),
-                                           _bias_grad(d_pre, g["b_1"])))
+                                           None if self.colsum_epi else _bias_grad(d_pre, g["b_1"])))
                 # FC1 dgrad (a partial sum under TP: all-reduced) -> LN2 backward (+ residual grad dy).
                 # The LN2 parameter gradients leave the input-gradient chain: side stream
                 # (fused), W task (decomposed, from the saved gln2)
@@ -956,7 +960,8 @@ class StageCompute:
                         _bias_grad(gy, g["b_2"])
                     K.gemm(gpre, self.h2[mb, li, :T], g["w_1"], epi=K.EPI_ACC_F32, a_mn=True,
                            b_mn=True, accumulate=True, m=Fd, n=D, k=T)
-                    _bias_grad(gpre, g["b_1"])
+                    if not self.colsum_epi:   # (else reduced by B's FC2-dgrad epilogue)
+                        _bias_grad(gpre, g["b_1"])
                 if self.w_split == "all" and part != "mlp":
                     gx2, gqkv = self.gx2[mb, li, :T], self.gqkv[mb, li, :T]
                     K.gemm(gx2, self.o_view[mb][li], g["w_o"], epi=K.EPI_ACC_F32, a_mn=True,

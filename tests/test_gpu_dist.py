@@ -79,3 +79,24 @@ def test_second_pipeline_in_the_same_processes():
     for r in res["ranks"]:
         if r["losses"][0] is not None:
             assert len(r["losses"]) == 3 and all(abs(l - ref) / ref < 1e-2 for l in r["losses"])
+
+
+def test_bench_two_ranks_end_to_end():
+    """`python bench.py --gpus 2` (re-exec under torchrun, 2 processes on one GPU)
+    with a 2-layer GPT-1.3B-width model: the full N>1 path of the driver's
+    scaling run -- timed steps, the 1F1B / BF / BFW comparison at a J-preset and
+    a lognormal sigma, the p2p block -- prints one JSON line with n_gpus 2."""
+    env = dict(os.environ, RRFP_SAME_DEVICE="1")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--layers", "2", "--mb", "4",
+           "--steps", "1", "--warmup", "3", "--sigmas", "0.5", "--compare-jitter", "J0,J2",
+           "--no-cpu-baseline"]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]
+    res = json.loads(line[-1])
+    assert res["n_gpus"] == 2 and res["config"]["parallelism"].startswith("pp2")
+    assert res["value"] > 0 and res["e2e"]["value"] > 0
+    v = res["variants"]
+    for name in ("1f1b", "bf", "bfw"):
+        for combo in ("J0+sigma0.0", "J0+sigma0.5", "J2+sigma0.5"):
+            assert v[f"{name}@{combo}"]["ms"] > 0, (name, combo)

@@ -200,3 +200,25 @@ def test_gemm_out_projection_2048_cube():
     _close(y, x.float() @ w.float().t() + bias.float() + res.float())
     _close(dx, dy.float() @ w.float())
     _close(gw, want_gw, 1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 8192, 2048), (200, 320, 192), (256, 512, 256)])
+def test_gemm_gelu_bwd_column_sums(M, N, K, variant):
+    """EPI_GELU_BWD with C2: the epilogue also accumulates the column sums of
+    the stored bf16 output (the FC1 bias gradient) into an fp32 vector (staged
+    epilogues only; the per-thread-store variants refuse it)."""
+    from paper_2605_18750_b200 import kernels as Kn
+    torch.manual_seed(11)
+    a, b, pre = _rand(M, K), _rand(N, K), _rand(M, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.randn(N, device="cuda")
+    base = cs.clone()
+    pair, tma = variant[0], variant[1]
+    if not pair or not tma:
+        with pytest.raises(RuntimeError):
+            Kn.gemm(a, b, out, epi=Kn.EPI_GELU_BWD, r=pre, c2=cs)
+        return
+    Kn.gemm(a, b, out, epi=Kn.EPI_GELU_BWD, r=pre, c2=cs)
+    torch.cuda.synchronize()
+    want = base + out.float().sum(0)
+    torch.testing.assert_close(cs, want, rtol=1e-4, atol=1e-2)
