@@ -852,7 +852,26 @@ __device__ void lane_complete(lane_state* L) {
 // next one and set the SWITCH branch (or end the WHILE).  One kernel node per
 // task instead of a dispatch and a completion kernel: ~1 device-side launch
 // less per decision (tools/dispatch_bench.py).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  bytes &= ~15u;
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __global__ void __launch_bounds__(32, 1) lane_step_kernel(lane_state* L) {
+  // Between two decisions the task body streams its working set through L2, so
+  // the lane state and the inbox are usually cold: pull them into L2 in bulk
+  // before the dependent chain of state reads starts (one HBM latency instead
+  // of one per access).
+  if (threadIdx.x == 0) {
+    l2_prefetch(L, (uint32_t)sizeof(lane_state));
+    lane_inbox* in = L->inbox;
+    const uint32_t keys = (uint32_t)L->KEYS;
+    l2_prefetch(in->fflag, keys * 4 + 12);
+    l2_prefetch(in->bflag, keys * 4 + 12);
+    l2_prefetch(in->fvis, keys * 8);
+    l2_prefetch(in->bvis, keys * 8);
+    l2_prefetch(in->tp_prop, (uint32_t)(sizeof(lane_inbox) - offsetof(lane_inbox, tp_prop)));
+  }
   if (L->d.virtual_clock) {
     lane_virtual(L);
     return;
