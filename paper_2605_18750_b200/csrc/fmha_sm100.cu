@@ -691,7 +691,16 @@ __global__ void __launch_bounds__(B_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 3) {
+    // Two MMA issuers: warp 1 issues S^T / dP^T of each step, warp 3 the gradient
+    // MMAs (dV, dK, dQ^T) of the step the elementwise pass finished.  One issuer
+    // spent ~1,800 of ~3,000 cycles per step issuing these 32 small MMAs
+    // (tools/attn_timeline.py --bwd); split, the two streams of issues overlap.
+    // Each warp commits only its own MMAs (tcgen05.commit tracks the issuing
+    // thread's operations); the barriers order what the two share: S^T / dP^T
+    // TMEM (s_full -> sd_free), P^T / dS^T smem (ds_full -> pds_free), the Q / dO
+    // stage (released by the gradient MMAs, which follow the stage's S^T / dP^T
+    // through ds_full), K / V (kv_free after the unit's last gradient MMAs).
     // S^T / dP^T: M=128 keys, N=64 queries, K=128 (A K-major keys/values, B K-major Q/dO)
     constexpr uint32_t idSD = sm100::idesc_bf16(128, 64, 0, 0);
     // dV / dK: M=128 keys, N=128 (d), K=64 queries (A = P^T / dS^T K-major, B = dO / Q MN-major)
@@ -708,67 +717,65 @@ __global__ void __launch_bounds__(B_THREADS, 1)
     const uint64_t dStg_k = sm100::umma_desc_sw128(sm100::smem_u32(stg), 16, 1024);
     const uint64_t dStg_mn = sm100::umma_desc_sw128(sm100::smem_u32(stg), B_QTILE / 2, 1024);
     int n = 0, step = 0;   // ring index, global step (sd/ds/pds/dq parities)
-    auto sd = [&](int st) {   // S^T, dP^T of a step into TMEM
-      const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
-        mma_ss_e(tS, dK_k + ka, dStg_k + so + kb, idSD, k != 0);
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
-        mma_ss_e(tP, dV_k + ka, dStg_k + so + ((B_QTILE >> 4) + kb), idSD, k != 0);
-      }
-      commit_e(s_full);
-    };
-    auto grads = [&](int st, int first, int gstep) {   // dV, dK, dQ^T of a step
-      DBG(1, 14, gstep);
-      wait(ds_full, gstep & 1);
-      DBG(1, 15, gstep);
-      sm100::tc_fence_after();
-      const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)   // dV += P^T dO
-        mma_ss_e(tmem, dP_a + ((k * 32) >> 4), dStg_mn + so + ((B_QTILE + k * 2048) >> 4), idVK, !first || k);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)   // dK += dS^T Q
-        mma_ss_e(tmem + 128, dDS_a + ((k * 32) >> 4), dStg_mn + so + ((k * 2048) >> 4), idVK, !first || k);
-      const int b = gstep & 1;
-      DBG(1, 16, gstep);
-      if (gstep >= 2) wait(&dq_free[b], ((gstep - 2) >> 1) & 1);
-      DBG(1, 17, gstep);
-      sm100::tc_fence_after();
-#pragma unroll
-      for (int k = 0; k < 8; ++k)   // dQ^T = K^T dS^T
-        mma_ss_e(tmem + 384 + 64 * b, dK_mn + ((k * 2048) >> 4), dDS_b + ((k * 2048) >> 4), idQ, k != 0);
-      commit_e(pds_free);
-      commit_e(&dq_full[b]);
-      commit_e(&empty[st]);
-      DBG(1, 18, gstep);
-    };
-    for (int un = 0; un < pl.n_units; ++un) {
-      const int kt = pl.kt[un], ni = bwd_ni(g, kt);
-      wait(kv_full, un & 1);
-      if (un) wait(acc_free, (un - 1) & 1);   // the previous unit's dV / dK are written out
-      sm100::tc_fence_after();
-      int prev_st = -1;
-      for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
-        const int st = n % B_STAGES;
-        DBG(1, 10, step);
-        wait(&full[st], (n / B_STAGES) & 1);
-        DBG(1, 11, step);
-        if (step) wait(sd_free, (step - 1) & 1);   // the elementwise pass has S^T / dP^T of the last step
-        DBG(1, 12, step);
+    if (warp == 1) {
+      for (int un = 0; un < pl.n_units; ++un) {
+        const int ni = bwd_ni(g, pl.kt[un]);
+        wait(kv_full, un & 1);
         sm100::tc_fence_after();
-        sd(st);
-        DBG(1, 13, step);
-        if (ii) grads(prev_st, ii == 1, step - 1);
-        prev_st = st;
+        for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
+          const int st = n % B_STAGES;
+          DBG(1, 10, step);
+          wait(&full[st], (n / B_STAGES) & 1);
+          DBG(1, 11, step);
+          if (step) wait(sd_free, (step - 1) & 1);   // the elementwise pass has S^T / dP^T of the last step
+          DBG(1, 12, step);
+          sm100::tc_fence_after();
+          const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
+            mma_ss_e(tS, dK_k + ka, dStg_k + so + kb, idSD, k != 0);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
+            mma_ss_e(tP, dV_k + ka, dStg_k + so + ((B_QTILE >> 4) + kb), idSD, k != 0);
+          }
+          commit_e(s_full);
+          DBG(1, 13, step);
+        }
       }
-      grads(prev_st, ni == 1, step - 1);
-      commit_e(acc_full);
-      commit_e(kv_free);
+    } else {
+      for (int un = 0; un < pl.n_units; ++un) {
+        const int ni = bwd_ni(g, pl.kt[un]);
+        wait(kv_full, un & 1);
+        if (un) wait(acc_free, (un - 1) & 1);   // the previous unit's dV / dK are written out
+        sm100::tc_fence_after();
+        for (int ii = 0; ii < ni; ++ii, ++n, ++step) {
+          const int st = n % B_STAGES;
+          const bool first = ii == 0;
+          wait(ds_full, step & 1);
+          sm100::tc_fence_after();
+          const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)   // dV += P^T dO
+            mma_ss_e(tmem, dP_a + ((k * 32) >> 4), dStg_mn + so + ((B_QTILE + k * 2048) >> 4), idVK, !first || k);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)   // dK += dS^T Q
+            mma_ss_e(tmem + 128, dDS_a + ((k * 32) >> 4), dStg_mn + so + ((k * 2048) >> 4), idVK, !first || k);
+          const int b = step & 1;
+          if (step >= 2) wait(&dq_free[b], ((step - 2) >> 1) & 1);
+          sm100::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)   // dQ^T = K^T dS^T
+            mma_ss_e(tmem + 384 + 64 * b, dK_mn + ((k * 2048) >> 4), dDS_b + ((k * 2048) >> 4), idQ, k != 0);
+          commit_e(pds_free);
+          commit_e(&dq_full[b]);
+          commit_e(&empty[st]);
+        }
+        commit_e(acc_full);
+        commit_e(kv_free);
+      }
     }
   } else if (warp >= 4 && warp < B_RD0) {
     // elementwise: thread = key row, B_EWC query columns of the sub-tile
