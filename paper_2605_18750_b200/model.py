@@ -467,8 +467,11 @@ class StageCompute:
         # ln_bwd_fused_kernel), the head's LN backward in one kernel; RRFP_LN_FUSED=0:
         # separate kernels
         self.ln_fused = os.environ.get("RRFP_LN_FUSED", "1") != "0" and D <= 4096
-        # FC1 bias gradient reduced in the FC2-dgrad GEMM epilogue (EPI_GELU_BWD + C2)
-        self.colsum_epi = os.environ.get("RRFP_COLSUM_EPI", "1") != "0"
+        # FC1 bias gradient reduced in the FC2-dgrad GEMM epilogue (EPI_GELU_BWD + C2):
+        # off by default -- the main-chain GEMM's epilogue got ~2.6 us/layer slower, more
+        # than the separate column-sum kernel costs on the side stream (B 12,207 vs
+        # 12,144 us per microbatch at PP=1); RRFP_COLSUM_EPI=1 selects it
+        self.colsum_epi = os.environ.get("RRFP_COLSUM_EPI", "0") == "1"
         self.attn_impl = os.environ.get("RRFP_ATTN", "cudnn_fe")
         self._sdpa = {}
         if self.attn_impl == "cudnn_fe" and nl:

@@ -43,6 +43,15 @@ def test_pipeline_model_on_host_twin():
             assert r["1f1b"]["ms"] > 0 and r["bf"]["speedup_vs_1f1b"] > 0.8
     # jitter makes every schedule slower
     assert out["pp8"]["sigma0.5"]["1f1b"]["ms"] > out["pp8"]["sigma0.0"]["1f1b"]["ms"]
+    # the (sigma x J-preset) operating grid at PP=8
+    g = half["pp8_grid"]
+    assert g["levels"] == ["J0", "J1", "J2", "J3"] and len(g["sigmas"]) == 6
+    for key in ("bfw_speedup", "bf_speedup", "bubble_1f1b", "bubble_bfw"):
+        assert all(len(g[key][j]) == 6 for j in g["levels"])
+    assert all(v > 0.9 for j in g["levels"] for v in g["bfw_speedup"][j])
+    assert all(g["bubble_bfw"][j][i] <= g["bubble_1f1b"][j][i] + 0.02 for j in g["levels"] for i in range(6))
+    assert all(g["bfw_speedup"][j][i] >= 1.5 for j, s in g["points_bfw_ge_1p5"]
+               for i in [g["sigmas"].index(s)])
 
 
 def test_dispatch_latency_from_trace():

@@ -100,3 +100,23 @@ def test_bench_two_ranks_end_to_end():
     for name in ("1f1b", "bf", "bfw"):
         for combo in ("J0+sigma0.0", "J0+sigma0.5", "J2+sigma0.5"):
             assert v[f"{name}@{combo}"]["ms"] > 0, (name, combo)
+
+
+def test_bench_emulated_pp_with_replay_prediction():
+    """The one-GPU PP emulation of the default bench (green-context partitions):
+    1F1B / BF / BFW at J0 and J2 with lognormal jitter, each variant carrying the
+    replay kernel's prediction from its own clean task times (model_ms); the
+    nominal times are measured without jitter, so the prediction tracks the
+    measurement."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--emulate-only", "--emulate-pp", "2", "--layers", "2",
+           "--mb", "4", "--steps", "1", "--warmup", "3", "--compare-jitter", "J0,J2", "--sigmas", "0.5"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]
+    res = json.loads(line[-1])
+    assert res["n_stages"] == 2 and res["jitter_time_scale"] > 1
+    for name in ("1f1b", "bf", "bfw"):
+        for combo in ("J0+sigma0.0", "J0+sigma0.5", "J2+sigma0.5"):
+            v = res["variants"][f"{name}@{combo}"]
+            assert v["ms"] > 0 and v["model_ms"] > 0, (name, combo, v)
+            assert abs(v["model_err"]) < 0.3, (name, combo, v)
