@@ -120,3 +120,24 @@ def test_bench_emulated_pp_with_replay_prediction():
             v = res["variants"][f"{name}@{combo}"]
             assert v["ms"] > 0 and v["model_ms"] > 0, (name, combo, v)
             assert abs(v["model_err"]) < 0.3, (name, combo, v)
+
+
+def test_bench_single_gpu_json_contract():
+    """The driver's N=1 command on a 2-layer model: one JSON line carrying the
+    contract keys (value, e2e with copied bytes, roofline with cuBLAS reference,
+    clocks, gpu_launches, dispatch with the step-kernel profile)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--layers", "2", "--mb", "4", "--steps", "2",
+           "--warmup", "3", "--emulate-pp", "0", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-3000:]
+    res = json.loads(line[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
+        assert k in res, k
+    assert res["n_gpus"] == 1 and res["warmup"] >= 3 and res["gpu_launches"] > 0
+    assert res["e2e"]["h2d_bytes_per_step"] > 0 and res["e2e"]["d2h_bytes_per_step"] > 0
+    r = res["roofline"]
+    assert r["bound"] == "tensor" and 0 < r["frac"] < 1 and len(r["cublas_per_gemm_tflops"]) == 12
+    assert res["dispatch"]["step_kernel"]["complete_us"]["n"] > 0
+    assert "pipeline_model" in res     # (a 2-layer model has too few units for PP=8: may carry "error")
