@@ -1,4 +1,4 @@
-"""Summarise an `ncu --set full` capture of tools/prof_gemm.py (the ten stage
+"""Summarise an `ncu --set full` capture of tools/prof_gemm.py (the twelve stage
 GEMMs of one layer, bench.py's roofline set) into profiles/gemm_traffic.json
 (bench.py's roofline.traffic) and a text table (dev tool).
 
@@ -11,9 +11,24 @@ NAMES = ["qkv fwd EPI_BF16 2048x6144x2048", "proj fwd EPI_RESID 2048x2048x2048",
          "fc1 fwd EPI_BIAS_GELU 2048x8192x2048", "fc2 fwd EPI_RESID 2048x2048x8192",
          "fc2 dgrad EPI_GELU_BWD 2048x8192x2048", "fc1 dgrad 2048x2048x8192", "qkv dgrad 2048x2048x6144",
          "fc2 wgrad EPI_ACC_F32 2048x8192x2048", "fc1 wgrad EPI_ACC_F32 8192x2048x2048",
-         "qkv wgrad EPI_ACC_F32 6144x2048x2048"]
-# algorithmic bytes: A + B read once (bf16), C written once (bf16; f32 accumulate: read + write)
-ALG_MB = [56, 32, 104, 80, 104, 80, 56, 112, 112, 84]
+         "qkv wgrad EPI_ACC_F32 6144x2048x2048", "proj dgrad 2048x2048x2048",
+         "proj wgrad EPI_ACC_F32 2048x2048x2048"]
+# algorithmic bytes (MB, 1e6): A + B read once (bf16), C written once (bf16; f32 accumulate:
+# read + write); the residual / pre-activation operand R of EPI_RESID / EPI_GELU_BWD read once
+_S, _D, _F = 2048, 2048, 8192
+_MB = lambda *elems: round(sum(elems) / 1e6, 1)
+ALG_MB = [_MB(2 * _S * _D, 2 * 3 * _D * _D, 2 * _S * 3 * _D),              # qkv fwd
+          _MB(2 * _S * _D, 2 * _D * _D, 2 * _S * _D, 2 * _S * _D),           # proj fwd + R
+          _MB(2 * _S * _D, 2 * _F * _D, 2 * 2 * _S * _F),                    # fc1 fwd (pre + act)
+          _MB(2 * _S * _F, 2 * _D * _F, 2 * _S * _D, 2 * _S * _D),           # fc2 fwd + R
+          _MB(2 * _S * _D, 2 * _D * _F, 2 * _S * _F, 2 * _S * _F),           # fc2 dgrad (+ pre)
+          _MB(2 * _S * _F, 2 * _F * _D, 2 * _S * _D),                        # fc1 dgrad
+          _MB(2 * _S * 3 * _D, 2 * 3 * _D * _D, 2 * _S * _D),                # qkv dgrad
+          _MB(2 * _S * _D, 2 * _S * _F, 8 * _D * _F),                        # fc2 wgrad f32 +=
+          _MB(2 * _S * _F, 2 * _S * _D, 8 * _F * _D),                        # fc1 wgrad f32 +=
+          _MB(2 * _S * 3 * _D, 2 * _S * _D, 8 * 3 * _D * _D),                # qkv wgrad f32 +=
+          _MB(2 * _S * _D, 2 * _D * _D, 2 * _S * _D),                        # proj dgrad
+          _MB(2 * _S * _D, 2 * _S * _D, 8 * _D * _D)]                        # proj wgrad f32 +=
 
 
 def main(rep, source):

@@ -1,5 +1,5 @@
-"""Run one layer's ten F/B/W stage GEMMs (bench.py's roofline set): 3 warm-up
-rounds, then one profiled round (for ncu --set full -k regex:gemm_bf16 -s 30 -c 10)."""
+"""Run one layer's twelve F/B/W stage GEMMs (bench.py's roofline set): 3 warm-up
+rounds, then one profiled round (for ncu --set full -k regex:gemm_bf16 -s 36 -c 12)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
