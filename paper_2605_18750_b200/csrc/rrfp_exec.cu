@@ -239,7 +239,7 @@ __device__ void build_view(lane_state* L, uint32_t* sF, uint32_t* sB, unsigned l
 // One record per evaluated arbitration: the exact inputs of rrfp_bp_update +
 // rrfp_arbitrate_core and the result (layout: include/rrfp_b200.h,
 // rrfp_runtime_declog).  Thread 0 only.
-__device__ void declog_put(lane_state* L, long long t, int mode_in, int focus_in, const uint32_t* fr,
+__device__ __noinline__ void declog_put(lane_state* L, long long t, int mode_in, int focus_in, const uint32_t* fr,
                            const uint32_t* br, const rrfp_decision& dec) {
   if (!L->declog) return;
   const int nw = L->nwords;
@@ -323,7 +323,7 @@ __device__ __forceinline__ uint32_t dec_code(const rrfp_decision& d) {
 // live._resolve_round 246-277): publish this rank's proposal into every
 // peer's board, gather all R (the same vector on every rank).  Returns the
 // sum of the proposers' arrival counts (free mode's retry snapshot).
-__device__ uint32_t tp_exchange(lane_state* L, const rrfp_decision& dec, rrfp_decision* ds) {
+__device__ __noinline__ uint32_t tp_exchange(lane_state* L, const rrfp_decision& dec, rrfp_decision* ds) {
   const rrfp_lane_desc& d = L->d;
   const int R = d.R;
   unsigned long long round = ++L->tp_round;
@@ -471,7 +471,7 @@ __device__ void lane_dispatch(lane_state* L) {
 // commute (no dispatch happens while it is busy), so a lane applies its
 // completion as soon as the body has run and its arrivals tick by tick.
 
-__device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end);
+__device__ __noinline__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end);
 
 __device__ __forceinline__ long long v_min(long long a, long long b) { return a < b ? a : b; }
 __device__ __forceinline__ long long v_max(long long a, long long b) { return a > b ? a : b; }
@@ -678,7 +678,7 @@ __device__ int v_dispatch(lane_state* L, long long T) {
 // The replay-mode step: complete the body that just ran, then advance the
 // virtual clock tick by tick until this lane commits its next task (SWITCH
 // branch set) or finishes (WHILE ends).
-__device__ void lane_virtual(lane_state* L) {
+__device__ __noinline__ void lane_virtual(lane_state* L) {
   __shared__ long long s_T;
   __shared__ int s_state;           // 0 wait, 1 process s_T, 2 exit
   __shared__ int s_kind;
@@ -769,7 +769,7 @@ __global__ void lane_spin_body_kernel(lane_state* L) {
 }
 
 // ---------------------------------------------------------------- complete
-__device__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end) {
+__device__ __noinline__ void lane_send(lane_state* L, int dir, int mb, int c, unsigned long long end) {
   const rrfp_lane_desc& d = L->d;
   int dst_c, dst_s;
   lane_inbox* const* dsts;
