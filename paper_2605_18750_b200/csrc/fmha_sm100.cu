@@ -103,6 +103,61 @@ __device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint6
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// N = 4 or 8 SS MMAs of one product (K = 16 N) in ONE asm block: one elect, the
+// descriptor bases moved to uniform registers once, per-k offsets as immediates
+// ((k / 4) * P + (k % 4) * S, in 16-byte units).  mma_ss_e per instruction costs
+// ~11 SASS (R2UR / ELECT / VOTEU per MMA): ~50 issue cycles each in the backward.
+template <int SA, int PA, int SB, int PB>
+__device__ __forceinline__ void mma_ss_x8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, q, e;\n"
+      ".reg .b64 ra, rb;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.u32 q, 0, 0;\n"
+      "add.s64 ra, %1, %5;  add.s64 rb, %2, %13;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p;\n"
+      "add.s64 ra, %1, %6;  add.s64 rb, %2, %14;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %7;  add.s64 rb, %2, %15;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %8;  add.s64 rb, %2, %16;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %9;  add.s64 rb, %2, %17;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %10; add.s64 rb, %2, %18;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %11; add.s64 rb, %2, %19;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %12; add.s64 rb, %2, %20;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "}\n" ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate),
+      "n"(0), "n"(SA), "n"(2 * SA), "n"(3 * SA), "n"(PA), "n"(PA + SA), "n"(PA + 2 * SA), "n"(PA + 3 * SA),
+      "n"(0), "n"(SB), "n"(2 * SB), "n"(3 * SB), "n"(PB), "n"(PB + SB), "n"(PB + 2 * SB), "n"(PB + 3 * SB));
+}
+template <int SA, int SB>
+__device__ __forceinline__ void mma_ss_x4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, q, e;\n"
+      ".reg .b64 ra, rb;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.u32 q, 0, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "add.s64 ra, %1, %5;  add.s64 rb, %2, %8;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %6;  add.s64 rb, %2, %9;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "add.s64 ra, %1, %7;  add.s64 rb, %2, %10;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, q;\n"
+      "}\n" ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate),
+      "n"(SA), "n"(2 * SA), "n"(3 * SA), "n"(SB), "n"(2 * SB), "n"(3 * SB));
+}
+
 __device__ __forceinline__ void commit_e(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -731,16 +786,9 @@ __global__ void __launch_bounds__(B_THREADS, 1)
           DBG(1, 12, step);
           sm100::tc_fence_after();
           const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
-            mma_ss_e(tS, dK_k + ka, dStg_k + so + kb, idSD, k != 0);
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t ka = ((k >> 2) * PANEL + (k & 3) * 32) >> 4, kb = ((k >> 2) * (B_QTILE / 2) + (k & 3) * 32) >> 4;
-            mma_ss_e(tP, dV_k + ka, dStg_k + so + ((B_QTILE >> 4) + kb), idSD, k != 0);
-          }
+          // (k-block offsets: K-major panels of 128 rows (A) / 64 rows (B), 32 B per k16)
+          mma_ss_x8<2, (PANEL >> 4), 2, ((B_QTILE / 2) >> 4)>(tS, dK_k, dStg_k + so, idSD, 0);
+          mma_ss_x8<2, (PANEL >> 4), 2, ((B_QTILE / 2) >> 4)>(tP, dV_k, dStg_k + so + (B_QTILE >> 4), idSD, 0);
           commit_e(s_full);
           DBG(1, 13, step);
         }
@@ -757,18 +805,14 @@ __global__ void __launch_bounds__(B_THREADS, 1)
           wait(ds_full, step & 1);
           sm100::tc_fence_after();
           const uint64_t so = (uint64_t)((st * B_STAGE) >> 4);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)   // dV += P^T dO
-            mma_ss_e(tmem, dP_a + ((k * 32) >> 4), dStg_mn + so + ((B_QTILE + k * 2048) >> 4), idVK, !first || k);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)   // dK += dS^T Q
-            mma_ss_e(tmem + 128, dDS_a + ((k * 32) >> 4), dStg_mn + so + ((k * 2048) >> 4), idVK, !first || k);
+          // dV += P^T dO, dK += dS^T Q  (A K-major: 32 B per k16; B MN-major: 16 rows x 128 B per k16)
+          mma_ss_x4<2, 128>(tmem, dP_a, dStg_mn + so + (B_QTILE >> 4), idVK, !first);
+          mma_ss_x4<2, 128>(tmem + 128, dDS_a, dStg_mn + so, idVK, !first);
           const int b = step & 1;
           if (step >= 2) wait(&dq_free[b], ((step - 2) >> 1) & 1);
           sm100::tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k)   // dQ^T = K^T dS^T
-            mma_ss_e(tmem + 384 + 64 * b, dK_mn + ((k * 2048) >> 4), dDS_b + ((k * 2048) >> 4), idQ, k != 0);
+          // dQ^T = K^T dS^T (both MN-major: 16 rows x 128 B per k16)
+          mma_ss_x8<128, 512, 128, 512>(tmem + 384 + 64 * b, dK_mn, dDS_b, idQ, 0);
           commit_e(pds_free);
           commit_e(&dq_full[b]);
           commit_e(&empty[st]);
