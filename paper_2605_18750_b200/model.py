@@ -462,11 +462,14 @@ class StageCompute:
         # attention core: cuDNN SDPA through the frontend graph API (attention.py) reading
         # the packed QKV and writing O / stats / packed dQKV into our own slots;
         # RRFP_ATTN=torch selects the aten op (separate dQ/dK/dV, copied in)
-        # LayerNorm parameter gradients fused with the adjacent bias gradients (column
-        # sums of the residual gradients) in one side-stream pass (ops.cu
-        # ln_bwd_fused_kernel), the head's LN backward in one kernel; RRFP_LN_FUSED=0:
-        # separate kernels
-        self.ln_fused = os.environ.get("RRFP_LN_FUSED", "1") != "0" and D <= 4096
+        # RRFP_LN_FUSED=1: LayerNorm parameter gradients fused with the adjacent bias
+        # gradients (column sums of the residual gradients) in one side-stream pass
+        # (ops.cu ln_bwd_fused_kernel), the head's LN backward in one kernel.
+        # Off by default: alone the fused pass takes 8.8 us against 15.6 for the two kernels
+        # it replaces (tools/ln_bench.py), but inside the task bodies the separate, smaller
+        # kernels fill the weight-gradient GEMMs' tails better: W 118.5 vs 124.5 us/layer,
+        # fused B 390.7 vs 394.2 (tools/task_times.py 9 [bfw], same box, interleaved)
+        self.ln_fused = os.environ.get("RRFP_LN_FUSED", "0") == "1" and D <= 4096
         # FC1 bias gradient reduced in the FC2-dgrad GEMM epilogue (EPI_GELU_BWD + C2):
         # off by default -- the main-chain GEMM's epilogue got ~2.6 us/layer slower, more
         # than the separate column-sum kernel costs on the side stream (B 12,207 vs
