@@ -281,3 +281,27 @@ def test_pipeline_with_own_attention_backward(monkeypatch):
         assert not bad, bad[:5]
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("hint", ["bf", "bfw"])
+def test_pipeline_with_opt_in_fusions(monkeypatch, hint):
+    """The opt-in fusions inside the captured bodies: the one-pass LayerNorm
+    reductions (RRFP_LN_FUSED=1: LN parameter + adjacent bias gradients) and the
+    FC1 bias gradient in the FC2-dgrad epilogue (RRFP_COLSUM_EPI=1), fused B and
+    BFW; the default LM-head statistics epilogue is on in both."""
+    monkeypatch.setenv("RRFP_LN_FUSED", "1")
+    monkeypatch.setenv("RRFP_COLSUM_EPI", "1")
+    from paper_2605_18750_b200.pipeline import GpuPipeline
+    cfg = _cfg()
+    pipe = GpuPipeline(cfg, 2, 4, hint=hint, mode="free")
+    try:
+        assert all(st.ln_fused and st.colsum_epi for st in pipe.stages)
+        assert pipe.stages[-1].ce_fused
+        for _ in range(2):
+            loss = pipe.step(watchdog_secs=60).item()
+        ref_loss, ref_grads = reference_loss_and_grads(cfg, pipe.stages)
+        assert abs(loss - ref_loss) / ref_loss < 1e-2, (loss, ref_loss)
+        bad = compare(ref_grads, device_grads(pipe.stages))
+        assert not bad, bad[:5]
+    finally:
+        pipe.close()
