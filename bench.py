@@ -523,6 +523,20 @@ def run_ours(args):
         lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
         line["emulated_pp"] = json.loads(lines[-1]) if (p.returncode == 0 and lines) else \
             {"error": f"rc={p.returncode}: {p.stderr[-300:]}"}
+        # the smaller pipelines of the PP sweep (BASELINE metric: PP=2/4/8), J0 and the first
+        # sigma only, one fresh process each
+        extra = {}
+        for n_pp in [int(x) for x in args.emulate_pp_extra.split(",") if x and int(x) != args.emulate_pp]:
+            cmd2 = list(cmd)
+            cmd2[cmd2.index("--emulate-pp") + 1] = str(n_pp)
+            cmd2[cmd2.index("--compare-jitter") + 1] = args.compare_jitter.split(",")[0]
+            p = subprocess.run(cmd2, capture_output=True, text=True)
+            sys.stderr.write(p.stderr[-2000:])
+            lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+            extra[f"pp{n_pp}"] = json.loads(lines[-1]) if (p.returncode == 0 and lines) else \
+                {"error": f"rc={p.returncode}: {p.stderr[-300:]}"}
+        if extra:
+            line["emulated_pp_sweep"] = extra
     if args.compare or (world > 1 and args.compare is None):
         line["variants"] = compare_variants(cfg, args, world, dist, barrier)
     if rank == 0:
@@ -1115,6 +1129,8 @@ def main():
     ap.add_argument("--emulate-pp", dest="emulate_pp", type=int, default=8,
                     help="(1 GPU) also run an emulated PP=N pipeline: N lanes, GEMMs on 148/N SMs each, "
                          "1F1B vs BF vs BFW at every --sigmas (default 8; 0 = off)")
+    ap.add_argument("--emulate-pp-extra", dest="emulate_pp_extra", default="2,4",
+                    help="(1 GPU) further emulated pipeline depths, J0 jitter only (default 2,4; '' = none)")
     ap.add_argument("--dry-run", dest="dry_run", action="store_true",
                     help="resolve the launch (re-exec under torchrun for --gpus N > 1, rendezvous) and "
                          "print the plan; no CUDA")
