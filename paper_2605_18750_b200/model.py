@@ -533,11 +533,19 @@ class StageCompute:
     def connect_outputs(self, fwd_out=None, bwd_out=None):
         """fwd_out / bwd_out: per-mb destination (tensor or RawBuffer) in the
         next / previous stage's mailbox, or per-mb LISTS of destinations (one per
-        TP rank of the neighbour stage: every sender rank writes every receiver
-        rank's slot -- identical bytes -- before raising its flags)."""
+        TP rank of the neighbour stage; a TP rank keeps only its own rank's)."""
         as_list = lambda v: v if isinstance(v, (list, tuple)) else [v]
-        self.fwd_out = [as_list(v) for v in fwd_out] if fwd_out is not None else None
-        self.bwd_out = [as_list(v) for v in bwd_out] if bwd_out is not None else None
+
+        def own_rank(lst):
+            # the R ranks of a TP group hold bit-identical activations / input gradients
+            # after the all-reduce (partials summed in rank order), so rank r feeds only
+            # the neighbour's rank r (whose flag it raises anyway): half the NVLink
+            # bytes of writing every receiver rank at TP=2 (RRFP_TP_ALL_RECEIVERS=1: all)
+            if self.R > 1 and len(lst) == self.R and os.environ.get("RRFP_TP_ALL_RECEIVERS", "0") != "1":
+                return [lst[self.tp_rank]]
+            return lst
+        self.fwd_out = [own_rank(as_list(v)) for v in fwd_out] if fwd_out is not None else None
+        self.bwd_out = [own_rank(as_list(v)) for v in bwd_out] if bwd_out is not None else None
 
     def param_bytes(self):
         return sum(t.numel() * 2 for p in self.p for t in p.values())
