@@ -453,9 +453,9 @@ def run_ours(args):
     it_flops = iteration_flops(args, cfg)
     n_dev = max(1, world)
     act = cfg.seq * cfg.d_model * 2
-    # per GPU: mailbox writes (F out + B out, one copy per receiving TP rank) and
+    # per GPU: mailbox writes (F out + B out, to the same TP rank of the neighbour) and
     # TP all-reduce peer reads (4 per layer per microbatch, R-1 partials each)
-    p2p = (2 * args.mb * act * args.tp if n > 1 else 0) + \
+    p2p = (2 * args.mb * act if n > 1 else 0) + \
         4 * (cfg.n_layer // n) * args.mb * act * (args.tp - 1)
     t_roof = it_flops / (n_dev * peak_sus * 1e12) + p2p / 770e9
     launches = pipe.kernel_launches_per_step() if hasattr(pipe, "kernel_launches_per_step") else 0
